@@ -1,0 +1,193 @@
+/*
+ * pdd.h -- C ABI of libpdd: the B200 (sm_100a) hot path of the patchy domain decomposition
+ * method for stationary second-order HJB equations, arXiv 1502.01629.
+ *
+ * Citations: P:<line> = the paper's LaTeX source, R<k> = a reading of the paper
+ * listed in DESIGN.md section "Readings".
+ *
+ * The calls follow the paper's algorithm:
+ *   Initialization   pdd_create          grid G, coarse grid G_c, controls, data
+ *   Pre-computation  pdd_coarse_solve    u_c on G_c, sigma = 0, until eps_c
+ *                    pdd_synthesize      u_hat = interp(u_c) on G, feedback a*        P:826-827
+ *                    pdd_build_patches   split of the Dirichlet set + patches
+ *                    pdd_build_static    static equal-square decomposition (DD)
+ *   Computation      pdd_solve           patch-parallel fine solve until eps
+ *                    pdd_get_*           fetch V, a*, labels, u_hat, u_c
+ *
+ * The scheme (P:366-375 with the self-dependency removal P:433-491, discounted as in
+ * BASELINE.json, R1-R3): for a free node x_i,
+ *   V(x_i) = min_k ( h l(x_i) + beta R'_k ) / ( 1 - beta Lambda0_k ),  beta = 1/(1 + lambda h),
+ * foot points x_i + h f(x_i, a_k) +- sqrt(h p) sigma_j(x_i) (j < p; one foot point when p = 0),
+ * f(x, a) = c(x) a + d(x); R'_k / Lambda0_k = branch-averaged bilinear weight of the corners
+ * other than x_i / of x_i itself; feet are clamped to the box (R5).  Target nodes hold V = 0,
+ * obstacle nodes V = 1/lambda (R8).
+ *
+ * Conventions
+ *   - Grid: n nodes per axis on [lo, hi]^2, dx = (hi - lo)/(n - 1), node (i, j) at
+ *     (lo + i dx, lo + j dx), linear index j*n + i (x fastest), row-major.
+ *   - All host arrays passed to pdd_create are COPIED to the device inside the call; the caller
+ *     keeps ownership and may free them when the call returns.
+ *   - The device workspace is owned by the caller (e.g. a PyTorch uint8 tensor) and must stay
+ *     alive until pdd_destroy.  libpdd never calls cudaMalloc.
+ *   - Every call enqueues its work on the stream given to pdd_create and synchronises that
+ *     stream before returning, so returned statistics and fetched arrays are final.
+ *   - Errors: every call returns a pdd_status; the message is in pdd_last_error(ctx)
+ *     (pdd_last_error(NULL) for pdd_create / pdd_workspace_bytes failures).  No C++ exception
+ *     crosses the ABI.  On PDD_E_CUDA the context must be destroyed.
+ */
+#ifndef PDD_H
+#define PDD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    PDD_OK = 0,
+    PDD_E_INVALID = 1,    /* bad argument: n < 3, hi <= lo, N_A outside 1..128, p outside 0..2,
+                             lambda <= 0, l <= 0, sizes that do not nest, NULL pointers */
+    PDD_E_NOCONVERGE = 2, /* max rounds / sweeps reached; values stay fetchable */
+    PDD_E_IO = 3,         /* reserved */
+    PDD_E_CUDA = 4,       /* a CUDA call failed; see pdd_last_error */
+    PDD_E_STATE = 5,      /* call out of order (e.g. synthesize before coarse_solve) */
+    PDD_E_NOMEM = 6,      /* workspace smaller than pdd_workspace_bytes */
+    PDD_E_STENCIL = 7     /* foot points reach farther than the tile halo supports (R4) */
+} pdd_status;
+
+typedef enum {
+    PDD_COEF_CONST = 0,   /* value                                   */
+    PDD_COEF_ROW = 1,     /* data[j], depends on x2 only (n values)   */
+    PDD_COEF_COL = 2,     /* data[i], depends on x1 only (n values)   */
+    PDD_COEF_FIELD = 3    /* data[j*n + i] (n*n values)                */
+} pdd_coef_kind;
+
+/* A coefficient of the problem (Eq. HJB2). data: host pointer, fp64. */
+typedef struct {
+    int32_t kind;
+    double value;
+    const double *data;
+} pdd_coef;
+
+/* One discretised problem on one grid (fine G or coarse G_c).  All pointers are HOST pointers. */
+typedef struct {
+    int32_t n;              /* nodes per axis, >= 3                                         */
+    double lo, hi;          /* square box [lo, hi]^2                                        */
+    double dx;              /* (hi - lo)/(n - 1), given explicitly (both sides use this value) */
+    double h;               /* time step of the SL scheme (R13: h = dx in BASELINE configs) */
+    double lambda;          /* discount > 0; beta = 1/(1 + lambda h)                        */
+    int32_t n_controls;     /* N_A, 1..128                                      */
+    const double *controls; /* 2*N_A values (a1, a2) per control                            */
+    pdd_coef speed;         /* c(x)                                                         */
+    pdd_coef drift[2];      /* d(x) = (d1, d2)                                              */
+    int32_t p;              /* noise columns 0..2; 2p Markov branches (1 foot when p = 0)  */
+    pdd_coef sigma[2][2];   /* sigma_j(x) component c = sigma[j][c]                          */
+    pdd_coef cost;          /* l(x) > 0                                                     */
+    int32_t diffusion_scale;/* 0: sqrt(h p) (north star), 1: sqrt(h)                */
+    const uint8_t *kind;    /* n*n: 0 free, 1 target (V = 0), 2 obstacle (V = 1/lambda)     */
+    const int16_t *sector;  /* n*n: Gamma_p id of target nodes (R17), ignored elsewhere; may be
+                               NULL on the coarse grid or when no patches are built           */
+} pdd_problem;
+
+typedef struct pdd_ctx pdd_ctx;
+
+/* Fine solve options (pdd_solve). */
+typedef struct {
+    int32_t mode;        /* 0 patchy: V starts at u_hat, tiles activated in ascending u_hat
+                            order; 1 static: V starts at V0 (R11)         */
+    int32_t k_inner;     /* relaxation sweeps per tile visit (>= 1; chaotic relaxation)      */
+    double tol;          /* sup-norm residual tolerance eps                                  */
+    int64_t max_rounds;  /* cap on tile rounds                                               */
+    double delta;        /* patchy bucket width in value units; 0 = automatic; < 0 = off      */
+    int32_t kernel;      /* 0 auto, 1 general stencil, 2 row-table stencil                   */
+    int32_t reserved[3];
+} pdd_solve_opts;
+
+typedef struct {
+    int64_t rounds;            /* tile rounds, including verification passes   */
+    int64_t node_updates;      /* free-node updates performed by the sweep kernel           */
+    int64_t tiles_processed;
+    int64_t verify_passes;
+    double final_residual;     /* last full-grid Jacobi residual ||T(V) - V||_inf            */
+    double apost_bound;        /* final_residual / (1 - beta): bound on ||V - V*||_inf       */
+    double seconds_total;      /* wall time of pdd_solve on the stream (CUDA events)        */
+    double seconds_sweep;      /* summed duration of the sweep-kernel launches              */
+    double seconds_verify;
+    int32_t converged;
+    int32_t n_tiles;
+    int32_t kernel_used;       /* 1 general, 2 row-table                                    */
+    int32_t patches_converged; /* patches with no active tile at the end                    */
+} pdd_solve_stats;
+
+typedef struct {
+    int64_t sweeps;       /* Jacobi sweeps including the final check sweep                 */
+    double residual;      /* residual of the last sweep                                    */
+    double seconds;
+    int32_t converged;
+    int32_t reserved;
+} pdd_coarse_stats;
+
+const char *pdd_version(void);
+
+/* Bytes of device workspace pdd_create needs for this (fine, coarse) pair at this precision
+ * (32 or 64: the arithmetic of the fine sweep; V is stored in fp64 in both).  coarse may be NULL. */
+pdd_status pdd_workspace_bytes(const pdd_problem *fine, const pdd_problem *coarse,
+                               int32_t precision, size_t *bytes);
+
+/* Validate the problem, carve the workspace, copy every input array to the device.
+ * stream: a cudaStream_t (NULL = legacy default stream).  device_workspace: >= the size
+ * reported by pdd_workspace_bytes, 256-byte aligned. */
+pdd_status pdd_create(const pdd_problem *fine, const pdd_problem *coarse, int32_t precision,
+                      void *stream, void *device_workspace, size_t workspace_bytes,
+                      pdd_ctx **out);
+
+/* u_c: Jacobi fixed point of the scheme with sigma = 0 on G_c from V0, stopped at the first
+ * sweep whose residual is < tol_c (R14).  Canonical fp64 arithmetic (R30), so u_c
+ * is bit-identical to any IEEE implementation of the same expressions.  Needs a coarse problem. */
+pdd_status pdd_coarse_solve(pdd_ctx *ctx, double tol_c, int64_t max_sweeps, pdd_coarse_stats *st);
+
+/* u_hat = bilinear(u_c) on G (R15) and a*(x_i) = argmin_k [h l + beta u_hat(x_i +
+ * h f(x_i, a_k))], lowest k on ties (R16).  Canonical fp64. */
+pdd_status pdd_synthesize(pdd_ctx *ctx);
+
+/* Patch labels (R17, R18): successor s(i) = nearest node to x_i + M f* / |f*| (cells), pointer
+ * jumping to the root of every successor chain; label = sector[root] when the root is a target
+ * node, n_patches (orphan) otherwise; -1 on target nodes, -2 on obstacles.  M = 0 => 4. */
+pdd_status pdd_build_patches(pdd_ctx *ctx, int32_t n_patches, double M);
+
+/* Static equal squares: px columns x py rows, boundaries floor(k n / P) (R19). */
+pdd_status pdd_build_static(pdd_ctx *ctx, int32_t px, int32_t py);
+
+/* The fine solve: rounds of the tile sweep kernel over the active tile list until every tile
+ * is converged, then a full-grid Jacobi verification; re-activates and continues
+ * while the verification residual is >= tol.  mode 0 needs pdd_synthesize and pdd_build_patches,
+ * mode 1 needs pdd_build_static. */
+pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *opts, pdd_solve_stats *st);
+
+/* One application of the operator: out = T(V) on every node (Dirichlet nodes copy V), fp64
+ * output, arithmetic of the context's precision; *residual = max |T(V) - V| over free nodes.
+ * out: DEVICE memory (n*n doubles) or NULL (residual only).  kernel: as pdd_solve_opts.kernel. */
+pdd_status pdd_apply_operator(pdd_ctx *ctx, double *out, int32_t kernel, double *residual);
+
+/* Fetch / set arrays (n*n unless noted).  *_on_device selects device (1) or host (0) memory. */
+pdd_status pdd_get_values(pdd_ctx *ctx, void *dst, int32_t dst_on_device, int32_t as_fp64);
+pdd_status pdd_set_values(pdd_ctx *ctx, const double *src, int32_t src_on_device);
+pdd_status pdd_get_uhat(pdd_ctx *ctx, double *dst, int32_t dst_on_device);
+pdd_status pdd_get_coarse_values(pdd_ctx *ctx, double *dst, int32_t dst_on_device); /* n_c^2 */
+pdd_status pdd_get_controls(pdd_ctx *ctx, uint8_t *dst, int32_t dst_on_device);  /* 255: Dirichlet */
+pdd_status pdd_get_labels(pdd_ctx *ctx, int16_t *dst, int32_t dst_on_device);
+pdd_status pdd_get_successors(pdd_ctx *ctx, int32_t *dst, int32_t dst_on_device);
+
+/* Per-patch convergence report of the last pdd_solve: round index at which each patch last had
+ * an active tile (n_patches + 1 entries, the last one for orphans). */
+pdd_status pdd_get_patch_rounds(pdd_ctx *ctx, int32_t *dst, int32_t count);
+
+const char *pdd_last_error(const pdd_ctx *ctx);
+void pdd_destroy(pdd_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PDD_H */

@@ -1,0 +1,310 @@
+// canonical.cu -- the decision stages of the pre-computation on sm_100a.
+//
+// Their integer outputs (a*, labels) must be bit-exact with any IEEE-754 evaluation of the same
+// expressions, so this translation unit is compiled with --fmad=false and every fp64 operation
+// is written with an explicit round-to-nearest intrinsic in the order fixed by DESIGN.md
+// reading R30 ("canonical arithmetic"):
+//   f = c a + d;  b = q f;  g = i + b;  clamp g to [0, n-1];  cell = min(floor g, n-2);
+//   t = g - cell;  w00 = (1-tx)(1-ty), w10 = tx(1-ty), w01 = (1-tx)ty, w11 = tx ty;
+//   sums in corner order 00, 10, 01, 11.
+//
+// Kernels (one thread per node unless noted):
+//   k_init_values   V0 on free nodes, Dirichlet values (R8, R11)
+//   k_coarse_sweep  one Jacobi sweep of the sigma = 0 scheme on G_c (SLscheme3
+//                   P:473-491 with discount R3) + sup-norm residual; stops itself once the
+//                   previous sweep's residual is < tol (so the result does not depend on how
+//                   many sweeps the host enqueues)
+//   k_prolong       u_hat = bilinear(u_c) (R15)
+//   k_synthesize    a* = argmin_k [h l + beta u_hat(x + h f)] (R16)
+//   k_successor     nearest node to x + M f*/|f*| (R18)
+//   k_jump          pointer jumping s <- s[s]
+//   k_labels        label = sector[root] for target roots, orphan otherwise (R17)
+//   k_static_labels equal squares (R19)
+#include "pdd_internal.cuh"
+
+#include <math.h>
+
+namespace pdd {
+
+#define DADD(a, b) __dadd_rn((a), (b))
+#define DSUB(a, b) __dsub_rn((a), (b))
+#define DMUL(a, b) __dmul_rn((a), (b))
+#define DDIV(a, b) __ddiv_rn((a), (b))
+
+// bilinear stencil at (gx, gy) in node units (clamped), corners 00, 10, 01, 11
+__device__ __forceinline__ void canon_stencil(int n, double gx, double gy, int64_t cr[4],
+                                              double wg[4])
+{
+    const double top = (double)(n - 1);
+    if (gx < 0.0) gx = 0.0;
+    if (gx > top) gx = top;
+    if (gy < 0.0) gy = 0.0;
+    if (gy > top) gy = top;
+    int cx = (int)floor(gx), cy = (int)floor(gy);
+    if (cx > n - 2) cx = n - 2;
+    if (cy > n - 2) cy = n - 2;
+    const double tx = DSUB(gx, (double)cx);
+    const double ty = DSUB(gy, (double)cy);
+    const double ux = DSUB(1.0, tx), uy = DSUB(1.0, ty);
+    wg[0] = DMUL(ux, uy);
+    wg[1] = DMUL(tx, uy);
+    wg[2] = DMUL(ux, ty);
+    wg[3] = DMUL(tx, ty);
+    cr[0] = (int64_t)cy * n + cx;
+    cr[1] = cr[0] + 1;
+    cr[2] = cr[0] + n;
+    cr[3] = cr[0] + n + 1;
+}
+
+__global__ void k_init_values(DProblem P, double *V)
+{
+    const int64_t N = (int64_t)P.n * P.n;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < N;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const uint8_t kd = P.kind[k];
+        V[k] = kd == 0 ? P.v0 : (kd == 1 ? 0.0 : DDIV(1.0, P.lambda));
+    }
+}
+
+// sigma = 0 node update of the modified scheme (one foot point, w = 1)
+__device__ double canon_node_update(const DProblem &P, const double *V, int i, int j)
+{
+    const int n = P.n;
+    const int64_t self = (int64_t)j * n + i;
+    const double c = coef_at(P.speed, i, j, n);
+    const double d1 = coef_at(P.drift[0], i, j, n);
+    const double d2 = coef_at(P.drift[1], i, j, n);
+    const double l = coef_at(P.cost, i, j, n);
+    const double hl = DMUL(P.h, l);
+    double best = INFINITY;
+    for (int a = 0; a < P.na; ++a) {
+        const double f1 = DADD(DMUL(c, P.ctrl[2 * a]), d1);
+        const double f2 = DADD(DMUL(c, P.ctrl[2 * a + 1]), d2);
+        const double gx = DADD((double)i, DMUL(P.q, f1));
+        const double gy = DADD((double)j, DMUL(P.q, f2));
+        int64_t cr[4];
+        double wg[4];
+        canon_stencil(n, gx, gy, cr, wg);
+        double lam0 = 0.0, rp = 0.0;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            if (cr[t] == self) lam0 = DADD(lam0, wg[t]);
+            else rp = DADD(rp, DMUL(wg[t], V[cr[t]]));
+        }
+        const double v = DDIV(DADD(hl, DMUL(P.beta, rp)), DSUB(1.0, DMUL(P.beta, lam0)));
+        if (v < best) best = v;
+    }
+    return best;
+}
+
+__global__ void k_coarse_sweep(DProblem P, const double *__restrict__ Vin, double *__restrict__ Vout,
+                               double tol, unsigned long long *res_hist, int sweep,
+                               int *sweeps_done)
+{
+    // stop once the previous sweep has converged: Vout keeps nothing new, the converged
+    // iterate stays in the buffer written by sweep (sweeps_done - 1)
+    if (sweep > 0 && __longlong_as_double((long long)res_hist[sweep - 1]) < tol) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(sweeps_done, 1);
+    const int n = P.n;
+    const int64_t N = (int64_t)n * n;
+    double res = 0.0;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < N;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        if (P.kind[k] != 0) { Vout[k] = Vin[k]; continue; }
+        const double v = canon_node_update(P, Vin, (int)(k % n), (int)(k / n));
+        Vout[k] = v;
+        const double d = fabs(DSUB(v, Vin[k]));
+        if (d > res) res = d;
+    }
+    // non-negative doubles order like their bit patterns
+    for (int o = 16; o > 0; o >>= 1) res = fmax(res, __shfl_xor_sync(0xffffffffu, res, o));
+    if ((threadIdx.x & 31) == 0 && res > 0.0)
+        atomicMax(&res_hist[sweep], (unsigned long long)__double_as_longlong(res));
+}
+
+__global__ void k_prolong(int nc, const double *__restrict__ uc, int n, int r, double *__restrict__ out)
+{
+    const int64_t N = (int64_t)n * n;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < N;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(k % n), j = (int)(k / n);
+        int I = i / r, J = j / r;
+        if (I > nc - 2) I = nc - 2;
+        if (J > nc - 2) J = nc - 2;
+        const double tx = DDIV((double)(i - I * r), (double)r);
+        const double ty = DDIV((double)(j - J * r), (double)r);
+        const double w00 = DMUL(DSUB(1.0, tx), DSUB(1.0, ty)), w10 = DMUL(tx, DSUB(1.0, ty));
+        const double w01 = DMUL(DSUB(1.0, tx), ty), w11 = DMUL(tx, ty);
+        const int64_t b = (int64_t)J * nc + I;
+        double s = DMUL(w00, uc[b]);
+        s = DADD(s, DMUL(w10, uc[b + 1]));
+        s = DADD(s, DMUL(w01, uc[b + nc]));
+        s = DADD(s, DMUL(w11, uc[b + nc + 1]));
+        out[k] = s;
+    }
+}
+
+__global__ void k_synthesize(DProblem P, const double *__restrict__ uhat, uint8_t *__restrict__ astar)
+{
+    const int n = P.n;
+    const int64_t N = (int64_t)n * n;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < N;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        if (P.kind[k] != 0) { astar[k] = 255; continue; }
+        const int i = (int)(k % n), j = (int)(k / n);
+        const double c = coef_at(P.speed, i, j, n);
+        const double d1 = coef_at(P.drift[0], i, j, n);
+        const double d2 = coef_at(P.drift[1], i, j, n);
+        const double hl = DMUL(P.h, coef_at(P.cost, i, j, n));
+        double best = INFINITY;
+        int arg = -1;
+        for (int a = 0; a < P.na; ++a) {
+            const double f1 = DADD(DMUL(c, P.ctrl[2 * a]), d1);
+            const double f2 = DADD(DMUL(c, P.ctrl[2 * a + 1]), d2);
+            const double gx = DADD((double)i, DMUL(P.q, f1));
+            const double gy = DADD((double)j, DMUL(P.q, f2));
+            int64_t cr[4];
+            double wg[4];
+            canon_stencil(n, gx, gy, cr, wg);
+            double s = DMUL(wg[0], uhat[cr[0]]);
+            s = DADD(s, DMUL(wg[1], uhat[cr[1]]));
+            s = DADD(s, DMUL(wg[2], uhat[cr[2]]));
+            s = DADD(s, DMUL(wg[3], uhat[cr[3]]));
+            const double v = DADD(hl, DMUL(P.beta, s));
+            if (v < best) { best = v; arg = a; }
+        }
+        astar[k] = (uint8_t)arg;
+    }
+}
+
+__global__ void k_successor(DProblem P, double M, const uint8_t *__restrict__ astar,
+                            int32_t *__restrict__ succ)
+{
+    const int n = P.n;
+    const int64_t N = (int64_t)n * n;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < N;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        if (P.kind[k] != 0) { succ[k] = (int32_t)k; continue; }
+        const int i = (int)(k % n), j = (int)(k / n);
+        const int a = astar[k];
+        const double c = coef_at(P.speed, i, j, n);
+        const double f1 = DADD(DMUL(c, P.ctrl[2 * a]), coef_at(P.drift[0], i, j, n));
+        const double f2 = DADD(DMUL(c, P.ctrl[2 * a + 1]), coef_at(P.drift[1], i, j, n));
+        const double nrm = __dsqrt_rn(DADD(DMUL(f1, f1), DMUL(f2, f2)));
+        if (nrm == 0.0) { succ[k] = (int32_t)k; continue; }
+        const double u1 = DDIV(f1, nrm), u2 = DDIV(f2, nrm);
+        const double gx = DADD((double)i, DMUL(M, u1));
+        const double gy = DADD((double)j, DMUL(M, u2));
+        int si = (int)floor(DADD(gx, 0.5)), sj = (int)floor(DADD(gy, 0.5));
+        si = si < 0 ? 0 : (si > n - 1 ? n - 1 : si);
+        sj = sj < 0 ? 0 : (sj > n - 1 ? n - 1 : sj);
+        succ[k] = (int32_t)((int64_t)sj * n + si);
+    }
+}
+
+__global__ void k_jump(const int32_t *__restrict__ in, int32_t *__restrict__ out, int64_t N,
+                       int *changed)
+{
+    bool ch = false;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < N;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t s = in[k];
+        const int32_t ss = in[s];
+        out[k] = ss;
+        ch |= (ss != s);
+    }
+    if (__any_sync(0xffffffffu, ch) && (threadIdx.x & 31) == 0) atomicOr(changed, 1);
+}
+
+__global__ void k_labels(const uint8_t *__restrict__ kind, const int16_t *__restrict__ sector,
+                         const int32_t *__restrict__ root, int n_patches, int64_t N,
+                         int16_t *__restrict__ labels)
+{
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < N;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const uint8_t kd = kind[k];
+        if (kd == 1) { labels[k] = -1; continue; }
+        if (kd == 2) { labels[k] = -2; continue; }
+        const int32_t r = root[k];
+        labels[k] = kind[r] == 1 ? sector[r] : (int16_t)n_patches;
+    }
+}
+
+__global__ void k_static_labels(int n, int px, int py, const uint8_t *__restrict__ kind,
+                                int16_t *__restrict__ labels)
+{
+    const int64_t N = (int64_t)n * n;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < N;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(k % n), j = (int)(k / n);
+        int bx = (int)(((int64_t)i * px) / n), by = (int)(((int64_t)j * py) / n);
+        // boundaries floor(k n / P): the largest b with floor(b n / P) <= i
+        while (bx + 1 < px && ((int64_t)(bx + 1) * n) / px <= i) ++bx;
+        while (bx > 0 && ((int64_t)bx * n) / px > i) --bx;
+        while (by + 1 < py && ((int64_t)(by + 1) * n) / py <= j) ++by;
+        while (by > 0 && ((int64_t)by * n) / py > j) --by;
+        const uint8_t kd = kind[k];
+        labels[k] = kd == 1 ? -1 : kd == 2 ? -2 : (int16_t)(by * px + bx);
+    }
+}
+
+static int grid_for(int64_t N, int block)
+{
+    int64_t g = (N + block - 1) / block;
+    if (g > 148 * 32) g = 148 * 32;
+    return (int)(g < 1 ? 1 : g);
+}
+
+void launch_init_values(const DProblem &P, double *V, cudaStream_t s)
+{
+    const int64_t N = (int64_t)P.n * P.n;
+    k_init_values<<<grid_for(N, 256), 256, 0, s>>>(P, V);
+}
+
+void launch_coarse_sweep(const DProblem &P, const double *Vin, double *Vout, double tol,
+                         unsigned long long *res_hist, int sweep, int *sweeps_done,
+                         cudaStream_t s)
+{
+    const int64_t N = (int64_t)P.n * P.n;
+    k_coarse_sweep<<<grid_for(N, 128), 128, 0, s>>>(P, Vin, Vout, tol, res_hist, sweep,
+                                                     sweeps_done);
+}
+
+void launch_prolong(int nc, const double *uc, int n, double *out, cudaStream_t s)
+{
+    const int64_t N = (int64_t)n * n;
+    k_prolong<<<grid_for(N, 256), 256, 0, s>>>(nc, uc, n, (n - 1) / (nc - 1), out);
+}
+
+void launch_synthesize(const DProblem &P, const double *uhat, uint8_t *astar, cudaStream_t s)
+{
+    const int64_t N = (int64_t)P.n * P.n;
+    k_synthesize<<<grid_for(N, 128), 128, 0, s>>>(P, uhat, astar);
+}
+
+void launch_successor(const DProblem &P, double M, const uint8_t *astar, int32_t *succ,
+                      cudaStream_t s)
+{
+    const int64_t N = (int64_t)P.n * P.n;
+    k_successor<<<grid_for(N, 256), 256, 0, s>>>(P, M, astar, succ);
+}
+
+void launch_jump(const int32_t *in, int32_t *out, int64_t N, int *changed, cudaStream_t s)
+{
+    k_jump<<<grid_for(N, 256), 256, 0, s>>>(in, out, N, changed);
+}
+
+void launch_labels(const uint8_t *kind, const int16_t *sector, const int32_t *root,
+                   int n_patches, int64_t N, int16_t *labels, cudaStream_t s)
+{
+    k_labels<<<grid_for(N, 256), 256, 0, s>>>(kind, sector, root, n_patches, N, labels);
+}
+
+void launch_static_labels(int n, int px, int py, const uint8_t *kind, int16_t *labels,
+                          cudaStream_t s)
+{
+    const int64_t N = (int64_t)n * n;
+    k_static_labels<<<grid_for(N, 256), 256, 0, s>>>(n, px, py, kind, labels);
+}
+
+}  // namespace pdd

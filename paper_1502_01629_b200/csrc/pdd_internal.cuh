@@ -1,0 +1,127 @@
+// pdd_internal.cuh -- device-side problem description and launch wrappers shared by the
+// libpdd translation units (runtime.cu, canonical.cu, sweep.cu).  Product code only; nothing
+// here is shared with oracle/.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace pdd {
+
+// A coefficient on the device: CONST value, ROW (x2) / COL (x1) table, or n*n FIELD.
+struct DCoef {
+    int kind;
+    double value;
+    const double *data;
+};
+
+__host__ __device__ __forceinline__ double coef_at(const DCoef &c, int i, int j, int n)
+{
+    switch (c.kind) {
+    case 0: return c.value;
+    case 1: return c.data[j];
+    case 2: return c.data[i];
+    default: return c.data[(int64_t)j * n + i];
+    }
+}
+
+// One discretised problem (fine G or coarse G_c), device pointers.
+struct DProblem {
+    int n;
+    double lo, dx, h, lambda;
+    double beta;      // 1/(1 + lambda h)
+    double q;         // h/dx: drift displacement in cells per unit speed
+    double sc;        // diffusion displacement in cells per unit sigma: sqrt(h p)/dx or sqrt(h)/dx
+    double lmax;      // max_x l(x)
+    double v0;        // h lmax/(1 - beta): initial supersolution (R11)
+    int na;
+    const double *ctrl;  // 2*na
+    DCoef speed, drift[2], sigma[2][2], cost;
+    int p;
+    const uint8_t *kind;
+};
+
+// Row-table stencil entry (row-uniform coefficients): for one grid row j and one control k,
+// the branch-merged compact stencil of an interior node relative to the node:
+//   v_k - V_ref = c_k + sum_{r<WY, x<WX} W[r][x] u(j + oy + r, i + ox + x),
+//   c_k = D E,  D = h l - (1 - beta) V_ref,  E = 1/(1 - beta Lambda0_k),
+//   W = beta w (sum of non-self bilinear weights of all branches at that node) E.
+template <typename real, int WY, int WX>
+struct RowEntry {
+    int oy, ox;
+    real E;
+    real W[WY * WX];
+};
+
+// ---------------------------------------------------------------- canonical.cu launchers
+void launch_init_values(const DProblem &P, double *V, cudaStream_t s);
+void launch_coarse_sweep(const DProblem &P, const double *Vin, double *Vout, double tol,
+                         unsigned long long *res_hist, int sweep, int *sweeps_done,
+                         cudaStream_t s);
+void launch_prolong(int nc, const double *uc, int n, double *out, cudaStream_t s);
+void launch_synthesize(const DProblem &P, const double *uhat, uint8_t *astar, cudaStream_t s);
+void launch_successor(const DProblem &P, double M, const uint8_t *astar, int32_t *succ,
+                      cudaStream_t s);
+void launch_jump(const int32_t *in, int32_t *out, int64_t N, int *changed, cudaStream_t s);
+void launch_labels(const uint8_t *kind, const int16_t *sector, const int32_t *root,
+                   int n_patches, int64_t N, int16_t *labels, cudaStream_t s);
+void launch_static_labels(int n, int px, int py, const uint8_t *kind, int16_t *labels,
+                          cudaStream_t s);
+
+// ---------------------------------------------------------------- sweep.cu
+struct TileGeom {
+    int TW, TH, H, tiles_x, tiles_y, pitch;
+};
+
+struct TileState {
+    int32_t *tile_free;      // free nodes per tile
+    double *tile_minu;       // min u_hat over free nodes (patchy bucket key)
+    double *tile_res;        // last in-tile residual (or verification residual)
+    double *tile_chg;        // net change of the last visit (0 if not visited this round)
+    int16_t *tile_lab;       // up to 4 distinct patch labels per tile (-1 unused)
+    int32_t *list[2];        // active tile lists
+    int32_t *all_list;       // tiles with free nodes
+    int32_t *patch_round;    // per patch: last round with an active tile
+    double *patch_res;       // per patch: max residual of its active tiles
+    void *counters;          // ActCounters (device)
+};
+
+struct ActCounters {
+    int32_t count;
+    int32_t pad;
+    long long free_sum;
+    unsigned long long min_pending;   // ordered bits of the min u_hat of needy ineligible tiles
+    unsigned long long max_res;       // ordered bits of the max tile residual
+};
+
+struct SweepLaunch {
+    DProblem P;
+    double *V;
+    const int16_t *labels;
+    TileGeom g;
+    const int32_t *list;
+    int n_list;
+    double *tile_res, *tile_chg;
+    int k_inner;
+    double *out;             // check mode with output (apply operator)
+    const void *rowtab;      // RowEntry array [n][na_pad]
+    int na_pad;
+    int Hx;                  // nodes with i < Hx or i > n-1-Hx use the general stencil
+    int path;                // 1 general, 2 row-table
+    int WY, WX;              // row-table window
+    int check;               // 1: pure Jacobi residual, no update
+    int precision;           // 32 | 64
+};
+
+void launch_tile_init(const DProblem &P, const TileGeom &g, const double *uhat,
+                      const int16_t *labels, TileState &T, cudaStream_t s);
+void launch_set_values(const DProblem &P, int mode, const double *uhat, double *V,
+                       cudaStream_t s);
+void launch_activate(const TileGeom &g, TileState &T, int out_list, double tol, double tol_act,
+                     double thr, int round, int n_tiles, cudaStream_t s);
+cudaError_t launch_sweep(const SweepLaunch &L, cudaStream_t s);
+bool rowtab_supported(int WY, int WX, int cpl);
+int rowtab_tw(int WY, int WX);
+size_t rowtab_entry_bytes(int precision, int WY, int WX);
+
+}  // namespace pdd

@@ -1,0 +1,990 @@
+// runtime.cu -- libpdd host runtime: the C ABI of include/pdd.h.
+//
+// Owns the device state carved from a caller-provided workspace, enqueues the kernels of
+// canonical.cu / sweep.cu on the caller's stream, and drives the two loops of the method:
+//   * the coarse Jacobi solve: batches of self-stopping sweeps, residual history
+//     on the device, one 4-byte readback per batch;
+//   * the fine solve: rounds of {activation / compaction -> tile sweep kernel}
+//     with one 24-byte counter readback per round, patchy bucket threshold (P:744-749,
+//     P:831), and a full-grid Jacobi verification pass when no tile is active.
+#include "../../include/pdd.h"
+#include "pdd_internal.cuh"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+using namespace pdd;
+
+namespace {
+
+thread_local std::string g_err;
+
+constexpr size_t kAlign = 256;
+constexpr int kMaxPatches = 32768;
+constexpr int64_t kMaxCoarseSweeps = 1 << 20;
+
+struct HostCoefInfo {
+    int kind;
+    double value;
+    size_t count;   // doubles to copy
+};
+
+size_t coef_count(const pdd_coef &c, int n)
+{
+    switch (c.kind) {
+    case PDD_COEF_ROW:
+    case PDD_COEF_COL: return (size_t)n;
+    case PDD_COEF_FIELD: return (size_t)n * n;
+    default: return 0;
+    }
+}
+
+struct Carver {
+    char *base;
+    size_t off = 0;
+    explicit Carver(void *b) : base((char *)b) {}
+    template <class T>
+    T *take(size_t count)
+    {
+        off = (off + kAlign - 1) / kAlign * kAlign;
+        T *p = base ? reinterpret_cast<T *>(base + off) : nullptr;
+        off += count * sizeof(T);
+        return p;
+    }
+};
+
+// device copies of one problem
+struct ProbBufs {
+    DProblem d;
+    double *ctrl = nullptr;
+    double *coef[8] = {nullptr};   // speed, drift0, drift1, s00, s01, s10, s11, cost
+    uint8_t *kind = nullptr;
+    int16_t *sector = nullptr;
+};
+
+const pdd_coef *coef_ptr(const pdd_problem *p, int k)
+{
+    switch (k) {
+    case 0: return &p->speed;
+    case 1: return &p->drift[0];
+    case 2: return &p->drift[1];
+    case 3: return &p->sigma[0][0];
+    case 4: return &p->sigma[0][1];
+    case 5: return &p->sigma[1][0];
+    case 6: return &p->sigma[1][1];
+    default: return &p->cost;
+    }
+}
+
+void carve_problem(Carver &cv, const pdd_problem *p, ProbBufs &b, bool with_sector)
+{
+    const int n = p->n;
+    b.ctrl = cv.take<double>(2 * (size_t)p->n_controls);
+    for (int k = 0; k < 8; ++k) {
+        const size_t c = coef_count(*coef_ptr(p, k), n);
+        b.coef[k] = c ? cv.take<double>(c) : nullptr;
+    }
+    b.kind = cv.take<uint8_t>((size_t)n * n);
+    b.sector = with_sector ? cv.take<int16_t>((size_t)n * n) : nullptr;
+}
+
+int na_pad_of(int na) { return na <= 32 ? 32 : (na <= 64 ? 64 : 0); }
+
+}  // namespace
+
+struct pdd_ctx {
+    std::string err;
+    cudaStream_t stream = nullptr;
+    int precision = 32;
+    bool owns_nothing = true;
+    pdd_problem fine{}, coarse{};
+    bool has_coarse = false;
+    ProbBufs F, Cc;
+    // fine fields
+    double *V = nullptr, *uhat = nullptr, *uc[2] = {nullptr, nullptr};
+    double *uc_final = nullptr;
+    uint8_t *astar = nullptr;
+    int16_t *labels = nullptr;
+    int32_t *succ0 = nullptr, *succA = nullptr, *succB = nullptr;
+    unsigned long long *res_hist = nullptr;
+    int *dev_int = nullptr;     // [0] sweeps_done, [1] jump changed flag
+    void *rowtab = nullptr;
+    size_t rowtab_bytes = 0;
+    TileState T{};
+    int max_tiles = 0;
+    double *outbuf = nullptr;
+    // host pinned
+    ActCounters *h_cnt = nullptr;
+    int *h_int = nullptr;
+    // state
+    bool coarse_done = false, synth_done = false;
+    int labels_mode = 0;        // 0 none, 1 patchy, 2 static
+    int n_patches = 0;
+    int n_patch_slots = 0;
+    // sweep configuration
+    int path = 0, WY = 0, WX = 0, Hx = 0;
+    TileGeom g{};
+    int n_tiles = 0;
+    int prepared_kernel = -1;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+};
+
+static pdd_status fail(pdd_ctx *c, pdd_status s, const char *fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (c) c->err = buf;
+    else g_err = buf;
+    return s;
+}
+
+#define CK(call)                                                                             \
+    do {                                                                                     \
+        cudaError_t e_ = (call);                                                             \
+        if (e_ != cudaSuccess)                                                               \
+            return fail(ctx, PDD_E_CUDA, "%s failed: %s (%s:%d)", #call,                     \
+                        cudaGetErrorString(e_), __FILE__, __LINE__);                         \
+    } while (0)
+
+static pdd_status validate(const pdd_problem *p, const char *what)
+{
+    if (!p) return fail(nullptr, PDD_E_INVALID, "%s problem is NULL", what);
+    if (p->n < 3) return fail(nullptr, PDD_E_INVALID, "%s: n = %d < 3", what, p->n);
+    if (!(p->hi > p->lo)) return fail(nullptr, PDD_E_INVALID, "%s: hi <= lo", what);
+    if (!(p->dx > 0.0) || !(p->h > 0.0))
+        return fail(nullptr, PDD_E_INVALID, "%s: dx and h must be > 0", what);
+    if (!(p->lambda > 0.0)) return fail(nullptr, PDD_E_INVALID, "%s: lambda must be > 0", what);
+    if (p->n_controls < 1 || p->n_controls > 128)
+        return fail(nullptr, PDD_E_INVALID, "%s: N_A = %d outside 1..128", what, p->n_controls);
+    if (!p->controls) return fail(nullptr, PDD_E_INVALID, "%s: controls is NULL", what);
+    if (p->p < 0 || p->p > 2) return fail(nullptr, PDD_E_INVALID, "%s: p = %d outside 0..2", what, p->p);
+    if (!p->kind) return fail(nullptr, PDD_E_INVALID, "%s: kind is NULL", what);
+    for (int k = 0; k < 8; ++k) {
+        const pdd_coef *c = coef_ptr(p, k);
+        if (c->kind < 0 || c->kind > 3) return fail(nullptr, PDD_E_INVALID, "%s: bad coef kind", what);
+        if (c->kind != PDD_COEF_CONST && !c->data)
+            return fail(nullptr, PDD_E_INVALID, "%s: coefficient %d has NULL data", what, k);
+    }
+    // l > 0
+    const pdd_coef &l = p->cost;
+    const size_t cnt = coef_count(l, p->n);
+    if (cnt == 0) {
+        if (!(l.value > 0.0)) return fail(nullptr, PDD_E_INVALID, "%s: running cost must be > 0", what);
+    } else {
+        for (size_t i = 0; i < cnt; ++i)
+            if (!(l.data[i] > 0.0)) return fail(nullptr, PDD_E_INVALID, "%s: running cost must be > 0", what);
+    }
+    return PDD_OK;
+}
+
+static double coef_max_abs(const pdd_coef &c, int n)
+{
+    const size_t cnt = coef_count(c, n);
+    if (!cnt) return std::fabs(c.value);
+    double m = 0.0;
+    for (size_t i = 0; i < cnt; ++i) m = std::max(m, std::fabs(c.data[i]));
+    return m;
+}
+
+static double host_coef_at(const pdd_coef &c, int i, int j, int n)
+{
+    switch (c.kind) {
+    case 0: return c.value;
+    case 1: return c.data[j];
+    case 2: return c.data[i];
+    default: return c.data[(size_t)j * n + i];
+    }
+}
+
+// reach of the foot points in cells (R4): (h max|f| + sc max|sigma_j|)/dx
+static double reach_cells(const pdd_problem *p)
+{
+    double amax = 0.0;
+    for (int k = 0; k < p->n_controls; ++k)
+        amax = std::max(amax, std::hypot(p->controls[2 * k], p->controls[2 * k + 1]));
+    const double fmax = coef_max_abs(p->speed, p->n) * amax +
+                        std::hypot(coef_max_abs(p->drift[0], p->n), coef_max_abs(p->drift[1], p->n));
+    double smax = 0.0;
+    if (p->p > 0) {
+        const double sc = p->diffusion_scale == 0 ? std::sqrt(p->h * p->p) : std::sqrt(p->h);
+        for (int k = 0; k < p->p; ++k)
+            smax = std::max(smax, sc * std::hypot(coef_max_abs(p->sigma[k][0], p->n),
+                                                  coef_max_abs(p->sigma[k][1], p->n)));
+    }
+    return (p->h * fmax + smax) / p->dx;
+}
+
+static int halo_of(const pdd_problem *p)
+{
+    const double r = reach_cells(p);
+    return (int)std::floor(r * (1.0 + 1e-9) + 1e-9) + 2;
+}
+
+static void make_dproblem(const pdd_problem *p, ProbBufs &b)
+{
+    DProblem &d = b.d;
+    d.n = p->n;
+    d.lo = p->lo;
+    d.dx = p->dx;
+    d.h = p->h;
+    d.lambda = p->lambda;
+    d.beta = 1.0 / (1.0 + p->lambda * p->h);
+    d.q = p->h / p->dx;
+    d.sc = p->p > 0 ? (p->diffusion_scale == 0 ? std::sqrt(p->h * (double)p->p) : std::sqrt(p->h)) / p->dx
+                    : 0.0;
+    double lmax = 0.0;
+    const size_t cl = coef_count(p->cost, p->n);
+    if (!cl) lmax = p->cost.value;
+    else for (size_t i = 0; i < cl; ++i) lmax = std::max(lmax, p->cost.data[i]);
+    d.lmax = lmax;
+    d.v0 = (p->h * lmax) / (1.0 - d.beta);     // canonical: same expression as the oracle
+    d.na = p->n_controls;
+    d.ctrl = b.ctrl;
+    DCoef *dc[8] = {&d.speed, &d.drift[0], &d.drift[1], &d.sigma[0][0], &d.sigma[0][1],
+                    &d.sigma[1][0], &d.sigma[1][1], &d.cost};
+    for (int k = 0; k < 8; ++k) {
+        const pdd_coef *c = coef_ptr(p, k);
+        dc[k]->kind = c->kind;
+        dc[k]->value = c->value;
+        dc[k]->data = b.coef[k];
+    }
+    d.p = p->p;
+    d.kind = b.kind;
+}
+
+static size_t layout(pdd_ctx *c, void *ws, const pdd_problem *f, const pdd_problem *cp)
+{
+    Carver cv(ws);
+    const int n = f->n;
+    const size_t N = (size_t)n * n;
+    ProbBufs F, Cc;
+    carve_problem(cv, f, F, f->sector != nullptr);
+    if (cp) carve_problem(cv, cp, Cc, false);
+    double *V = cv.take<double>(N);
+    double *uhat = cp ? cv.take<double>(N) : nullptr;
+    double *uc0 = cp ? cv.take<double>((size_t)cp->n * cp->n) : nullptr;
+    double *uc1 = cp ? cv.take<double>((size_t)cp->n * cp->n) : nullptr;
+    unsigned long long *rh = cp ? cv.take<unsigned long long>(kMaxCoarseSweeps) : nullptr;
+    uint8_t *astar = cv.take<uint8_t>(N);
+    int16_t *labels = cv.take<int16_t>(N);
+    int32_t *s0 = cp ? cv.take<int32_t>(N) : nullptr;
+    int32_t *sA = cp ? cv.take<int32_t>(N) : nullptr;
+    int32_t *sB = cp ? cv.take<int32_t>(N) : nullptr;
+    int *di = cv.take<int>(8);
+    const int napad = na_pad_of(f->n_controls);
+    const size_t rtb = napad ? (size_t)n * napad * 160 : 0;   // >= sizeof(RowEntry<double,4,4>)
+    void *rt = rtb ? cv.take<unsigned char>(rtb) : nullptr;
+    const int tmax = ((n + 31) / 32) * ((n + 31) / 32);
+    TileState T{};
+    T.tile_free = cv.take<int32_t>(tmax);
+    T.tile_minu = cv.take<double>(tmax);
+    T.tile_res = cv.take<double>(tmax);
+    T.tile_chg = cv.take<double>(tmax);
+    T.tile_lab = cv.take<int16_t>(4 * (size_t)tmax);
+    T.list[0] = cv.take<int32_t>(tmax);
+    T.list[1] = cv.take<int32_t>(tmax);
+    T.all_list = cv.take<int32_t>(tmax);
+    T.patch_round = cv.take<int32_t>(kMaxPatches + 1);
+    T.patch_res = cv.take<double>(kMaxPatches + 1);
+    T.counters = cv.take<ActCounters>(1);
+    if (c) {
+        c->F = F;
+        c->Cc = Cc;
+        c->V = V;
+        c->uhat = uhat;
+        c->uc[0] = uc0;
+        c->uc[1] = uc1;
+        c->res_hist = rh;
+        c->astar = astar;
+        c->labels = labels;
+        c->succ0 = s0;
+        c->succA = sA;
+        c->succB = sB;
+        c->dev_int = di;
+        c->rowtab = rt;
+        c->rowtab_bytes = rtb;
+        c->T = T;
+        c->max_tiles = tmax;
+    }
+    return cv.off + kAlign;
+}
+
+extern "C" {
+
+const char *pdd_version(void) { return "pdd-b200 0.1 (sm_100a)"; }
+
+const char *pdd_last_error(const pdd_ctx *ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
+
+pdd_status pdd_workspace_bytes(const pdd_problem *fine, const pdd_problem *coarse,
+                               int32_t precision, size_t *bytes)
+{
+    pdd_status s = validate(fine, "fine");
+    if (s != PDD_OK) return s;
+    if (coarse && (s = validate(coarse, "coarse")) != PDD_OK) return s;
+    if (precision != 32 && precision != 64)
+        return fail(nullptr, PDD_E_INVALID, "precision must be 32 or 64");
+    if (!bytes) return fail(nullptr, PDD_E_INVALID, "bytes is NULL");
+    *bytes = layout(nullptr, nullptr, fine, coarse);
+    return PDD_OK;
+}
+
+static pdd_status copy_problem(pdd_ctx *ctx, const pdd_problem *p, ProbBufs &b, bool sector)
+{
+    const int n = p->n;
+    CK(cudaMemcpyAsync(b.ctrl, p->controls, sizeof(double) * 2 * p->n_controls,
+                       cudaMemcpyHostToDevice, ctx->stream));
+    for (int k = 0; k < 8; ++k) {
+        const pdd_coef *c = coef_ptr(p, k);
+        const size_t cnt = coef_count(*c, n);
+        if (cnt) CK(cudaMemcpyAsync(b.coef[k], c->data, sizeof(double) * cnt,
+                                    cudaMemcpyHostToDevice, ctx->stream));
+    }
+    CK(cudaMemcpyAsync(b.kind, p->kind, (size_t)n * n, cudaMemcpyHostToDevice, ctx->stream));
+    if (sector && b.sector)
+        CK(cudaMemcpyAsync(b.sector, p->sector, sizeof(int16_t) * n * n, cudaMemcpyHostToDevice,
+                           ctx->stream));
+    make_dproblem(p, b);
+    return PDD_OK;
+}
+
+pdd_status pdd_create(const pdd_problem *fine, const pdd_problem *coarse, int32_t precision,
+                      void *stream, void *workspace, size_t workspace_bytes, pdd_ctx **out)
+{
+    if (!out) return fail(nullptr, PDD_E_INVALID, "out is NULL");
+    *out = nullptr;
+    size_t need = 0;
+    pdd_status s = pdd_workspace_bytes(fine, coarse, precision, &need);
+    if (s != PDD_OK) return s;
+    if (!workspace) return fail(nullptr, PDD_E_INVALID, "workspace is NULL");
+    if (workspace_bytes < need)
+        return fail(nullptr, PDD_E_NOMEM, "workspace of %zu bytes < %zu needed", workspace_bytes, need);
+    if (coarse) {
+        if (coarse->lo != fine->lo || coarse->hi != fine->hi)
+            return fail(nullptr, PDD_E_INVALID, "coarse and fine boxes differ");
+        if ((fine->n - 1) % (coarse->n - 1) != 0)
+            return fail(nullptr, PDD_E_INVALID, "coarse grid (n=%d) does not nest in fine grid (n=%d)",
+                        coarse->n, fine->n);
+        if (coarse->p != 0)
+            return fail(nullptr, PDD_E_INVALID, "the coarse problem must have sigma = 0 (p = 0), P:825");
+    }
+    pdd_ctx *ctx = new pdd_ctx();
+    ctx->stream = (cudaStream_t)stream;
+    ctx->precision = precision;
+    ctx->fine = *fine;
+    ctx->has_coarse = coarse != nullptr;
+    if (coarse) ctx->coarse = *coarse;
+    // aligned base
+    char *base = (char *)workspace;
+    const size_t mis = (size_t)((uintptr_t)base % kAlign);
+    if (mis) base += kAlign - mis;
+    layout(ctx, base, fine, coarse);
+    // host pinned scratch
+    {
+        cudaError_t e = cudaHostAlloc((void **)&ctx->h_cnt, sizeof(ActCounters) + 64, 0);
+        if (e != cudaSuccess) {
+            pdd_status st = fail(nullptr, PDD_E_CUDA, "cudaHostAlloc: %s", cudaGetErrorString(e));
+            delete ctx;
+            return st;
+        }
+        ctx->h_int = reinterpret_cast<int *>(ctx->h_cnt + 1);
+    }
+    for (int k = 0; k < 4; ++k) cudaEventCreate(&ctx->ev[k]);
+    s = copy_problem(ctx, fine, ctx->F, true);
+    if (s == PDD_OK && coarse) s = copy_problem(ctx, coarse, ctx->Cc, false);
+    if (s == PDD_OK) {
+        launch_init_values(ctx->F.d, ctx->V, ctx->stream);
+        cudaError_t e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+        if (e != cudaSuccess) s = fail(nullptr, PDD_E_CUDA, "create: %s", cudaGetErrorString(e));
+    } else {
+        g_err = ctx->err;
+    }
+    if (s != PDD_OK) {
+        pdd_destroy(ctx);
+        return s;
+    }
+    *out = ctx;
+    return PDD_OK;
+}
+
+void pdd_destroy(pdd_ctx *ctx)
+{
+    if (!ctx) return;
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    for (int k = 0; k < 4; ++k)
+        if (ctx->ev[k]) cudaEventDestroy(ctx->ev[k]);
+    if (ctx->h_cnt) cudaFreeHost(ctx->h_cnt);
+    delete ctx;
+}
+
+pdd_status pdd_coarse_solve(pdd_ctx *ctx, double tol_c, int64_t max_sweeps, pdd_coarse_stats *st)
+{
+    if (!ctx) return fail(nullptr, PDD_E_INVALID, "ctx is NULL");
+    if (!ctx->has_coarse) return fail(ctx, PDD_E_STATE, "no coarse problem was given to pdd_create");
+    if (!(tol_c > 0.0)) return fail(ctx, PDD_E_INVALID, "tol_c must be > 0");
+    if (max_sweeps <= 0 || max_sweeps > kMaxCoarseSweeps)
+        return fail(ctx, PDD_E_INVALID, "max_sweeps must be in 1..%lld", (long long)kMaxCoarseSweeps);
+    cudaStream_t s = ctx->stream;
+    const DProblem &Pc = ctx->Cc.d;
+    CK(cudaEventRecord(ctx->ev[0], s));
+    launch_init_values(Pc, ctx->uc[0], s);
+    CK(cudaMemsetAsync(ctx->res_hist, 0, sizeof(unsigned long long) * max_sweeps, s));
+    CK(cudaMemsetAsync(ctx->dev_int, 0, sizeof(int), s));
+    int64_t issued = 0;
+    int done = 0;
+    bool converged = false;
+    int64_t batch = 8;
+    while (issued < max_sweeps) {
+        const int64_t b = std::min<int64_t>(batch, max_sweeps - issued);
+        for (int64_t q = 0; q < b; ++q, ++issued)
+            launch_coarse_sweep(Pc, ctx->uc[issued & 1], ctx->uc[(issued + 1) & 1], tol_c,
+                                ctx->res_hist, (int)issued, ctx->dev_int, s);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(ctx->h_int, ctx->dev_int, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        done = ctx->h_int[0];
+        if (done < issued) { converged = true; break; }
+        unsigned long long last = 0;
+        CK(cudaMemcpy(&last, ctx->res_hist + (issued - 1), sizeof last, cudaMemcpyDeviceToHost));
+        double lr;
+        std::memcpy(&lr, &last, sizeof lr);
+        if (lr < tol_c) { converged = true; break; }
+        batch = std::min<int64_t>(batch * 2, 256);
+    }
+    CK(cudaEventRecord(ctx->ev[1], s));
+    CK(cudaEventSynchronize(ctx->ev[1]));
+    ctx->uc_final = ctx->uc[done & 1];
+    ctx->coarse_done = true;
+    ctx->synth_done = false;
+    unsigned long long lastbits = 0;
+    if (done > 0)
+        CK(cudaMemcpy(&lastbits, ctx->res_hist + (done - 1), sizeof lastbits, cudaMemcpyDeviceToHost));
+    if (st) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]);
+        st->sweeps = done;
+        std::memcpy(&st->residual, &lastbits, sizeof(double));
+        st->seconds = ms * 1e-3;
+        st->converged = converged ? 1 : 0;
+    }
+    return converged ? PDD_OK : fail(ctx, PDD_E_NOCONVERGE, "coarse solve: %lld sweeps without reaching tol",
+                                     (long long)done);
+}
+
+pdd_status pdd_synthesize(pdd_ctx *ctx)
+{
+    if (!ctx) return fail(nullptr, PDD_E_INVALID, "ctx is NULL");
+    if (!ctx->coarse_done) return fail(ctx, PDD_E_STATE, "pdd_synthesize needs pdd_coarse_solve first");
+    cudaStream_t s = ctx->stream;
+    launch_prolong(ctx->coarse.n, ctx->uc_final, ctx->fine.n, ctx->uhat, s);
+    launch_synthesize(ctx->F.d, ctx->uhat, ctx->astar, s);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s));
+    ctx->synth_done = true;
+    return PDD_OK;
+}
+
+pdd_status pdd_build_patches(pdd_ctx *ctx, int32_t n_patches, double M)
+{
+    if (!ctx) return fail(nullptr, PDD_E_INVALID, "ctx is NULL");
+    if (!ctx->synth_done) return fail(ctx, PDD_E_STATE, "pdd_build_patches needs pdd_synthesize first");
+    if (n_patches < 1 || n_patches >= kMaxPatches)
+        return fail(ctx, PDD_E_INVALID, "n_patches must be in 1..%d", kMaxPatches - 1);
+    if (!ctx->F.sector) return fail(ctx, PDD_E_INVALID, "the fine problem has no sector table");
+    if (M == 0.0) M = 4.0;
+    if (!(M > 0.0)) return fail(ctx, PDD_E_INVALID, "M must be > 0");
+    cudaStream_t s = ctx->stream;
+    const int64_t N = (int64_t)ctx->fine.n * ctx->fine.n;
+    launch_successor(ctx->F.d, M, ctx->astar, ctx->succ0, s);
+    CK(cudaGetLastError());
+    // pointer jumping: after K rounds every chain of length < 2^K has reached its root
+    int K = 1;
+    while ((int64_t(1) << K) < N) ++K;
+    const int32_t *in = ctx->succ0;
+    int32_t *bufs[2] = {ctx->succA, ctx->succB};
+    int r = 0;
+    for (; r < K + 1; ++r) {
+        CK(cudaMemsetAsync(ctx->dev_int + 1, 0, sizeof(int), s));
+        launch_jump(in, bufs[r & 1], N, ctx->dev_int + 1, s);
+        CK(cudaGetLastError());
+        in = bufs[r & 1];
+        if ((r & 3) == 3) {
+            CK(cudaMemcpyAsync(ctx->h_int + 1, ctx->dev_int + 1, sizeof(int), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            if (ctx->h_int[1] == 0) break;
+        }
+    }
+    launch_labels(ctx->F.kind, ctx->F.sector, in, n_patches, N, ctx->labels, s);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s));
+    ctx->labels_mode = 1;
+    ctx->n_patches = n_patches;
+    ctx->prepared_kernel = -1;
+    return PDD_OK;
+}
+
+pdd_status pdd_build_static(pdd_ctx *ctx, int32_t px, int32_t py)
+{
+    if (!ctx) return fail(nullptr, PDD_E_INVALID, "ctx is NULL");
+    if (px < 1 || py < 1 || (int64_t)px * py >= kMaxPatches || px > ctx->fine.n || py > ctx->fine.n)
+        return fail(ctx, PDD_E_INVALID, "bad static decomposition %d x %d", px, py);
+    launch_static_labels(ctx->fine.n, px, py, ctx->F.kind, ctx->labels, ctx->stream);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->labels_mode = 2;
+    ctx->n_patches = px * py;
+    ctx->prepared_kernel = -1;
+    return PDD_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------------ sweep preparation
+
+// Row-uniform compact stencils (host, fp64): returns false when the problem is not row-uniform.
+template <typename real, int WY, int WX>
+static void fill_rowtab(const pdd_problem *p, const DProblem &d, int napad, int H,
+                        std::vector<unsigned char> &buf, int &oxmin, int &oxmax)
+{
+    const int n = p->n;
+    const int na = p->n_controls;
+    const int nb = p->p > 0 ? 2 * p->p : 1;
+    const double w = 1.0 / nb;
+    buf.assign((size_t)n * napad * sizeof(RowEntry<real, WY, WX>), 0);
+    auto *E = reinterpret_cast<RowEntry<real, WY, WX> *>(buf.data());
+    oxmin = 1 << 30;
+    oxmax = -(1 << 30);
+    const int imid = n / 2;
+    for (int j = 0; j < n; ++j) {
+        const double c = host_coef_at(p->speed, imid, j, n);
+        const double d1 = host_coef_at(p->drift[0], imid, j, n);
+        const double d2 = host_coef_at(p->drift[1], imid, j, n);
+        double off[2][2] = {{0, 0}, {0, 0}};
+        for (int k = 0; k < p->p; ++k) {
+            off[k][0] = d.sc * host_coef_at(p->sigma[k][0], imid, j, n);
+            off[k][1] = d.sc * host_coef_at(p->sigma[k][1], imid, j, n);
+        }
+        for (int a = 0; a < na; ++a) {
+            const double bx = d.q * (c * p->controls[2 * a] + d1);
+            const double by = d.q * (c * p->controls[2 * a + 1] + d2);
+            double acc[16][16];
+            for (auto &r : acc) for (double &v : r) v = 0.0;
+            double lam0 = 0.0;
+            int ymin = 99, xmin = 99;
+            struct Cn { int dy, dx; double w; } cn[16];
+            int ncn = 0;
+            for (int b = 0; b < nb; ++b) {
+                double xr = bx, yr = by;
+                if (p->p > 0) {
+                    const int kk = b >> 1;
+                    if (b & 1) { xr -= off[kk][0]; yr -= off[kk][1]; }
+                    else { xr += off[kk][0]; yr += off[kk][1]; }
+                }
+                yr = std::min(std::max(yr, (double)-j), (double)(n - 1 - j));
+                const double fx = std::floor(xr);
+                const double fy = std::min(std::floor(yr), (double)(n - 2 - j));
+                const double tx = xr - fx, ty = yr - fy;
+                const double ww[4] = {(1 - tx) * (1 - ty), tx * (1 - ty), (1 - tx) * ty, tx * ty};
+                for (int t = 0; t < 4; ++t) {
+                    const int dx = (int)fx + (t & 1), dy = (int)fy + (t >> 1);
+                    if (dx == 0 && dy == 0) { lam0 += w * ww[t]; continue; }
+                    cn[ncn++] = {dy, dx, w * ww[t]};
+                    ymin = std::min(ymin, dy);
+                    xmin = std::min(xmin, dx);
+                }
+            }
+            // window origin: keep inside the halo [-H, H]
+            int oy = std::min(ymin, H - (WY - 1));
+            int ox = std::min(xmin, H - (WX - 1));
+            oy = std::max(oy, -H);
+            ox = std::max(ox, -H);
+            const double Ek = 1.0 / (1.0 - d.beta * lam0);
+            RowEntry<real, WY, WX> &e = E[(size_t)j * napad + a];
+            e.oy = oy;
+            e.ox = ox;
+            e.E = (real)Ek;
+            for (int t = 0; t < ncn; ++t) {
+                const int r = cn[t].dy - oy, x = cn[t].dx - ox;
+                acc[r][x] += cn[t].w;
+            }
+            for (int r = 0; r < WY; ++r)
+                for (int x = 0; x < WX; ++x) e.W[r * WX + x] = (real)(d.beta * acc[r][x] * Ek);
+            oxmin = std::min(oxmin, ox);
+            oxmax = std::max(oxmax, ox);
+        }
+    }
+}
+
+// Smallest (WY, WX) window over all rows/controls; false if not row-uniform.
+static bool rowtab_window(const pdd_problem *p, const DProblem &d, int &WY, int &WX)
+{
+    auto row_ok = [](const pdd_coef &c) { return c.kind == PDD_COEF_CONST || c.kind == PDD_COEF_ROW; };
+    if (!row_ok(p->speed) || !row_ok(p->drift[0]) || !row_ok(p->drift[1])) return false;
+    for (int k = 0; k < 2; ++k)
+        for (int c = 0; c < 2; ++c)
+            if (!row_ok(p->sigma[k][c])) return false;
+    if (p->cost.kind != PDD_COEF_CONST) return false;
+    if (na_pad_of(p->n_controls) == 0) return false;
+    const int n = p->n;
+    const int nb = p->p > 0 ? 2 * p->p : 1;
+    int ey = 0, ex = 0;
+    for (int j = 0; j < n; ++j) {
+        const double c = host_coef_at(p->speed, 0, j, n);
+        const double d1 = host_coef_at(p->drift[0], 0, j, n);
+        const double d2 = host_coef_at(p->drift[1], 0, j, n);
+        for (int a = 0; a < p->n_controls; ++a) {
+            const double bx = d.q * (c * p->controls[2 * a] + d1);
+            const double by = d.q * (c * p->controls[2 * a + 1] + d2);
+            int ymin = 1 << 30, ymax = -(1 << 30), xmin = 1 << 30, xmax = -(1 << 30);
+            for (int b = 0; b < nb; ++b) {
+                double xr = bx, yr = by;
+                if (p->p > 0) {
+                    const int kk = b >> 1;
+                    const double ox = d.sc * host_coef_at(p->sigma[kk][0], 0, j, n);
+                    const double oy = d.sc * host_coef_at(p->sigma[kk][1], 0, j, n);
+                    if (b & 1) { xr -= ox; yr -= oy; } else { xr += ox; yr += oy; }
+                }
+                yr = std::min(std::max(yr, (double)-j), (double)(n - 1 - j));
+                const int fx = (int)std::floor(xr);
+                const int fy = (int)std::min(std::floor(yr), (double)(n - 2 - j));
+                xmin = std::min(xmin, fx);
+                xmax = std::max(xmax, fx + 1);
+                ymin = std::min(ymin, fy);
+                ymax = std::max(ymax, fy + 1);
+            }
+            ey = std::max(ey, ymax - ymin + 1);
+            ex = std::max(ex, xmax - xmin + 1);
+        }
+    }
+    const int cand[3][2] = {{3, 3}, {2, 5}, {4, 4}};
+    for (auto &cw : cand)
+        if (ey <= cw[0] && ex <= cw[1]) { WY = cw[0]; WX = cw[1]; return true; }
+    return false;
+}
+
+static pdd_status prepare(pdd_ctx *ctx, int kernel_req)
+{
+    if (ctx->prepared_kernel == kernel_req) return PDD_OK;
+    const pdd_problem *p = &ctx->fine;
+    const DProblem &d = ctx->F.d;
+    const int H = halo_of(p);
+    if (H > 8) return fail(ctx, PDD_E_STENCIL, "foot points reach %.2f cells; tile halo limited to 8",
+                           reach_cells(p));
+    int WY = 0, WX = 0;
+    int path = 1;
+    const int napad = na_pad_of(p->n_controls);
+    if (kernel_req != 1 && rowtab_window(p, d, WY, WX) && rowtab_supported(WY, WX, napad / 32))
+        path = 2;
+    if (kernel_req == 2 && path != 2)
+        return fail(ctx, PDD_E_INVALID, "row-table stencil requested but the problem is not row-uniform");
+    ctx->path = path;
+    ctx->WY = WY;
+    ctx->WX = WX;
+    ctx->Hx = H;
+    TileGeom g{};
+    g.TW = path == 2 ? rowtab_tw(WY, WX) : 64;
+    g.TH = 32;
+    g.H = H;
+    g.tiles_x = (p->n + g.TW - 1) / g.TW;
+    g.tiles_y = (p->n + g.TH - 1) / g.TH;
+    int mod = 4;
+    if (path == 2) {
+        std::vector<unsigned char> buf;
+        int oxmin = 0, oxmax = 0;
+        const bool f32 = ctx->precision == 32;
+#define PDD_FILL(WY_, WX_)                                                                      \
+        if (WY == WY_ && WX == WX_) {                                                           \
+            if (f32) fill_rowtab<float, WY_, WX_>(p, d, napad, H, buf, oxmin, oxmax);           \
+            else fill_rowtab<double, WY_, WX_>(p, d, napad, H, buf, oxmin, oxmax);              \
+        }
+        PDD_FILL(3, 3)
+        PDD_FILL(2, 5)
+        PDD_FILL(4, 4)
+#undef PDD_FILL
+        if (buf.size() > ctx->rowtab_bytes)
+            return fail(ctx, PDD_E_NOMEM, "row table of %zu bytes exceeds its workspace slot", buf.size());
+        CK(cudaMemcpy(ctx->rowtab, buf.data(), buf.size(), cudaMemcpyHostToDevice));
+        mod = std::max(1, oxmax - oxmin + 1);
+    }
+    const int banks = ctx->precision == 32 ? 32 : 16;
+    int pitch = g.TW + 2 * H;
+    while (pitch % banks != mod % banks) ++pitch;
+    g.pitch = pitch;
+    ctx->g = g;
+    ctx->n_tiles = g.tiles_x * g.tiles_y;
+    if (ctx->n_tiles > ctx->max_tiles) return fail(ctx, PDD_E_NOMEM, "too many tiles");
+    std::vector<int32_t> all(ctx->n_tiles);
+    for (int t = 0; t < ctx->n_tiles; ++t) all[t] = t;
+    CK(cudaMemcpy(ctx->T.all_list, all.data(), sizeof(int32_t) * all.size(), cudaMemcpyHostToDevice));
+    ctx->prepared_kernel = kernel_req;
+    return PDD_OK;
+}
+
+static SweepLaunch make_launch(pdd_ctx *ctx, const int32_t *list, int n_list, int k_inner, int check,
+                               double *out)
+{
+    SweepLaunch L{};
+    L.P = ctx->F.d;
+    L.V = ctx->V;
+    L.labels = ctx->labels;
+    L.g = ctx->g;
+    L.list = list;
+    L.n_list = n_list;
+    L.tile_res = ctx->T.tile_res;
+    L.tile_chg = ctx->T.tile_chg;
+    L.k_inner = k_inner;
+    L.out = out;
+    L.rowtab = ctx->rowtab;
+    L.na_pad = na_pad_of(ctx->fine.n_controls);
+    L.Hx = ctx->Hx;
+    L.path = ctx->path;
+    L.WY = ctx->WY;
+    L.WX = ctx->WX;
+    L.check = check;
+    L.precision = ctx->precision;
+    return L;
+}
+
+static double bits_to_double(unsigned long long b)
+{
+    double d;
+    std::memcpy(&d, &b, sizeof d);
+    return d;
+}
+
+static pdd_status activate(pdd_ctx *ctx, int out_list, double tol, double thr, int round)
+{
+    cudaStream_t s = ctx->stream;
+    CK(cudaMemsetAsync(ctx->T.counters, 0, sizeof(ActCounters), s));
+    CK(cudaMemsetAsync(&reinterpret_cast<ActCounters *>(ctx->T.counters)->min_pending, 0xff, 8, s));
+    launch_activate(ctx->g, ctx->T, out_list, tol, tol, thr, round, ctx->n_tiles, s);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(ctx->h_cnt, ctx->T.counters, sizeof(ActCounters), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return PDD_OK;
+}
+
+__global__ void k_to_f32(const double *in, float *out, int64_t N)
+{
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < N; k += (int64_t)gridDim.x * blockDim.x)
+        out[k] = (float)in[k];
+}
+
+extern "C" {
+
+pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
+{
+    if (!ctx) return fail(nullptr, PDD_E_INVALID, "ctx is NULL");
+    if (!o) return fail(ctx, PDD_E_INVALID, "opts is NULL");
+    if (o->mode != 0 && o->mode != 1) return fail(ctx, PDD_E_INVALID, "mode must be 0 or 1");
+    if (o->k_inner < 1 || o->k_inner > 1024) return fail(ctx, PDD_E_INVALID, "k_inner outside 1..1024");
+    if (!(o->tol > 0.0)) return fail(ctx, PDD_E_INVALID, "tol must be > 0");
+    if (o->mode == 0 && (!ctx->synth_done || ctx->labels_mode != 1))
+        return fail(ctx, PDD_E_STATE, "patchy solve needs pdd_synthesize and pdd_build_patches");
+    if (o->mode == 1 && ctx->labels_mode != 2)
+        return fail(ctx, PDD_E_STATE, "static solve needs pdd_build_static");
+    pdd_status ps = prepare(ctx, o->kernel);
+    if (ps != PDD_OK) return ps;
+    cudaStream_t s = ctx->stream;
+    const DProblem &d = ctx->F.d;
+    CK(cudaEventRecord(ctx->ev[0], s));
+    launch_set_values(d, o->mode == 0 ? 0 : 1, ctx->uhat, ctx->V, s);
+    launch_tile_init(d, ctx->g, o->mode == 0 ? ctx->uhat : nullptr, ctx->labels, ctx->T, s);
+    CK(cudaMemsetAsync(ctx->T.patch_round, 0xff, sizeof(int32_t) * (ctx->n_patches + 1), s));
+    CK(cudaMemsetAsync(ctx->T.patch_res, 0, sizeof(double) * (ctx->n_patches + 1), s));
+    CK(cudaGetLastError());
+
+    double delta = o->delta;
+    if (o->mode == 1) delta = -1.0;
+    if (delta == 0.0) delta = ctx->g.TW * ctx->fine.h * d.lmax;   // ~ one tile of travel at unit speed
+    double thr = delta > 0.0 ? -1.0 : INFINITY;
+
+    pdd_solve_stats S{};
+    S.n_tiles = ctx->n_tiles;
+    S.kernel_used = ctx->path;
+    int cur = 0;
+    int round = 0;
+    bool converged = false;
+    double last_verify = INFINITY;
+    float ms_sweep = 0.f, ms_verify = 0.f;
+    while (true) {
+        if (S.rounds >= o->max_rounds) break;
+        pdd_status r = activate(ctx, cur, o->tol, thr, round);
+        if (r != PDD_OK) return r;
+        const ActCounters c = *ctx->h_cnt;
+        if (c.count > 0) {
+            CK(cudaMemsetAsync(ctx->T.tile_chg, 0, sizeof(double) * ctx->n_tiles, s));
+            CK(cudaEventRecord(ctx->ev[2], s));
+            SweepLaunch L = make_launch(ctx, ctx->T.list[cur], c.count, o->k_inner, 0, nullptr);
+            CK(launch_sweep(L, s));
+            CK(cudaEventRecord(ctx->ev[3], s));
+            CK(cudaEventSynchronize(ctx->ev[3]));
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]);
+            ms_sweep += ms;
+            S.rounds++;
+            S.tiles_processed += c.count;
+            S.node_updates += c.free_sum * (long long)o->k_inner;
+            if (delta > 0.0) thr += delta;
+            ++round;
+            continue;
+        }
+        const double pend = bits_to_double(c.min_pending);
+        if (c.min_pending != 0xffffffffffffffffull && std::isfinite(pend)) {
+            thr = std::max(thr, pend) + (delta > 0.0 ? delta : 0.0);
+            continue;
+        }
+        // nothing active: full-grid Jacobi verification
+        CK(cudaEventRecord(ctx->ev[2], s));
+        SweepLaunch L = make_launch(ctx, ctx->T.all_list, ctx->n_tiles, 1, 1, nullptr);
+        CK(launch_sweep(L, s));
+        CK(cudaMemsetAsync(ctx->T.tile_chg, 0, sizeof(double) * ctx->n_tiles, s));
+        CK(cudaEventRecord(ctx->ev[3], s));
+        S.rounds++;
+        S.verify_passes++;
+        ++round;
+        r = activate(ctx, cur, o->tol, INFINITY, round);
+        if (r != PDD_OK) return r;
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]);
+        ms_verify += ms;
+        last_verify = bits_to_double(ctx->h_cnt->max_res);
+        if (ctx->h_cnt->count == 0) { converged = true; break; }
+        thr = INFINITY;   // after a verification every offending tile is eligible
+    }
+    CK(cudaEventRecord(ctx->ev[1], s));
+    CK(cudaEventSynchronize(ctx->ev[1]));
+    float ms_total = 0.f;
+    cudaEventElapsedTime(&ms_total, ctx->ev[0], ctx->ev[1]);
+    S.final_residual = last_verify;
+    S.apost_bound = last_verify / (1.0 - d.beta);
+    S.seconds_total = ms_total * 1e-3;
+    S.seconds_sweep = ms_sweep * 1e-3;
+    S.seconds_verify = ms_verify * 1e-3;
+    S.converged = converged ? 1 : 0;
+    {
+        std::vector<int32_t> pr(ctx->n_patches + 1);
+        CK(cudaMemcpy(pr.data(), ctx->T.patch_round, sizeof(int32_t) * pr.size(), cudaMemcpyDeviceToHost));
+        int pc = 0;
+        for (size_t k = 0; k + 1 < pr.size(); ++k) pc += 1;   // all patches converged when solve converged
+        S.patches_converged = converged ? pc : 0;
+    }
+    if (st) *st = S;
+    return converged ? PDD_OK
+                     : fail(ctx, PDD_E_NOCONVERGE, "fine solve: %lld rounds without convergence (residual %.3e)",
+                            (long long)S.rounds, last_verify);
+}
+
+pdd_status pdd_apply_operator(pdd_ctx *ctx, double *out, int32_t kernel, double *residual)
+{
+    if (!ctx) return fail(nullptr, PDD_E_INVALID, "ctx is NULL");
+    if (kernel < 0 || kernel > 2) return fail(ctx, PDD_E_INVALID, "kernel must be 0, 1 or 2");
+    pdd_status ps = prepare(ctx, kernel);
+    if (ps != PDD_OK) return ps;
+    cudaStream_t s = ctx->stream;
+    const size_t N = (size_t)ctx->fine.n * ctx->fine.n;
+    double *dst = out;
+    if (dst) CK(cudaMemcpyAsync(dst, ctx->V, sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
+    launch_tile_init(ctx->F.d, ctx->g, nullptr, nullptr, ctx->T, s);
+    SweepLaunch L = make_launch(ctx, ctx->T.all_list, ctx->n_tiles, 1, 1, dst);
+    CK(launch_sweep(L, s));
+    pdd_status r = activate(ctx, 0, INFINITY, INFINITY, 0);
+    if (r != PDD_OK) return r;
+    if (residual) *residual = bits_to_double(ctx->h_cnt->max_res);
+    return PDD_OK;
+}
+
+pdd_status pdd_get_patch_rounds(pdd_ctx *ctx, int32_t *dst, int32_t count)
+{
+    if (!ctx || !dst) return fail(ctx, PDD_E_INVALID, "NULL argument");
+    if (count > ctx->n_patches + 1) count = ctx->n_patches + 1;
+    CK(cudaMemcpy(dst, ctx->T.patch_round, sizeof(int32_t) * count, cudaMemcpyDeviceToHost));
+    return PDD_OK;
+}
+
+static pdd_status fetch(pdd_ctx *ctx, void *dst, const void *src, size_t bytes, int on_device)
+{
+    if (!dst) return fail(ctx, PDD_E_INVALID, "dst is NULL");
+    if (!src) return fail(ctx, PDD_E_STATE, "array not computed yet");
+    CK(cudaMemcpyAsync(dst, src, bytes, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return PDD_OK;
+}
+
+
+pdd_status pdd_get_values(pdd_ctx *ctx, void *dst, int32_t dst_on_device, int32_t as_fp64)
+{
+    if (!ctx) return fail(nullptr, PDD_E_INVALID, "ctx is NULL");
+    const size_t N = (size_t)ctx->fine.n * ctx->fine.n;
+    if (as_fp64) return fetch(ctx, dst, ctx->V, sizeof(double) * N, dst_on_device);
+    if (!dst_on_device) {
+        std::vector<double> h(N);
+        pdd_status r = fetch(ctx, h.data(), ctx->V, sizeof(double) * N, 0);
+        if (r != PDD_OK) return r;
+        float *f = (float *)dst;
+        for (size_t k = 0; k < N; ++k) f[k] = (float)h[k];
+        return PDD_OK;
+    }
+    k_to_f32<<<4 * 148, 256, 0, ctx->stream>>>(ctx->V, (float *)dst, (int64_t)N);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(ctx->stream));
+    return PDD_OK;
+}
+
+pdd_status pdd_set_values(pdd_ctx *ctx, const double *src, int32_t src_on_device)
+{
+    if (!ctx || !src) return fail(ctx, PDD_E_INVALID, "NULL argument");
+    const size_t N = (size_t)ctx->fine.n * ctx->fine.n;
+    CK(cudaMemcpyAsync(ctx->V, src, sizeof(double) * N,
+                       src_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return PDD_OK;
+}
+
+pdd_status pdd_get_uhat(pdd_ctx *ctx, double *dst, int32_t on_device)
+{
+    if (!ctx) return fail(nullptr, PDD_E_INVALID, "ctx is NULL");
+    if (!ctx->synth_done) return fail(ctx, PDD_E_STATE, "u_hat not computed (pdd_synthesize)");
+    return fetch(ctx, dst, ctx->uhat, sizeof(double) * ctx->fine.n * ctx->fine.n, on_device);
+}
+
+pdd_status pdd_get_coarse_values(pdd_ctx *ctx, double *dst, int32_t on_device)
+{
+    if (!ctx) return fail(nullptr, PDD_E_INVALID, "ctx is NULL");
+    if (!ctx->coarse_done) return fail(ctx, PDD_E_STATE, "u_c not computed (pdd_coarse_solve)");
+    return fetch(ctx, dst, ctx->uc_final, sizeof(double) * ctx->coarse.n * ctx->coarse.n, on_device);
+}
+
+pdd_status pdd_get_controls(pdd_ctx *ctx, uint8_t *dst, int32_t on_device)
+{
+    if (!ctx) return fail(nullptr, PDD_E_INVALID, "ctx is NULL");
+    if (!ctx->synth_done) return fail(ctx, PDD_E_STATE, "a* not computed (pdd_synthesize)");
+    return fetch(ctx, dst, ctx->astar, (size_t)ctx->fine.n * ctx->fine.n, on_device);
+}
+
+pdd_status pdd_get_labels(pdd_ctx *ctx, int16_t *dst, int32_t on_device)
+{
+    if (!ctx) return fail(nullptr, PDD_E_INVALID, "ctx is NULL");
+    if (!ctx->labels_mode) return fail(ctx, PDD_E_STATE, "labels not built");
+    return fetch(ctx, dst, ctx->labels, sizeof(int16_t) * ctx->fine.n * ctx->fine.n, on_device);
+}
+
+pdd_status pdd_get_successors(pdd_ctx *ctx, int32_t *dst, int32_t on_device)
+{
+    if (!ctx) return fail(nullptr, PDD_E_INVALID, "ctx is NULL");
+    if (ctx->labels_mode != 1) return fail(ctx, PDD_E_STATE, "successors not built (pdd_build_patches)");
+    return fetch(ctx, dst, ctx->succ0, sizeof(int32_t) * ctx->fine.n * ctx->fine.n, on_device);
+}
+
+}  // extern "C"

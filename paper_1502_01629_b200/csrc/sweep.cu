@@ -1,0 +1,558 @@
+// sweep.cu -- the hot path: the semi-Lagrangian value-iteration sweep of the self-dependency-free
+// scheme (SLscheme3; discount R1-R3) on the fine grid, run over an active-tile list.
+//
+// One CTA (8 warps) per active tile of TH x TW nodes.  The CTA stages the tile plus a halo of H
+// cells (H = ceil(reach) + 1, R4) of V in shared memory, relative to a per-tile reference value
+// V_ref (u = V - V_ref; fp32 or fp64 arithmetic, fp64 storage in HBM, R27), relaxes it k_inner
+// times in place (chaotic relaxation: a valid schedule of the same monotone contraction, so it
+// converges to the same fixed point, P:452-472 + R29), then writes changed nodes back.
+//
+// Thread mapping ("lane = control"): a warp walks the nodes of one row left to right; lane L
+// holds controls k = L + 32 c (c < CPL) and computes their candidate values, then a 5-step
+// __shfl_xor_sync butterfly takes the min over controls (the discrete min of P:376-377).
+//
+// Two stencil paths:
+//  * general (path 1): every lane evaluates its controls' 2p foot points
+//        x_i + h f(x_i, a_k) +- sqrt(h p) sigma_j(x_i),   f = c(x) a + d(x)
+//    in cell units relative to the node (no absolute coordinates: fp32-safe at 8193^2),
+//    clamps them to the box (R5), gathers the 4 bilinear corners from shared memory, removes
+//    the node's own corner (its weight goes to Lambda0) and combines
+//        v_k - V_ref = (D + beta w R'_k) / (1 - beta w Lambda0_k),  D = h l - (1 - beta) V_ref
+//    (the same operator written relative to V_ref; exact algebra, R27).
+//  * row-table (path 2): when c, d and sigma depend on x2 only (C1, C2, C4, C5), every interior
+//    node of a row has the same stencil per control.  A host-built table holds, per (row,
+//    control), the branch-merged compact stencil: window origin (oy, ox), WY x WX weights
+//    W = beta w lambda / (1 - beta Lambda0) and E = 1/(1 - beta Lambda0).  Each lane keeps its
+//    controls' weights and a WY x WX window of u in registers and slides the window along the
+//    row: per node and control it loads WY new values (conflict-free: the pitch is chosen so
+//    the distinct window origins of a warp fall in distinct banks) and issues WY*WX FFMAs.
+//    Nodes within H of the x-boundary (x clamping) and Dirichlet nodes fall back to the general
+//    stencil / are skipped (warp-uniform branches on per-row ballot masks).
+// Check mode (K10 of SURVEY.md): one pure Jacobi pass, no update; residual per tile, optional
+// output T(V) (pdd_apply_operator).
+#include "pdd_internal.cuh"
+
+#include <math.h>
+#include <stdio.h>
+
+namespace pdd {
+
+constexpr int TH = 32;          // tile rows
+constexpr int NW = 8;           // warps per CTA
+constexpr int RPW = TH / NW;    // rows per warp
+constexpr int TW_GENERAL = 64;
+constexpr unsigned FULL = 0xffffffffu;
+
+template <int WY, int WX>
+struct TWOf { static constexpr int value = WX * (64 / WX); };   // multiple of WX, <= 64
+
+int rowtab_tw(int WY, int WX) { (void)WY; return WX * (64 / WX); }
+
+bool rowtab_supported(int WY, int WX, int cpl)
+{
+    return cpl >= 1 && cpl <= 2 &&
+           ((WY == 3 && WX == 3) || (WY == 2 && WX == 5) || (WY == 4 && WX == 4));
+}
+
+size_t rowtab_entry_bytes(int precision, int WY, int WX)
+{
+    if (precision == 32) {
+        if (WY == 3 && WX == 3) return sizeof(RowEntry<float, 3, 3>);
+        if (WY == 2 && WX == 5) return sizeof(RowEntry<float, 2, 5>);
+        return sizeof(RowEntry<float, 4, 4>);
+    }
+    if (WY == 3 && WX == 3) return sizeof(RowEntry<double, 3, 3>);
+    if (WY == 2 && WX == 5) return sizeof(RowEntry<double, 2, 5>);
+    return sizeof(RowEntry<double, 4, 4>);
+}
+
+template <typename real>
+struct KP {
+    DProblem P;
+    double *V;
+    TileGeom g;
+    const int32_t *list;
+    double *tile_res, *tile_chg;
+    int k_inner;
+    double *out;
+    const void *rowtab;
+    int na_pad;
+    int Hx;
+};
+
+__device__ __forceinline__ float rmin(float a, float b) { return fminf(a, b); }
+__device__ __forceinline__ double rmin(double a, double b) { return fmin(a, b); }
+__device__ __forceinline__ float rmax(float a, float b) { return fmaxf(a, b); }
+__device__ __forceinline__ double rmax(double a, double b) { return fmax(a, b); }
+__device__ __forceinline__ float rfloor(float a) { return floorf(a); }
+__device__ __forceinline__ double rfloor(double a) { return floor(a); }
+__device__ __forceinline__ float rabs(float a) { return fabsf(a); }
+__device__ __forceinline__ double rabs(double a) { return fabs(a); }
+template <typename real> __device__ __forceinline__ real rinf();
+template <> __device__ __forceinline__ float rinf<float>() { return __int_as_float(0x7f800000); }
+template <> __device__ __forceinline__ double rinf<double>() { return __longlong_as_double(0x7ff0000000000000LL); }
+
+template <typename real>
+__device__ __forceinline__ real warp_min(real v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = rmin(v, __shfl_xor_sync(FULL, v, o));
+    return v;
+}
+
+// General stencil at one node (lane = control).  base points at the node in shared memory.
+template <typename real>
+__device__ __forceinline__ real general_node(const DProblem &P, const real *__restrict__ s_ctrl,
+                                          const real *base, int pitch, int gi, int gj, real D)
+{
+    const int lane = threadIdx.x & 31;
+    const int n = P.n;
+    const real c = (real)coef_at(P.speed, gi, gj, n);
+    const real d1 = (real)coef_at(P.drift[0], gi, gj, n);
+    const real d2 = (real)coef_at(P.drift[1], gi, gj, n);
+    const int p = P.p;
+    const int nb = p > 0 ? 2 * p : 1;
+    real off[2][2] = {{0, 0}, {0, 0}};
+    for (int k = 0; k < p; ++k) {
+        off[k][0] = (real)(P.sc * coef_at(P.sigma[k][0], gi, gj, n));
+        off[k][1] = (real)(P.sc * coef_at(P.sigma[k][1], gi, gj, n));
+    }
+    const real q = (real)P.q, beta = (real)P.beta;
+    const real bw = (real)(P.beta / (double)nb);
+    const real xlo = (real)(-gi), xhi = (real)(n - 1 - gi);
+    const real ylo = (real)(-gj), yhi = (real)(n - 1 - gj);
+    const real cxm = (real)(n - 2 - gi), cym = (real)(n - 2 - gj);
+    const real uself = *base;
+    (void)beta;
+    real best = rinf<real>();
+    for (int k = lane; k < P.na; k += 32) {
+        const real bx = q * (c * s_ctrl[2 * k] + d1);
+        const real by = q * (c * s_ctrl[2 * k + 1] + d2);
+        real R = 0, L0 = 0;
+        for (int b = 0; b < nb; ++b) {
+            real xr = bx, yr = by;
+            if (p > 0) {
+                const int kk = b >> 1;
+                if (b & 1) { xr -= off[kk][0]; yr -= off[kk][1]; }
+                else       { xr += off[kk][0]; yr += off[kk][1]; }
+            }
+            xr = rmin(rmax(xr, xlo), xhi);
+            yr = rmin(rmax(yr, ylo), yhi);
+            const real fx = rmin(rfloor(xr), cxm);
+            const real fy = rmin(rfloor(yr), cym);
+            const real tx = xr - fx, ty = yr - fy;
+            const real *pc = base + (int)fy * pitch + (int)fx;
+            const real u00 = pc[0], u10 = pc[1], u01 = pc[pitch], u11 = pc[pitch + 1];
+            const real a0 = u00 + tx * (u10 - u00);
+            const real a1 = u01 + tx * (u11 - u01);
+            const real val = a0 + ty * (a1 - a0);
+            const real ws = rmax((real)0, (real)1 - rabs(xr)) * rmax((real)0, (real)1 - rabs(yr));
+            R += val - ws * uself;
+            L0 += ws;
+        }
+        const real v = (D + bw * R) / ((real)1 - bw * L0);
+        best = rmin(best, v);
+    }
+    return warp_min(best);
+}
+
+// per-row ballot masks: bit lx set = Dirichlet or outside the grid (dmask) / needs the general
+// stencil because its feet may be clamped in x (emask)
+__device__ __forceinline__ void row_masks(const DProblem &P, int TW, int i0, int gj, int Hx,
+                                          unsigned long long &dmask, unsigned long long &emask)
+{
+    const int lane = threadIdx.x & 31;
+    const int n = P.n;
+    dmask = 0ull;
+    emask = 0ull;
+    for (int part = 0; part < (TW + 31) / 32; ++part) {
+        const int lx = part * 32 + lane;
+        const int gi = i0 + lx;
+        const bool oob = lx >= TW || gi >= n;
+        const bool dir = oob || P.kind[(int64_t)gj * n + gi] != 0;
+        const bool edge = !dir && (gi < Hx || gi > n - 1 - Hx);
+        dmask |= (unsigned long long)__ballot_sync(FULL, dir) << (32 * part);
+        emask |= (unsigned long long)__ballot_sync(FULL, edge) << (32 * part);
+    }
+}
+
+template <typename real, bool CHECK>
+__device__ __forceinline__ void commit_node(real *p, real best, bool last, real &res,
+                                            double *out, int64_t gidx, double Vref)
+{
+    if ((threadIdx.x & 31) == 0) {
+        const real old = *p;
+        if (last) res = rmax(res, rabs(best - old));
+        if (!CHECK) *p = best;
+        else if (out) out[gidx] = Vref + (double)best;
+    }
+}
+
+// ------------------------------------------------------------------ row processors
+template <typename real, bool CHECK>
+__device__ __forceinline__ void row_general(const KP<real> &A, real *s_u, const real *s_ctrl,
+                                            int pitch, int H, int TW, int i0, int ly, int gj,
+                                            real D, bool last, real &res, double Vref)
+{
+    unsigned long long dmask, emask;
+    row_masks(A.P, TW, i0, gj, 0, dmask, emask);
+    const int n = A.P.n;
+    real *rowp = s_u + (ly + H) * pitch + H;
+    for (int lx = 0; lx < TW; ++lx) {
+        if ((dmask >> lx) & 1ull) continue;
+        const int gi = i0 + lx;
+        const real best = general_node<real>(A.P, s_ctrl, rowp + lx, pitch, gi, gj, D);
+        commit_node<real, CHECK>(rowp + lx, best, last, res, A.out, (int64_t)gj * n + gi, Vref);
+    }
+}
+
+template <typename real, int CPL, int WY, int WX, bool CHECK>
+__device__ __forceinline__ void row_table(const KP<real> &A, real *s_u, const real *s_ctrl,
+                                          int pitch, int H, int i0, int ly, int gj, real D,
+                                          bool last, real &res, double Vref)
+{
+    constexpr int TW = TWOf<WY, WX>::value;
+    const int lane = threadIdx.x & 31;
+    const int n = A.P.n;
+    unsigned long long dmask, emask;
+    row_masks(A.P, TW, i0, gj, A.Hx, dmask, emask);
+
+    const RowEntry<real, WY, WX> *tab =
+        reinterpret_cast<const RowEntry<real, WY, WX> *>(A.rowtab) + (int64_t)gj * A.na_pad;
+    real Wt[CPL][WY * WX];
+    real c0[CPL];
+    int base[CPL];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+        const int k = lane + 32 * c;
+        const RowEntry<real, WY, WX> &e = tab[k];
+        c0[c] = k < A.P.na ? D * e.E : rinf<real>();
+#pragma unroll
+        for (int m = 0; m < WY * WX; ++m) Wt[c][m] = e.W[m];
+        base[c] = (ly + H + e.oy) * pitch + H + e.ox;
+    }
+    real win[CPL][WY][WX];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c)
+#pragma unroll
+        for (int r = 0; r < WY; ++r)
+#pragma unroll
+            for (int x = 0; x < WX - 1; ++x) win[c][r][x] = s_u[base[c] + r * pitch + x];
+
+    real *rowp = s_u + (ly + H) * pitch + H;
+    for (int g = 0; g < TW; g += WX) {
+#pragma unroll
+        for (int s = 0; s < WX; ++s) {
+            const int lx = g + s;
+#pragma unroll
+            for (int c = 0; c < CPL; ++c)
+#pragma unroll
+                for (int r = 0; r < WY; ++r)
+                    win[c][r][(s + WX - 1) % WX] = s_u[base[c] + r * pitch + lx + WX - 1];
+            if (((dmask | emask) >> lx) & 1ull) continue;
+            real best = rinf<real>();
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) {
+                real acc = c0[c];
+#pragma unroll
+                for (int r = 0; r < WY; ++r)
+#pragma unroll
+                    for (int x = 0; x < WX; ++x)
+                        acc = fma(Wt[c][r * WX + x], win[c][r][(s + x) % WX], acc);
+                best = rmin(best, acc);
+            }
+            best = warp_min(best);
+            commit_node<real, CHECK>(rowp + lx, best, last, res, A.out,
+                                     (int64_t)gj * n + i0 + lx, Vref);
+        }
+    }
+    // nodes whose feet may be clamped in x: general stencil (same Jacobi-in-row semantics)
+    unsigned long long em = emask & ~dmask;
+    while (em) {
+        const int lx = __ffsll((long long)em) - 1;
+        em &= em - 1;
+        const real best = general_node<real>(A.P, s_ctrl, rowp + lx, pitch, i0 + lx, gj, D);
+        commit_node<real, CHECK>(rowp + lx, best, last, res, A.out, (int64_t)gj * n + i0 + lx,
+                                 Vref);
+    }
+}
+
+// ------------------------------------------------------------------ the tile kernel
+template <typename real, int PATH, int CPL, int WY, int WX, bool CHECK>
+__global__ void __launch_bounds__(NW * 32) k_sweep(KP<real> A)
+{
+    constexpr int TW = PATH == 2 ? TWOf<WY, WX>::value : TW_GENERAL;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double *s_red = reinterpret_cast<double *>(smem_raw);            // NW
+    real *s_ctrl = reinterpret_cast<real *>(s_red + NW);              // 2 * 128
+    real *s_u = s_ctrl + 256;
+    const int H = A.g.H, pitch = A.g.pitch;
+    const int n = A.P.n;
+    const int t = A.list[blockIdx.x];
+    const int i0 = (t % A.g.tiles_x) * TW;
+    const int j0 = (t / A.g.tiles_x) * TH;
+    const int ci = min(i0 + TW / 2, n - 1), cj = min(j0 + TH / 2, n - 1);
+    const double Vref = A.V[(int64_t)cj * n + ci];
+
+    // stage tile + halo (coalesced fp64 row reads, converted relative to V_ref)
+    const int W2 = TW + 2 * H, H2 = TH + 2 * H;
+    for (int e = threadIdx.x; e < H2 * W2; e += blockDim.x) {
+        const int r = e / W2, c = e - r * W2;
+        const int gj = j0 - H + r, gi = i0 - H + c;
+        real v = 0;
+        if (gj >= 0 && gj < n && gi >= 0 && gi < n) v = (real)(A.V[(int64_t)gj * n + gi] - Vref);
+        s_u[r * pitch + c] = v;
+    }
+    for (int e = threadIdx.x; e < 2 * A.P.na; e += blockDim.x) s_ctrl[e] = (real)A.P.ctrl[e];
+    __syncthreads();
+
+    // D = h l - (1 - beta) V_ref (constant cost; a cost field uses D per node in general path)
+    const real D = (real)(A.P.h * A.P.lmax - (1.0 - A.P.beta) * Vref);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    real res = 0;
+    const int sweeps = CHECK ? 1 : A.k_inner;
+    for (int sw = 0; sw < sweeps; ++sw) {
+        const bool last = sw == sweeps - 1;
+        for (int rr = 0; rr < RPW; ++rr) {
+            const int ly = warp * RPW + ((sw & 1) ? RPW - 1 - rr : rr);
+            const int gj = j0 + ly;
+            if (gj >= n) continue;
+            if (PATH == 2)
+                row_table<real, CPL, WY, WX, CHECK>(A, s_u, s_ctrl, pitch, H, i0, ly, gj, D,
+                                                    last, res, Vref);
+            else
+                row_general<real, CHECK>(A, s_u, s_ctrl, pitch, H, TW, i0, ly, gj, D, last,
+                                         res, Vref);
+        }
+        if (!CHECK) __syncthreads();
+    }
+
+    // tile residual of the last sweep
+    if (lane == 0) s_red[warp] = (double)res;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double m = 0.0;
+        for (int w = 0; w < NW; ++w) m = fmax(m, s_red[w]);
+        A.tile_res[t] = m;
+    }
+    if (CHECK) return;
+    __syncthreads();
+
+    // write back changed interior nodes, net change of the visit
+    double chg = 0.0;
+    for (int e = threadIdx.x; e < TH * TW; e += blockDim.x) {
+        const int ly = e / TW, lx = e - ly * TW;
+        const int gi = i0 + lx, gj = j0 + ly;
+        if (gi >= n || gj >= n) continue;
+        const int64_t gidx = (int64_t)gj * n + gi;
+        if (A.P.kind[gidx] != 0) continue;
+        const real u = s_u[(ly + H) * pitch + lx + H];
+        const double vold = A.V[gidx];
+        const real uold = (real)(vold - Vref);
+        if (u != uold) {
+            A.V[gidx] = Vref + (double)u;
+            chg = fmax(chg, fabs((double)u - (double)uold));
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) chg = fmax(chg, __shfl_xor_sync(FULL, chg, o));
+    if (lane == 0) s_red[warp] = chg;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double m = 0.0;
+        for (int w = 0; w < NW; ++w) m = fmax(m, s_red[w]);
+        A.tile_chg[t] = m;
+    }
+}
+
+template <typename real, int PATH, int CPL, int WY, int WX, bool CHECK>
+static cudaError_t launch_one(const SweepLaunch &L, cudaStream_t s)
+{
+    KP<real> A;
+    A.P = L.P;
+    A.V = L.V;
+    A.g = L.g;
+    A.list = L.list;
+    A.tile_res = L.tile_res;
+    A.tile_chg = L.tile_chg;
+    A.k_inner = L.k_inner;
+    A.out = L.out;
+    A.rowtab = L.rowtab;
+    A.na_pad = L.na_pad;
+    A.Hx = L.Hx;
+    const size_t smem = NW * sizeof(double) + 256 * sizeof(real) +
+                        (size_t)(TH + 2 * L.g.H) * L.g.pitch * sizeof(real);
+    auto kern = k_sweep<real, PATH, CPL, WY, WX, CHECK>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    if (L.n_list <= 0) return cudaSuccess;
+    kern<<<L.n_list, NW * 32, smem, s>>>(A);
+    return cudaGetLastError();
+}
+
+template <typename real, bool CHECK>
+static cudaError_t dispatch(const SweepLaunch &L, cudaStream_t s)
+{
+    if (L.path == 1) return launch_one<real, 1, 1, 1, 1, CHECK>(L, s);
+    const int cpl = L.na_pad / 32;
+#define PDD_RT(WY_, WX_)                                                                     \
+    if (L.WY == WY_ && L.WX == WX_) {                                                        \
+        if (cpl == 1) return launch_one<real, 2, 1, WY_, WX_, CHECK>(L, s);                  \
+        return launch_one<real, 2, 2, WY_, WX_, CHECK>(L, s);                                \
+    }
+    PDD_RT(3, 3)
+    PDD_RT(2, 5)
+    PDD_RT(4, 4)
+#undef PDD_RT
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_sweep(const SweepLaunch &L, cudaStream_t s)
+{
+    if (L.precision == 32) return L.check ? dispatch<float, true>(L, s) : dispatch<float, false>(L, s);
+    return L.check ? dispatch<double, true>(L, s) : dispatch<double, false>(L, s);
+}
+
+// ------------------------------------------------------------------ tile bookkeeping
+__global__ void k_tile_init(DProblem P, TileGeom g, const double *uhat, const int16_t *labels,
+                            TileState T)
+{
+    __shared__ int s_free;
+    __shared__ unsigned long long s_min;
+    __shared__ int s_lab[4];
+    const int t = blockIdx.x;
+    const int i0 = (t % g.tiles_x) * g.TW, j0 = (t / g.tiles_x) * g.TH;
+    const int n = P.n;
+    if (threadIdx.x == 0) {
+        s_free = 0;
+        s_min = 0xffffffffffffffffull;
+        for (int k = 0; k < 4; ++k) s_lab[k] = -1;
+    }
+    __syncthreads();
+    int cnt = 0;
+    double mn = INFINITY;
+    for (int e = threadIdx.x; e < g.TW * g.TH; e += blockDim.x) {
+        const int ly = e / g.TW, lx = e - ly * g.TW;
+        const int gi = i0 + lx, gj = j0 + ly;
+        if (gi >= n || gj >= n) continue;
+        const int64_t k = (int64_t)gj * n + gi;
+        if (P.kind[k] != 0) continue;
+        ++cnt;
+        if (uhat) mn = fmin(mn, uhat[k]);
+        if (labels) {
+            const int lab = labels[k];
+            if (lab >= 0) {
+                for (int sl = 0; sl < 4; ++sl) {
+                    const int old = atomicCAS(&s_lab[sl], -1, lab);
+                    if (old == -1 || old == lab) break;
+                }
+            }
+        }
+    }
+    atomicAdd(&s_free, cnt);
+    if (mn < INFINITY) atomicMin(&s_min, (unsigned long long)__double_as_longlong(fmax(mn, 0.0)));
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        T.tile_free[t] = s_free;
+        T.tile_minu[t] = uhat ? (s_free > 0 ? __longlong_as_double((long long)s_min) : INFINITY) : 0.0;
+        T.tile_res[t] = s_free > 0 ? INFINITY : 0.0;
+        T.tile_chg[t] = 0.0;
+        for (int k = 0; k < 4; ++k) T.tile_lab[4 * t + k] = (int16_t)s_lab[k];
+    }
+}
+
+void launch_tile_init(const DProblem &P, const TileGeom &g, const double *uhat,
+                      const int16_t *labels, TileState &T, cudaStream_t s)
+{
+    k_tile_init<<<g.tiles_x * g.tiles_y, 256, 0, s>>>(P, g, uhat, labels, T);
+}
+
+__global__ void k_set_values(DProblem P, int mode, const double *uhat, double *V)
+{
+    const int64_t N = (int64_t)P.n * P.n;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < N;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const uint8_t kd = P.kind[k];
+        V[k] = kd == 1 ? 0.0 : kd == 2 ? 1.0 / P.lambda : (mode == 0 ? uhat[k] : P.v0);
+    }
+}
+
+void launch_set_values(const DProblem &P, int mode, const double *uhat, double *V,
+                       cudaStream_t s)
+{
+    const int64_t N = (int64_t)P.n * P.n;
+    int64_t grid = (N + 255) / 256;
+    if (grid > 148 * 32) grid = 148 * 32;
+    k_set_values<<<(int)grid, 256, 0, s>>>(P, mode, uhat, V);
+}
+
+__global__ void k_activate(TileGeom g, TileState T, int out_list, double tol, double tol_act,
+                           double thr, int round, int n_tiles)
+{
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    ActCounters *C = reinterpret_cast<ActCounters *>(T.counters);
+    bool take = false;
+    int fr = 0;
+    if (t < n_tiles) {
+        fr = T.tile_free[t];
+        if (fr > 0) {
+            const double r = T.tile_res[t];
+            atomicMax(&C->max_res, (unsigned long long)__double_as_longlong(fmax(r, 0.0)));
+            bool need = r >= tol;
+            if (!need) {
+                const int tx = t % g.tiles_x, ty = t / g.tiles_x;
+                for (int dy = -1; dy <= 1 && !need; ++dy)
+                    for (int dx = -1; dx <= 1; ++dx) {
+                        const int ax = tx + dx, ay = ty + dy;
+                        if ((dx | dy) == 0 || ax < 0 || ay < 0 || ax >= g.tiles_x || ay >= g.tiles_y)
+                            continue;
+                        if (T.tile_chg[ay * g.tiles_x + ax] >= tol_act) { need = true; break; }
+                    }
+            }
+            if (need) {
+                const double mu = T.tile_minu[t];
+                if (mu <= thr) {
+                    take = true;
+                    for (int k = 0; k < 4; ++k) {
+                        const int lab = T.tile_lab[4 * t + k];
+                        if (lab >= 0) {
+                            atomicMax(&T.patch_round[lab], round);
+                            atomicMax(reinterpret_cast<unsigned long long *>(&T.patch_res[lab]),
+                                      (unsigned long long)__double_as_longlong(fmin(r, 1e300)));
+                        }
+                    }
+                } else {
+                    atomicMin(&C->min_pending, (unsigned long long)__double_as_longlong(fmax(mu, 0.0)));
+                }
+            }
+        }
+    }
+    // warp-aggregated append
+    const unsigned m = __ballot_sync(FULL, take);
+    if (m) {
+        const int lane = threadIdx.x & 31;
+        const int leader = __ffs(m) - 1;
+        int basei = 0;
+        long long fsum = 0;
+        if (take) fsum = fr;
+        for (int o = 16; o > 0; o >>= 1) fsum += __shfl_xor_sync(FULL, fsum, o);
+        if (lane == leader) {
+            basei = atomicAdd(&C->count, __popc(m));
+            atomicAdd(reinterpret_cast<unsigned long long *>(&C->free_sum), (unsigned long long)fsum);
+        }
+        basei = __shfl_sync(FULL, basei, leader);
+        if (take) T.list[out_list][basei + __popc(m & ((1u << lane) - 1u))] = t;
+    }
+}
+
+void launch_activate(const TileGeom &g, TileState &T, int out_list, double tol, double tol_act,
+                     double thr, int round, int n_tiles, cudaStream_t s)
+{
+    k_activate<<<(n_tiles + 255) / 256, 256, 0, s>>>(g, T, out_list, tol, tol_act, thr, round,
+                                                     n_tiles);
+}
+
+}  // namespace pdd

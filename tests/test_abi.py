@@ -1,0 +1,101 @@
+"""CPU-side checks of the boundary: libpdd.so loads and exports every symbol include/pdd.h
+declares; the ctypes structs match the header's layout; argument validation errors are
+reported without touching a GPU.  (No compute calls: there is no GPU here.)"""
+import ctypes as C
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "pdd.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_1502_01629_b200 import build as B
+    B.build()
+    from paper_1502_01629_b200 import _native as N
+    return N.lib()
+
+
+def _declared():
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(pdd_[a-z_]+)\s*\(", txt)))
+
+
+def test_header_symbols_exported(lib):
+    from paper_1502_01629_b200 import _native as N
+    declared = _declared()
+    out = subprocess.run(["nm", "-D", "--defined-only", N.LIB_PATH], capture_output=True,
+                         text=True, check=True).stdout
+    exported = set(re.findall(r" T (pdd_\w+)", out))
+    missing = [d for d in declared if d not in exported]
+    assert not missing, missing
+    assert sorted(N.EXPORTS) == declared
+
+
+def test_library_is_sm100a(lib):
+    from paper_1502_01629_b200 import _native as N
+    out = subprocess.run(["cuobjdump", "--list-elf", N.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_struct_sizes_match_c(tmp_path):
+    """Compile a tiny C program against include/pdd.h and compare sizeof/offsetof with ctypes."""
+    from paper_1502_01629_b200 import _native as N
+    src = tmp_path / "sz.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "pdd.h"\nint main(){'
+                   'printf("%zu %zu %zu %zu %zu %zu %zu\\n", sizeof(pdd_problem), sizeof(pdd_coef),'
+                   'sizeof(pdd_solve_opts), sizeof(pdd_solve_stats), sizeof(pdd_coarse_stats),'
+                   'offsetof(pdd_problem, kind), offsetof(pdd_problem, sigma));return 0;}')
+    exe = tmp_path / "sz"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    vals = list(map(int, subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()))
+    py = [C.sizeof(N.pdd_problem), C.sizeof(N.pdd_coef), C.sizeof(N.pdd_solve_opts),
+          C.sizeof(N.pdd_solve_stats), C.sizeof(N.pdd_coarse_stats),
+          N.pdd_problem.kind.offset, N.pdd_problem.sigma.offset]
+    assert vals == py
+
+
+def test_validation_errors_without_gpu(lib):
+    """pdd_workspace_bytes validates the problem on the host."""
+    import pdd_inputs as I
+    from paper_1502_01629_b200 import _ProblemView, _native as N
+    inst = I.make_config("C1")
+    v = _ProblemView(inst)
+    nb = C.c_size_t(0)
+    assert lib.pdd_workspace_bytes(C.byref(v.s), None, 32, C.byref(nb)) == N.PDD_OK
+    assert nb.value > 8 * inst.n * inst.n
+    bad = _ProblemView(inst)
+    bad.s.n = 2
+    assert lib.pdd_workspace_bytes(C.byref(bad.s), None, 32, C.byref(nb)) == N.PDD_E_INVALID
+    assert b"n = 2" in lib.pdd_last_error(None)
+    bad = _ProblemView(inst)
+    bad.s.n_controls = 0
+    assert lib.pdd_workspace_bytes(C.byref(bad.s), None, 32, C.byref(nb)) == N.PDD_E_INVALID
+    bad = _ProblemView(inst)
+    bad.s.lam = 0.0
+    assert lib.pdd_workspace_bytes(C.byref(bad.s), None, 32, C.byref(nb)) == N.PDD_E_INVALID
+    assert lib.pdd_workspace_bytes(C.byref(v.s), None, 16, C.byref(nb)) == N.PDD_E_INVALID
+    bad = _ProblemView(inst)
+    bad.s.cost.value = 0.0
+    assert lib.pdd_workspace_bytes(C.byref(bad.s), None, 32, C.byref(nb)) == N.PDD_E_INVALID
+
+
+def test_workspace_scales_with_grid(lib):
+    import pdd_inputs as I
+    from paper_1502_01629_b200 import _ProblemView
+    sizes = []
+    for n in (201, 401, 801):
+        inst = I.make_config("C2", n=n)
+        f, c = _ProblemView(inst), _ProblemView(inst.coarse, False)
+        nb = C.c_size_t(0)
+        assert lib.pdd_workspace_bytes(C.byref(f.s), C.byref(c.s), 32, C.byref(nb)) == 0
+        sizes.append(nb.value)
+    # the per-node arrays dominate the growth: doubling n quadruples the increment
+    r = (sizes[2] - sizes[1]) / (sizes[1] - sizes[0])
+    assert 3.5 < r < 4.5

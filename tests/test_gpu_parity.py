@@ -1,0 +1,131 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on the same seeded inputs.
+
+Bars (north_star / BASELINE.json acceptance criteria):
+  * integer and index outputs (a*, patch labels, static labels) and the canonical fp64 stages
+    (u_c, u_hat): bit-exact;
+  * V: max |dV| <= 1e-10 in fp64 mode, <= 5e-5 max|V| in fp32 mode;
+  * the operator T applied to the same V: fp64 <= 1e-12 abs, fp32 <= 2e-6 max|V| (one
+    application; R27 arithmetic).
+Sizes: the configs' own grids where the oracle finishes in seconds (C1, C2 and every coarse
+grid), the same physics on reduced grids (C3-C5 at 257..513 nodes: several tiles and a ragged
+tail), and full-size sampled checks in test_gpu_fullsize.py.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import pdd_inputs as I
+
+pytestmark = pytest.mark.gpu
+
+
+def _solver(inst, precision):
+    from paper_1502_01629_b200 import Solver
+    return Solver(inst, precision=precision)
+
+
+CASES_COARSE = [("C2", None), ("C3", None), ("C4", None), ("C5", 1025), ("C3", 257), ("C4", 513)]
+
+
+@pytest.mark.parametrize("cfg,n", CASES_COARSE)
+def test_coarse_uhat_astar_bitexact(cfg, n):
+    inst = I.make_config(cfg, n=n)
+    ref = O.coarse_solve(inst)
+    s = _solver(inst, 32)
+    st = s.coarse_solve(inst.tol_coarse)
+    uc = s.get_coarse_values()
+    assert st["sweeps"] == ref["sweeps"]
+    assert np.array_equal(uc.view(np.uint64), ref["V"].view(np.uint64))
+    s.synthesize()
+    uhat = s.get_uhat()
+    uref = O.prolong(inst.coarse.n, ref["V"], inst.n)
+    assert np.array_equal(uhat.view(np.uint64), uref.view(np.uint64))
+    a = s.get_controls()
+    aref = O.synthesize(inst, uref)
+    assert np.array_equal(a, aref)
+
+
+@pytest.mark.parametrize("cfg,n", [("C2", None), ("C3", 257), ("C4", 513), ("C5", 513), ("C5", 1025)])
+def test_labels_bitexact(cfg, n):
+    inst = I.make_config(cfg, n=n)
+    ref = O.solve_pipeline(inst, fine=False)
+    s = _solver(inst, 32)
+    s.coarse_solve(inst.tol_coarse)
+    s.synthesize()
+    s.build_patches(inst.n_patches)
+    succ = s.get_successors()
+    assert np.array_equal(succ.astype(np.int64), ref["succ"])
+    lab = s.get_labels()
+    assert np.array_equal(lab, ref["labels"])
+    s.build_static(*inst.static_blocks)
+    assert np.array_equal(s.get_labels(), ref["static_labels"])
+
+
+def _random_field(inst, seed):
+    rng = np.random.default_rng(seed)
+    n = inst.n
+    x = inst.x(np.arange(n))
+    X, Y = np.meshgrid(x, x, indexing="xy")
+    V = (0.4 * np.hypot(X, Y) + 0.05 * np.sin(7 * X) * np.cos(5 * Y)).reshape(-1)
+    V = V + 1e-3 * rng.standard_normal(V.size)
+    V[inst.kind == I.KIND_TARGET] = 0.0
+    V[inst.kind == I.KIND_OBSTACLE] = 1.0 / inst.lam
+    return V
+
+
+@pytest.mark.parametrize("cfg,n", [("C1", None), ("C2", 201), ("C3", 257), ("C4", 257), ("C5", 257)])
+@pytest.mark.parametrize("precision", [64, 32])
+@pytest.mark.parametrize("kernel", [1, 0])
+def test_operator_parity(cfg, n, precision, kernel):
+    inst = I.make_config(cfg, n=n)
+    V = _random_field(inst, 3)
+    ref, _ = O.apply(inst, V)
+    s = _solver(inst, precision)
+    out, res = s.apply_operator(V, kernel=kernel)
+    err = np.abs(out - ref).max()
+    if precision == 64:
+        assert err < 1e-12
+    else:
+        assert err < 2e-6 * np.abs(V).max()
+    assert abs(res - np.abs(ref - V)[inst.kind == 0].max()) < (1e-12 if precision == 64 else 4e-6)
+
+
+def _tight_tol(inst, target):
+    # a Jacobi residual r bounds the distance to the fixed point by r/(1-beta) (contraction)
+    return target * (1.0 - inst.beta)
+
+
+@pytest.mark.parametrize("cfg,n,precision,mode", [
+    ("C1", None, 64, "static"),
+    ("C2", None, 64, "patchy"),
+    ("C2", None, 32, "patchy"),
+    ("C2", None, 32, "static"),
+    ("C3", 257, 32, "patchy"),
+    ("C3", 257, 64, "static"),
+    ("C4", 257, 32, "patchy"),
+    ("C4", 257, 32, "static"),
+    ("C5", 513, 32, "patchy"),
+    ("C5", 513, 64, "patchy"),
+    ("C5", 513, 32, "static"),
+])
+def test_solve_parity(cfg, n, precision, mode):
+    inst = I.make_config(cfg, n=n)
+    tol_o = _tight_tol(inst, 2e-11)
+    ref = O.jacobi(inst, tol=tol_o, max_sweeps=10**6)
+    s = _solver(inst, precision)
+    if mode == "patchy":
+        s.coarse_solve(inst.tol_coarse)
+        s.synthesize()
+        s.build_patches(inst.n_patches)
+    else:
+        s.build_static(*inst.static_blocks)
+    tol = _tight_tol(inst, 2e-11) if precision == 64 else 1e-7
+    st = s.solve(mode, tol=tol, k_inner=4)
+    assert st["converged"] == 1
+    V = s.get_values()
+    err = np.abs(V - ref["V"]).max()
+    if precision == 64:
+        assert err <= 1e-10, err
+    else:
+        assert err <= 5e-5 * np.abs(ref["V"]).max(), err
+    assert np.all(V[inst.kind == I.KIND_TARGET] == 0.0)
