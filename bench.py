@@ -1,0 +1,366 @@
+"""bench.py -- the hot path of arXiv 1502.01629 on B200, BASELINE.json metric
+"SL sweep node-updates/s, time-to-converge patchy vs static (1 B200)".
+
+A step = one pass of the whole hot path on config C5
+(8193^2 Zermelo navigation, 64 controls, 4 Markov branches, fp32 arithmetic): coarse solve on
+513^2 -> prolongation -> synthesis -> patch labels (256 patches) -> patchy fine solve until the
+full-grid Jacobi residual is < 1e-6 (verified).  Inputs are resident in HBM when the timed
+region starts (the problem arrays are uploaded once by pdd_create); V (fp64, 537 MB) and the
+other per-node arrays are larger than L2, so no flush is needed between steps.
+
+value      = free-node updates performed by the sweep kernel in the K timed steps, all ranks,
+             / max-over-ranks device time of the K steps (CUDA events, barrier + sync on both
+             sides).
+e2e        = same metric through the C ABI with HOST buffers: every step creates the context
+             from pinned host arrays (H2D inside the timed region), runs the pipeline and copies
+             V back to pinned host memory (D2H).
+roofline   = the sweep kernel (k_sweep): algorithmic fp32 flop per node-update
+             F = N_A * 2p * 4 * 2 (each of the 2p N_A bilinear reconstructions is a 4-term
+             multiply-add) times the updates of the timed region / the summed
+             duration of the sweep launches (CUDA events on the launching stream); peak = FP32
+             FMA rate derived from the guide's unit counts: 148 SMs x 128 lanes x 2 flop x
+             1965 MHz = 74.4 TFLOP/s ("bound": "alu").
+cpu_baseline = the fp64 oracle (oracle/, plain C + OpenMP on all host cores) applying the same
+             operator T to a bounded sample of the same grid (a band of rows of C5), in
+             node-updates/s.
+
+--impl reference : the oracle as the reference arm (this tier has no reference code): each step
+             is a bounded sample (one oracle Jacobi application to a band of C5 rows).
+--gpus N (torchrun): "replicas only": every rank solves its own copy; value sums
+             the ranks' updates over the max-over-ranks time; scaling "weak".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SL sweep node-updates/s, time-to-converge patchy vs static (1 B200)"
+UNIT = "node-updates/s"
+FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12      # 74.4
+FP64_PEAK_TFLOPS = FP32_PEAK_TFLOPS / 2.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--n", type=int, default=None, help="override grid size (not for the headline)")
+    ap.add_argument("--precision", type=int, default=32)
+    ap.add_argument("--k-inner", type=int, default=4)
+    ap.add_argument("--tol", type=float, default=1e-6)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-static", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- distributed
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def allreduce(val, op, world):
+    if world == 1:
+        return val
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(val)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=op)
+    return float(t.item())
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- oracle legs
+def oracle_sample(inst, seconds: float):
+    """Time the oracle's operator T (fp64, all host cores) on a band of rows of ``inst``,
+    sized to take about ``seconds``.  Returns (node-updates/s, description, threads)."""
+    import numpy as np
+    import oracle as O
+    n = inst.n
+    V = O.init_v0(inst)
+    rows0 = max(8, min(n, 64))
+    idx = np.arange(n * (n // 2), n * (n // 2) + rows0 * n, dtype=np.int64)
+    t = time.perf_counter()
+    O.apply_at(inst, V, idx)
+    dt = max(time.perf_counter() - t, 1e-6)
+    rate = idx.size / dt
+    rows = int(min(n, max(rows0, seconds * rate / n)))
+    j0 = max(0, n // 2 - rows // 2)
+    idx = np.arange(j0 * n, (j0 + rows) * n, dtype=np.int64)
+    t = time.perf_counter()
+    O.apply_at(inst, V, idx)
+    dt = time.perf_counter() - t
+    desc = (f"one fp64 application of the scheme's operator T (oracle, {O.num_threads()} threads) "
+            f"to {rows} full rows ({idx.size} nodes) of the {inst.name} grid ({n}^2), "
+            f"{dt:.1f} s")
+    return idx.size / dt, desc, O.num_threads(), dt
+
+
+def run_reference(args, world, rank):
+    import pdd_inputs as I
+    import oracle as O
+    if rank != 0:
+        return
+    inst = I.make_config(args.config, n=args.n)
+    per = max(2.0, min(args.cpu_seconds, 60.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        oracle_sample(inst, per / 4)
+    vals, times, desc = [], [], ""
+    for _ in range(args.steps):
+        v, desc, thr, dt = oracle_sample(inst, per)
+        vals.append(v)
+        times.append(dt)
+    value = sum(vals) / len(vals)
+    out = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{inst.name}: oracle operator application on a row band",
+                   "grid": inst.n, "controls": inst.n_controls, "branches": 2 * inst.p},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": thr, "kind": "oracle",
+                         "sample": desc},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+# ----------------------------------------------------------------------------- our arm
+def pipeline_step(s, inst, args, mode="patchy"):
+    """One pass of the hot path on a resident context; returns the fine-solve stats."""
+    if mode == "patchy":
+        s.coarse_solve(inst.tol_coarse)
+        s.synthesize()
+        s.build_patches(inst.n_patches)
+    else:
+        s.build_static(*inst.static_blocks)
+    return s.solve(mode, tol=args.tol, k_inner=args.k_inner)
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        barrier(world)
+        return
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import pdd_inputs as I
+    from paper_1502_01629_b200 import Solver
+
+    torch.cuda.set_device(local)
+    inst = I.make_config(args.config, n=args.n)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    s = Solver(inst, precision=args.precision, device=str(dev))
+
+    for _ in range(args.warmup):
+        pipeline_step(s, inst, args)
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    barrier(world)
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = s.kernel_launches()
+    ev0.record(stream)
+    nu, t_sweep, t_verify, rounds, t_solve = 0, 0.0, 0.0, 0, 0.0
+    for _ in range(args.steps):
+        st = pipeline_step(s, inst, args)
+        assert st["converged"] == 1
+        nu += st["node_updates"]
+        t_sweep += st["seconds_sweep"]
+        t_verify += st["seconds_verify"]
+        t_solve += st["seconds_total"]
+        rounds += st["rounds"]
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    launches = s.kernel_launches() - l0
+    clk = clocks.stop()
+    t_local = ev0.elapsed_time(ev1) * 1e-3
+    t_max = allreduce(t_local, dist.ReduceOp.MAX if world > 1 else None, world)
+    nu_all = allreduce(nu, dist.ReduceOp.SUM if world > 1 else None, world)
+    value = nu_all / t_max
+    last = st
+
+    # static decomposition on the same kernels (time-to-converge comparison)
+    static = None
+    if not args.no_static:
+        sst = pipeline_step(s, inst, args, mode="static")
+        static = {"time_to_converge_s": sst["seconds_total"], "rounds": sst["rounds"],
+                  "node_updates": sst["node_updates"],
+                  "sweep_equivalents": sst["node_updates"] / inst.free_count(),
+                  "kernel_node_updates_per_s": sst["node_updates"] / max(sst["seconds_sweep"], 1e-12),
+                  "converged": sst["converged"], "final_residual": sst["final_residual"]}
+
+    # end to end through the C ABI with host buffers
+    e2e = None
+    if not args.no_e2e:
+        views = Solver.make_views(inst, pin_host=True)
+        hostV = torch.empty(inst.n * inst.n, dtype=torch.float64 if args.precision == 64 else torch.float32).pin_memory()
+        h2d = sum(int(a.nbytes) for v in views if v is not None for a in v._keep
+                  if hasattr(a, "nbytes") and not hasattr(a, "pin_memory"))
+        del s
+        torch.cuda.synchronize()
+        barrier(world)
+        t0 = time.perf_counter()
+        e_nu = 0
+        for _ in range(max(1, min(args.steps, 2))):
+            se = Solver(inst, precision=args.precision, device=str(dev), views=views)
+            st_e = pipeline_step(se, inst, args)
+            se.get_values_into(hostV, on_device=False, as_fp64=(args.precision == 64))
+            e_nu += st_e["node_updates"]
+            se.close()
+            del se
+        torch.cuda.synchronize()
+        t_e = allreduce(time.perf_counter() - t0, dist.ReduceOp.MAX if world > 1 else None, world)
+        e_nu = allreduce(e_nu, dist.ReduceOp.SUM if world > 1 else None, world)
+        e2e = {"value": e_nu / t_e, "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": int(hostV.numel() * hostV.element_size())}
+
+    flop_per_update = inst.n_controls * 2 * max(1, inst.p) * 4 * 2
+    achieved = flop_per_update * nu / max(t_sweep, 1e-12) / 1e12
+    peak = FP32_PEAK_TFLOPS if args.precision == 32 else FP64_PEAK_TFLOPS
+    roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": achieved / peak, "traffic": None,
+            "kernel": "k_sweep (row-table stencil)" if last["kernel_used"] == 2 else "k_sweep (general)",
+            "flop_per_node_update": flop_per_update,
+            "kernel_node_updates_per_s": nu / max(t_sweep, 1e-12),
+            "kernel_seconds_share_of_step": t_sweep / max(t_local, 1e-12),
+            "peak_basis": "derived: 148 SM x 128 FP32 lanes x 2 x 1965 MHz (guide unit counts)"}
+    prof = os.path.join(ROOT, "profiles", "sweep_traffic.json")
+    if os.path.exists(prof):
+        try:
+            pj = json.load(open(prof))
+            roof["traffic"] = pj.get("dram_bytes_per_node_update")
+            roof["traffic_unit"] = "bytes per node-update (ncu --set full, see profiles/)"
+        except Exception:
+            pass
+
+    cpu = None
+    if not args.no_cpu and rank == 0 and world == 1:
+        v, desc, thr, _ = oracle_sample(inst, args.cpu_seconds)
+        cpu = {"value": v, "unit": UNIT, "cores": thr, "kind": "oracle", "sample": desc}
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32" if args.precision == 32 else "f64", "data": "synthetic",
+            "config": {"workload": f"{inst.name}: patchy pipeline (coarse {inst.coarse.n}^2 solve,"
+                                   f" synthesis, {inst.n_patches} patch labels, fine solve to "
+                                   f"tol {args.tol:g}) on {inst.n}^2",
+                       "grid": inst.n, "controls": inst.n_controls, "branches": 2 * inst.p,
+                       "patches": inst.n_patches, "k_inner": args.k_inner,
+                       "l2": "inputs larger than L2 (V fp64 %d MB)" % (inst.n * inst.n * 8 >> 20),
+                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+            "time_to_converge": {"patchy_s": t_solve / args.steps,
+                                 "patchy_pipeline_s": t_max / args.steps,
+                                 "static_s": static["time_to_converge_s"] if static else None,
+                                 "rounds_patchy": rounds // args.steps,
+                                 "sweep_equivalents_patchy": nu / args.steps / inst.free_count()},
+            "static": static,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk,
+        }
+        if cpu:
+            # plain-Jacobi oracle time-to-converge estimate: sweeps ~ 0.71 n
+            out["time_to_converge"]["oracle_jacobi_estimate_s"] = (
+                inst.free_count() * 0.71 * inst.n / cpu["value"])
+        print(json.dumps(out), flush=True)
+    barrier(world)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -184,6 +184,9 @@ pdd_status pdd_get_successors(pdd_ctx *ctx, int32_t *dst, int32_t dst_on_device)
  * an active tile (n_patches + 1 entries, the last one for orphans). */
 pdd_status pdd_get_patch_rounds(pdd_ctx *ctx, int32_t *dst, int32_t count);
 
+/* Number of kernels this context has enqueued since pdd_create (all calls). */
+long long pdd_kernel_launches(const pdd_ctx *ctx);
+
 const char *pdd_last_error(const pdd_ctx *ctx);
 void pdd_destroy(pdd_ctx *ctx);
 

@@ -229,6 +229,9 @@ class Solver:
         self._ck(N.lib().pdd_get_patch_rounds(self._ctx, C.c_void_p(a.ctypes.data), int(count)))
         return a
 
+    def kernel_launches(self) -> int:
+        return int(N.lib().pdd_kernel_launches(self._ctx))
+
     # ------------------------------------------------------------------ convenience
     def run_patchy(self, tol: float, k_inner: int = 4, tol_c: float = 1e-12, **kw) -> dict:
         out = {"coarse": self.coarse_solve(tol_c)}

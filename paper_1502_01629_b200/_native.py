@@ -21,7 +21,7 @@ EXPORTS = ["pdd_version", "pdd_workspace_bytes", "pdd_create", "pdd_coarse_solve
            "pdd_synthesize", "pdd_build_patches", "pdd_build_static", "pdd_solve",
            "pdd_apply_operator", "pdd_get_values", "pdd_set_values", "pdd_get_uhat",
            "pdd_get_coarse_values", "pdd_get_controls", "pdd_get_labels", "pdd_get_successors",
-           "pdd_get_patch_rounds", "pdd_last_error", "pdd_destroy"]
+           "pdd_get_patch_rounds", "pdd_kernel_launches", "pdd_last_error", "pdd_destroy"]
 
 
 class pdd_coef(C.Structure):
@@ -95,9 +95,11 @@ def lib():
         getattr(L, f).argtypes = [ctx, vp, C.c_int32]
     L.pdd_get_patch_rounds.argtypes = [ctx, vp, C.c_int32]
     L.pdd_destroy.argtypes = [ctx]
+    L.pdd_kernel_launches.argtypes = [ctx]
+    L.pdd_kernel_launches.restype = C.c_longlong
     L.pdd_destroy.restype = None
     for f in EXPORTS:
-        if f not in ("pdd_version", "pdd_last_error", "pdd_destroy"):
+        if f not in ("pdd_version", "pdd_last_error", "pdd_destroy", "pdd_kernel_launches"):
             getattr(L, f).restype = C.c_int
     _lib = L
     return L

@@ -134,6 +134,7 @@ struct pdd_ctx {
     int n_tiles = 0;
     int prepared_kernel = -1;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    long long launches = 0;     // kernels enqueued by this context (all calls)
 };
 
 static pdd_status fail(pdd_ctx *c, pdd_status s, const char *fmt, ...)
@@ -325,6 +326,8 @@ const char *pdd_version(void) { return "pdd-b200 0.1 (sm_100a)"; }
 
 const char *pdd_last_error(const pdd_ctx *ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
 
+long long pdd_kernel_launches(const pdd_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
 pdd_status pdd_workspace_bytes(const pdd_problem *fine, const pdd_problem *coarse,
                                int32_t precision, size_t *bytes)
 {
@@ -403,6 +406,7 @@ pdd_status pdd_create(const pdd_problem *fine, const pdd_problem *coarse, int32_
     if (s == PDD_OK && coarse) s = copy_problem(ctx, coarse, ctx->Cc, false);
     if (s == PDD_OK) {
         launch_init_values(ctx->F.d, ctx->V, ctx->stream);
+        ctx->launches++;
         cudaError_t e = cudaGetLastError();
         if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
         if (e != cudaSuccess) s = fail(nullptr, PDD_E_CUDA, "create: %s", cudaGetErrorString(e));
@@ -438,6 +442,7 @@ pdd_status pdd_coarse_solve(pdd_ctx *ctx, double tol_c, int64_t max_sweeps, pdd_
     const DProblem &Pc = ctx->Cc.d;
     CK(cudaEventRecord(ctx->ev[0], s));
     launch_init_values(Pc, ctx->uc[0], s);
+    ctx->launches++;
     CK(cudaMemsetAsync(ctx->res_hist, 0, sizeof(unsigned long long) * max_sweeps, s));
     CK(cudaMemsetAsync(ctx->dev_int, 0, sizeof(int), s));
     int64_t issued = 0;
@@ -449,6 +454,7 @@ pdd_status pdd_coarse_solve(pdd_ctx *ctx, double tol_c, int64_t max_sweeps, pdd_
         for (int64_t q = 0; q < b; ++q, ++issued)
             launch_coarse_sweep(Pc, ctx->uc[issued & 1], ctx->uc[(issued + 1) & 1], tol_c,
                                 ctx->res_hist, (int)issued, ctx->dev_int, s);
+        ctx->launches += b;
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(ctx->h_int, ctx->dev_int, sizeof(int), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
@@ -488,6 +494,7 @@ pdd_status pdd_synthesize(pdd_ctx *ctx)
     cudaStream_t s = ctx->stream;
     launch_prolong(ctx->coarse.n, ctx->uc_final, ctx->fine.n, ctx->uhat, s);
     launch_synthesize(ctx->F.d, ctx->uhat, ctx->astar, s);
+    ctx->launches += 2;
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(s));
     ctx->synth_done = true;
@@ -506,6 +513,7 @@ pdd_status pdd_build_patches(pdd_ctx *ctx, int32_t n_patches, double M)
     cudaStream_t s = ctx->stream;
     const int64_t N = (int64_t)ctx->fine.n * ctx->fine.n;
     launch_successor(ctx->F.d, M, ctx->astar, ctx->succ0, s);
+    ctx->launches++;
     CK(cudaGetLastError());
     // pointer jumping: after K rounds every chain of length < 2^K has reached its root
     int K = 1;
@@ -516,6 +524,7 @@ pdd_status pdd_build_patches(pdd_ctx *ctx, int32_t n_patches, double M)
     for (; r < K + 1; ++r) {
         CK(cudaMemsetAsync(ctx->dev_int + 1, 0, sizeof(int), s));
         launch_jump(in, bufs[r & 1], N, ctx->dev_int + 1, s);
+        ctx->launches++;
         CK(cudaGetLastError());
         in = bufs[r & 1];
         if ((r & 3) == 3) {
@@ -525,6 +534,7 @@ pdd_status pdd_build_patches(pdd_ctx *ctx, int32_t n_patches, double M)
         }
     }
     launch_labels(ctx->F.kind, ctx->F.sector, in, n_patches, N, ctx->labels, s);
+    ctx->launches++;
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(s));
     ctx->labels_mode = 1;
@@ -539,6 +549,7 @@ pdd_status pdd_build_static(pdd_ctx *ctx, int32_t px, int32_t py)
     if (px < 1 || py < 1 || (int64_t)px * py >= kMaxPatches || px > ctx->fine.n || py > ctx->fine.n)
         return fail(ctx, PDD_E_INVALID, "bad static decomposition %d x %d", px, py);
     launch_static_labels(ctx->fine.n, px, py, ctx->F.kind, ctx->labels, ctx->stream);
+    ctx->launches++;
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(ctx->stream));
     ctx->labels_mode = 2;
@@ -768,6 +779,7 @@ static pdd_status activate(pdd_ctx *ctx, int out_list, double tol, double thr, i
     CK(cudaMemsetAsync(ctx->T.counters, 0, sizeof(ActCounters), s));
     CK(cudaMemsetAsync(&reinterpret_cast<ActCounters *>(ctx->T.counters)->min_pending, 0xff, 8, s));
     launch_activate(ctx->g, ctx->T, out_list, tol, tol, thr, round, ctx->n_tiles, s);
+    ctx->launches++;
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(ctx->h_cnt, ctx->T.counters, sizeof(ActCounters), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -800,6 +812,7 @@ pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
     CK(cudaEventRecord(ctx->ev[0], s));
     launch_set_values(d, o->mode == 0 ? 0 : 1, ctx->uhat, ctx->V, s);
     launch_tile_init(d, ctx->g, o->mode == 0 ? ctx->uhat : nullptr, ctx->labels, ctx->T, s);
+    ctx->launches += 2;
     CK(cudaMemsetAsync(ctx->T.patch_round, 0xff, sizeof(int32_t) * (ctx->n_patches + 1), s));
     CK(cudaMemsetAsync(ctx->T.patch_res, 0, sizeof(double) * (ctx->n_patches + 1), s));
     CK(cudaGetLastError());
@@ -827,6 +840,7 @@ pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
             CK(cudaEventRecord(ctx->ev[2], s));
             SweepLaunch L = make_launch(ctx, ctx->T.list[cur], c.count, o->k_inner, 0, nullptr);
             CK(launch_sweep(L, s));
+            ctx->launches++;
             CK(cudaEventRecord(ctx->ev[3], s));
             CK(cudaEventSynchronize(ctx->ev[3]));
             float ms = 0.f;
@@ -848,6 +862,7 @@ pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
         CK(cudaEventRecord(ctx->ev[2], s));
         SweepLaunch L = make_launch(ctx, ctx->T.all_list, ctx->n_tiles, 1, 1, nullptr);
         CK(launch_sweep(L, s));
+        ctx->launches++;
         CK(cudaMemsetAsync(ctx->T.tile_chg, 0, sizeof(double) * ctx->n_tiles, s));
         CK(cudaEventRecord(ctx->ev[3], s));
         S.rounds++;
@@ -896,6 +911,7 @@ pdd_status pdd_apply_operator(pdd_ctx *ctx, double *out, int32_t kernel, double 
     double *dst = out;
     if (dst) CK(cudaMemcpyAsync(dst, ctx->V, sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
     launch_tile_init(ctx->F.d, ctx->g, nullptr, nullptr, ctx->T, s);
+    ctx->launches += 2;
     SweepLaunch L = make_launch(ctx, ctx->T.all_list, ctx->n_tiles, 1, 1, dst);
     CK(launch_sweep(L, s));
     pdd_status r = activate(ctx, 0, INFINITY, INFINITY, 0);
@@ -937,6 +953,7 @@ pdd_status pdd_get_values(pdd_ctx *ctx, void *dst, int32_t dst_on_device, int32_
         return PDD_OK;
     }
     k_to_f32<<<4 * 148, 256, 0, ctx->stream>>>(ctx->V, (float *)dst, (int64_t)N);
+    ctx->launches++;
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(ctx->stream));
     return PDD_OK;
