@@ -317,8 +317,11 @@ def main():
     if os.path.exists(prof):
         try:
             pj = json.load(open(prof))
-            roof["traffic"] = pj.get("dram_bytes_per_node_update")
-            roof["traffic_unit"] = "bytes per node-update (ncu --set full, see profiles/)"
+            per_launch_updates = nu / max(1, rounds)
+            roof["traffic"] = pj["dram_bytes_per_node_update"] * per_launch_updates
+            roof["traffic_basis"] = ("dram bytes per node-update from ncu --set full (%s) x the "
+                                     "average node-updates per sweep launch of this run; "
+                                     "algorithmic bytes per node-update ~4.6" % pj["source"])
         except Exception:
             pass
 

@@ -71,6 +71,7 @@ void launch_static_labels(int n, int px, int py, const uint8_t *kind, int16_t *l
 // ---------------------------------------------------------------- sweep.cu
 struct TileGeom {
     int TW, TH, H, tiles_x, tiles_y, pitch;
+    int cstride;   // floats between the 4 shifted smem copies (path 3)
 };
 
 struct TileState {
@@ -107,7 +108,7 @@ struct SweepLaunch {
     const void *rowtab;      // RowEntry array [n][na_pad]
     int na_pad;
     int Hx;                  // nodes with i < Hx or i > n-1-Hx use the general stencil
-    int path;                // 1 general, 2 row-table
+    int path;                // 1 general, 2 row-table, 3 row-table fp32 G=4
     int WY, WX;              // row-table window
     int check;               // 1: pure Jacobi residual, no update
     int precision;           // 32 | 64

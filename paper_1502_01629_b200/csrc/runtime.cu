@@ -696,14 +696,17 @@ static pdd_status prepare(pdd_ctx *ctx, int kernel_req)
     const int napad = na_pad_of(p->n_controls);
     if (kernel_req != 1 && rowtab_window(p, d, WY, WX) && rowtab_supported(WY, WX, napad / 32))
         path = 2;
-    if (kernel_req == 2 && path != 2)
+    if ((kernel_req == 2 || kernel_req == 3) && path != 2)
         return fail(ctx, PDD_E_INVALID, "row-table stencil requested but the problem is not row-uniform");
-    ctx->path = path;
+    // fp32 row-table problems use the 4-nodes-per-step kernel (path 3) unless kernel 3 asks for
+    // the one-node-per-step variant (path 2, kept for A/B measurements and fp64)
+    const bool g4 = path == 2 && ctx->precision == 32 && kernel_req != 3;
+    ctx->path = g4 ? 3 : path;
     ctx->WY = WY;
     ctx->WX = WX;
     ctx->Hx = H;
     TileGeom g{};
-    g.TW = path == 2 ? rowtab_tw(WY, WX) : 64;
+    g.TW = (path == 2 && !g4) ? rowtab_tw(WY, WX) : 64;
     g.TH = 32;
     g.H = H;
     g.tiles_x = (p->n + g.TW - 1) / g.TW;
@@ -729,7 +732,17 @@ static pdd_status prepare(pdd_ctx *ctx, int kernel_req)
     }
     const int banks = ctx->precision == 32 ? 32 : 16;
     int pitch = g.TW + 2 * H;
-    while (pitch % banks != mod % banks) ++pitch;
+    if (g4) {
+        // 16-byte rows; consecutive window rows land in different 16-byte bank groups
+        while (pitch % 4 != 0 || ((pitch / 4) & 1) == 0) ++pitch;
+        const int rows = g.TH + 2 * H;
+        int cs = rows * pitch + 4;
+        while (cs % 4 != 0 || ((cs / 4) % 8) != 2) ++cs;   // spread the 4 copies over bank groups
+        g.cstride = cs;
+    } else {
+        while (pitch % banks != mod % banks) ++pitch;
+        g.cstride = 0;
+    }
     g.pitch = pitch;
     ctx->g = g;
     ctx->n_tiles = g.tiles_x * g.tiles_y;
@@ -903,7 +916,7 @@ pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
 pdd_status pdd_apply_operator(pdd_ctx *ctx, double *out, int32_t kernel, double *residual)
 {
     if (!ctx) return fail(nullptr, PDD_E_INVALID, "ctx is NULL");
-    if (kernel < 0 || kernel > 2) return fail(ctx, PDD_E_INVALID, "kernel must be 0, 1 or 2");
+    if (kernel < 0 || kernel > 3) return fail(ctx, PDD_E_INVALID, "kernel must be 0..3");
     pdd_status ps = prepare(ctx, kernel);
     if (ps != PDD_OK) return ps;
     cudaStream_t s = ctx->stream;

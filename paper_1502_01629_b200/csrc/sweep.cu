@@ -176,15 +176,22 @@ __device__ __forceinline__ void row_masks(const DProblem &P, int TW, int i0, int
     }
 }
 
-template <typename real, bool CHECK>
+// NCOPY: the G4 path keeps 4 copies of the tile shifted by q floats (copy q of element e at
+// q*cstride + q + e) so that every lane's 4-column window load is a 16-byte aligned LDS.128.
+template <typename real, bool CHECK, int NCOPY = 1>
 __device__ __forceinline__ void commit_node(real *p, real best, bool last, real &res,
-                                            double *out, int64_t gidx, double Vref)
+                                            double *out, int64_t gidx, double Vref,
+                                            int cstride = 0)
 {
     if ((threadIdx.x & 31) == 0) {
         const real old = *p;
         if (last) res = rmax(res, rabs(best - old));
-        if (!CHECK) *p = best;
-        else if (out) out[gidx] = Vref + (double)best;
+        if (!CHECK) {
+#pragma unroll
+            for (int q = 0; q < NCOPY; ++q) p[q * cstride + q] = best;
+        } else if (out) {
+            out[gidx] = Vref + (double)best;
+        }
     }
 }
 
@@ -277,11 +284,131 @@ __device__ __forceinline__ void row_table(const KP<real> &A, real *s_u, const re
     }
 }
 
+// Row-table stencil, fp32, G = 4 nodes per warp step (path 3).
+//  * window: per lane and control, WY rows x (WX + 3) columns in registers; each step loads the
+//    4 new columns of every window row with one 16-byte LDS.128 from the shifted copy in which
+//    that lane's address is aligned, and carries WX - 1 columns over from the previous step;
+//  * 4 x CPL independent FFMA chains per lane (ILP), WY*WX FFMAs per node and control;
+//  * transposed min-reduction over the 32 lanes for the 4 nodes at once: 6 SHFL for 4 nodes
+//    (2 exchange-halving stages, then a 3-stage butterfly), leaving node g's min in lanes
+//    8g..8g+7; lane 8g commits node g (Jacobi among the 4 nodes of a step).
+template <int CPL, int WY, int WX, bool CHECK>
+__device__ __forceinline__ void row_table4(const KP<float> &A, float *s_u, const float *s_ctrl,
+                                           int pitch, int cstride, int H, int i0, int ly,
+                                           int gj, float D, bool last, float &res, double Vref)
+{
+    constexpr int TW = 64;
+    constexpr int NWC = WX + 3;          // window columns per step
+    const int lane = threadIdx.x & 31;
+    const int n = A.P.n;
+    unsigned long long dmask, emask;
+    row_masks(A.P, TW, i0, gj, A.Hx, dmask, emask);
+    const unsigned long long skip = dmask | emask;
+
+    const RowEntry<float, WY, WX> *tab =
+        reinterpret_cast<const RowEntry<float, WY, WX> *>(A.rowtab) + (int64_t)gj * A.na_pad;
+    float Wt[CPL][WY * WX];
+    float c0[CPL];
+    const float *src[CPL];      // aligned load address of window row 0, column WX-1, at lx = 0
+    float win[CPL][WY][NWC];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+        const int k = lane + 32 * c;
+        const RowEntry<float, WY, WX> &e = tab[k];
+        c0[c] = k < A.P.na ? D * e.E : rinf<float>();
+#pragma unroll
+        for (int m = 0; m < WY * WX; ++m) Wt[c][m] = e.W[m];
+        const int e0 = (ly + H + e.oy) * pitch + H + e.ox;      // element of window (0, 0)
+        const int q = (4 - ((e0 + WX - 1) & 3)) & 3;            // copy with aligned loads
+        src[c] = s_u + q * cstride + q + e0 + WX - 1;
+#pragma unroll
+        for (int r = 0; r < WY; ++r)
+#pragma unroll
+            for (int x = 0; x < WX - 1; ++x) win[c][r][x] = s_u[e0 + r * pitch + x];
+    }
+
+    float *rowp = s_u + (ly + H) * pitch + H;
+#pragma unroll 1
+    for (int g = 0; g < TW; g += 4) {
+#pragma unroll
+        for (int c = 0; c < CPL; ++c)
+#pragma unroll
+            for (int r = 0; r < WY; ++r) {
+                const float4 v = *reinterpret_cast<const float4 *>(src[c] + r * pitch + g);
+                win[c][r][WX - 1] = v.x;
+                win[c][r][WX] = v.y;
+                win[c][r][WX + 1] = v.z;
+                win[c][r][WX + 2] = v.w;
+            }
+        float m[4];
+#pragma unroll
+        for (int gg = 0; gg < 4; ++gg) m[gg] = rinf<float>();
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+#pragma unroll
+            for (int gg = 0; gg < 4; ++gg) {
+                float acc = c0[c];
+#pragma unroll
+                for (int r = 0; r < WY; ++r)
+#pragma unroll
+                    for (int x = 0; x < WX; ++x)
+                        acc = fmaf(Wt[c][r * WX + x], win[c][r][gg + x], acc);
+                m[gg] = fminf(m[gg], acc);
+            }
+        }
+        // carry the last WX - 1 columns into the next step's window
+#pragma unroll
+        for (int c = 0; c < CPL; ++c)
+#pragma unroll
+            for (int r = 0; r < WY; ++r)
+#pragma unroll
+                for (int x = 0; x < WX - 1; ++x) win[c][r][x] = win[c][r][x + 4];
+        // transposed reduction: lanes < 16 keep nodes {0,1}, lanes >= 16 keep {2,3}
+        const bool hi = lane & 16;
+        float k0 = hi ? m[2] : m[0], k1 = hi ? m[3] : m[1];
+        const float s0 = hi ? m[0] : m[2], s1 = hi ? m[1] : m[3];
+        k0 = fminf(k0, __shfl_xor_sync(FULL, s0, 16));
+        k1 = fminf(k1, __shfl_xor_sync(FULL, s1, 16));
+        const bool b8 = lane & 8;
+        float x = b8 ? k1 : k0;
+        x = fminf(x, __shfl_xor_sync(FULL, b8 ? k0 : k1, 8));
+        x = fminf(x, __shfl_xor_sync(FULL, x, 4));
+        x = fminf(x, __shfl_xor_sync(FULL, x, 2));
+        x = fminf(x, __shfl_xor_sync(FULL, x, 1));
+        // lane 8*gg holds node gg = 2*(lane >= 16) + (lane & 8 ? 1 : 0) = lane >> 3
+        if ((lane & 7) == 0) {
+            const int gg = lane >> 3;
+            const int lx = g + gg;
+            if (!((skip >> lx) & 1ull)) {
+                float *p = rowp + lx;
+                const float old = *p;
+                if (last) res = fmaxf(res, fabsf(x - old));
+                if (!CHECK) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) p[q * cstride + q] = x;
+                } else if (A.out) {
+                    A.out[(int64_t)gj * n + i0 + lx] = Vref + (double)x;
+                }
+            }
+        }
+    }
+    // nodes whose feet may be clamped in x: general stencil on copy 0, commit to all copies
+    unsigned long long em = emask & ~dmask;
+    while (em) {
+        const int lx = __ffsll((long long)em) - 1;
+        em &= em - 1;
+        const float best = general_node<float>(A.P, s_ctrl, rowp + lx, pitch, i0 + lx, gj, D);
+        commit_node<float, CHECK, 4>(rowp + lx, best, last, res, A.out, (int64_t)gj * n + i0 + lx,
+                                     Vref, cstride);
+    }
+}
+
 // ------------------------------------------------------------------ the tile kernel
 template <typename real, int PATH, int CPL, int WY, int WX, bool CHECK>
 __global__ void __launch_bounds__(NW * 32) k_sweep(KP<real> A)
 {
     constexpr int TW = PATH == 2 ? TWOf<WY, WX>::value : TW_GENERAL;
+    constexpr int NCOPY = PATH == 3 ? 4 : 1;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double *s_red = reinterpret_cast<double *>(smem_raw);            // NW
     real *s_ctrl = reinterpret_cast<real *>(s_red + NW);              // 2 * 128
@@ -301,7 +428,8 @@ __global__ void __launch_bounds__(NW * 32) k_sweep(KP<real> A)
         const int gj = j0 - H + r, gi = i0 - H + c;
         real v = 0;
         if (gj >= 0 && gj < n && gi >= 0 && gi < n) v = (real)(A.V[(int64_t)gj * n + gi] - Vref);
-        s_u[r * pitch + c] = v;
+#pragma unroll
+        for (int q = 0; q < NCOPY; ++q) s_u[q * A.g.cstride + q + r * pitch + c] = v;
     }
     for (int e = threadIdx.x; e < 2 * A.P.na; e += blockDim.x) s_ctrl[e] = (real)A.P.ctrl[e];
     __syncthreads();
@@ -317,7 +445,10 @@ __global__ void __launch_bounds__(NW * 32) k_sweep(KP<real> A)
             const int ly = warp * RPW + ((sw & 1) ? RPW - 1 - rr : rr);
             const int gj = j0 + ly;
             if (gj >= n) continue;
-            if (PATH == 2)
+            if constexpr (PATH == 3 && sizeof(real) == 4)
+                row_table4<CPL, WY, WX, CHECK>(A, s_u, s_ctrl, pitch, A.g.cstride, H, i0, ly, gj,
+                                               D, last, res, Vref);
+            else if constexpr (PATH == 2)
                 row_table<real, CPL, WY, WX, CHECK>(A, s_u, s_ctrl, pitch, H, i0, ly, gj, D,
                                                     last, res, Vref);
             else
@@ -327,7 +458,9 @@ __global__ void __launch_bounds__(NW * 32) k_sweep(KP<real> A)
         if (!CHECK) __syncthreads();
     }
 
-    // tile residual of the last sweep
+    // tile residual of the last sweep (path 3 commits from lanes 0, 8, 16, 24)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) res = rmax(res, __shfl_xor_sync(FULL, res, o));
     if (lane == 0) s_red[warp] = (double)res;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -381,7 +514,8 @@ static cudaError_t launch_one(const SweepLaunch &L, cudaStream_t s)
     A.na_pad = L.na_pad;
     A.Hx = L.Hx;
     const size_t smem = NW * sizeof(double) + 256 * sizeof(real) +
-                        (size_t)(TH + 2 * L.g.H) * L.g.pitch * sizeof(real);
+                        (PATH == 3 ? (size_t)4 * L.g.cstride
+                                   : (size_t)(TH + 2 * L.g.H) * L.g.pitch) * sizeof(real);
     auto kern = k_sweep<real, PATH, CPL, WY, WX, CHECK>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -398,6 +532,20 @@ static cudaError_t dispatch(const SweepLaunch &L, cudaStream_t s)
 {
     if (L.path == 1) return launch_one<real, 1, 1, 1, 1, CHECK>(L, s);
     const int cpl = L.na_pad / 32;
+    if constexpr (sizeof(real) == 4) {
+        if (L.path == 3) {
+#define PDD_RT4(WY_, WX_)                                                                    \
+            if (L.WY == WY_ && L.WX == WX_) {                                               \
+                if (cpl == 1) return launch_one<float, 3, 1, WY_, WX_, CHECK>(L, s);        \
+                return launch_one<float, 3, 2, WY_, WX_, CHECK>(L, s);                      \
+            }
+            PDD_RT4(3, 3)
+            PDD_RT4(2, 5)
+            PDD_RT4(4, 4)
+#undef PDD_RT4
+            return cudaErrorInvalidValue;
+        }
+    }
 #define PDD_RT(WY_, WX_)                                                                     \
     if (L.WY == WY_ && L.WX == WX_) {                                                        \
         if (cpl == 1) return launch_one<real, 2, 1, WY_, WX_, CHECK>(L, s);                  \

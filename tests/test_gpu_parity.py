@@ -75,8 +75,10 @@ def _random_field(inst, seed):
 
 @pytest.mark.parametrize("cfg,n", [("C1", None), ("C2", 201), ("C3", 257), ("C4", 257), ("C5", 257)])
 @pytest.mark.parametrize("precision", [64, 32])
-@pytest.mark.parametrize("kernel", [1, 0])
+@pytest.mark.parametrize("kernel", [1, 0, 3])
 def test_operator_parity(cfg, n, precision, kernel):
+    if kernel == 3 and cfg == "C3":
+        pytest.skip("C3's speed field is not row-uniform: no row-table stencil")
     inst = I.make_config(cfg, n=n)
     V = _random_field(inst, 3)
     ref, _ = O.apply(inst, V)
