@@ -101,8 +101,15 @@ typedef struct {
     double tol;          /* sup-norm residual tolerance eps                                  */
     int64_t max_rounds;  /* cap on tile rounds                                               */
     double delta;        /* patchy bucket width in value units; 0 = automatic; < 0 = off      */
-    int32_t kernel;      /* 0 auto, 1 general stencil, 2 row-table stencil                   */
-    int32_t reserved[3];
+    int32_t kernel;      /* 0 auto, 1 general stencil, 2 row-table stencil, 3 row-table one
+                            node per warp step (A/B only)                                    */
+    int32_t schedule;    /* 0 rounds (default): rounds over the list of active tiles, every
+                            tile visit an in-tile Gauss-Seidel solve; patchy admits tiles in
+                            buckets of min u_hat of width delta;
+                            1 ordered: Gauss-Seidel passes over the tiles in key order (u_hat
+                            for patchy, block-lexicographic for static), each tile waiting for
+                            its lower-key neighbours (delta = key slack)                     */
+    int32_t reserved[2];
 } pdd_solve_opts;
 
 typedef struct {

@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpdd.so")
+# PDD_LIB: development override (A/B builds of the same sources); default is the in-tree lib
+LIB_PATH = os.environ.get("PDD_LIB") or os.path.join(HERE, "libpdd.so")
 
 PDD_OK, PDD_E_INVALID, PDD_E_NOCONVERGE, PDD_E_IO, PDD_E_CUDA, PDD_E_STATE, PDD_E_NOMEM, \
     PDD_E_STENCIL = range(8)
@@ -40,7 +41,7 @@ class pdd_problem(C.Structure):
 class pdd_solve_opts(C.Structure):
     _fields_ = [("mode", C.c_int32), ("k_inner", C.c_int32), ("tol", C.c_double),
                 ("max_rounds", C.c_int64), ("delta", C.c_double), ("kernel", C.c_int32),
-                ("reserved", C.c_int32 * 3)]
+                ("schedule", C.c_int32), ("reserved", C.c_int32 * 2)]
 
 
 class pdd_solve_stats(C.Structure):

@@ -33,31 +33,36 @@ def _nvcc():
     return "nvcc"
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, defines=(), out: str = None) -> str:
+    """Compile and link.  ``defines``/``out``: development A/B variants (e.g.
+    defines=["PDD_G_UNROLL=1"], out="build/variants/u1/libpdd.so"); the product lib is LIB."""
+    lib = out or LIB
+    bdir = os.path.dirname(os.path.abspath(lib)) if out else BUILD
+    os.makedirs(bdir, exist_ok=True)
     srcs = [os.path.join(CSRC, u) for u in UNITS] + [os.path.join(CSRC, "pdd_internal.cuh"),
                                                      os.path.join(ROOT, "include", "pdd.h")]
     newest = max(os.path.getmtime(s) for s in srcs)
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= newest:
-        return LIB
+    if not force and os.path.exists(lib) and os.path.getmtime(lib) >= newest:
+        return lib
+    dflags = [f"-D{d}" for d in defines]
     objs = []
     for unit, extra in UNITS.items():
-        obj = os.path.join(BUILD, unit.replace(".cu", ".o"))
-        cmd = [_nvcc(), *ARCH, *COMMON, *extra, "-c", os.path.join(CSRC, unit), "-o", obj]
+        obj = os.path.join(bdir, unit.replace(".cu", ".o"))
+        cmd = [_nvcc(), *ARCH, *COMMON, *dflags, *extra, "-c", os.path.join(CSRC, unit), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if verbose or r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {unit}")
-        with open(os.path.join(BUILD, unit + ".ptxas.txt"), "w") as f:
+        with open(os.path.join(bdir, unit + ".ptxas.txt"), "w") as f:
             f.write(r.stderr)
         objs.append(obj)
-    cmd = [_nvcc(), *ARCH, "-shared", "-o", LIB, *objs, "-lcudart"]
+    cmd = [_nvcc(), *ARCH, "-shared", "-o", lib, *objs, "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("link failed")
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

@@ -85,6 +85,21 @@ struct TileState {
     int32_t *patch_round;    // per patch: last round with an active tile
     double *patch_res;       // per patch: max residual of its active tiles
     void *counters;          // ActCounters (device)
+    // ordered schedule
+    double *tile_key;        // sort key per tile
+    int32_t *tile_group;     // static block of the tile (dependency groups), or unused
+    int32_t *order;          // tile ids sorted by key
+    int *done;               // last pass that finished the tile
+    long long *stamp;        // visit sequence number of the tile's last visit
+    void *ocounters;         // OrdCounters (device)
+};
+
+struct OrdCounters {
+    int counter;
+    int processed;
+    unsigned long long free_sum;
+    unsigned long long max_res;
+    unsigned long long seq;
 };
 
 struct ActCounters {
@@ -93,6 +108,26 @@ struct ActCounters {
     long long free_sum;
     unsigned long long min_pending;   // ordered bits of the min u_hat of needy ineligible tiles
     unsigned long long max_res;       // ordered bits of the max tile residual
+};
+
+// Ordered schedule (k_sweep_ordered): one Gauss-Seidel pass over the tiles in key order.
+struct OrderArgs {
+    const int32_t *order;         // tile ids sorted by key
+    int n_order;
+    const double *key;            // per tile: min u_hat (patchy) or block-lexicographic rank
+    const int32_t *group;         // per tile group (static block) or NULL: dependencies only
+                                  // between tiles of the same group
+    const int32_t *tile_free;
+    int *done;                    // per tile: last pass whose visit (or skip) finished
+    long long *stamp;             // per tile: visit sequence number of its last visit
+    unsigned long long *seq;      // global visit sequence counter
+    int *counter;                 // work counter of this pass
+    int *processed;               // tiles visited this pass
+    unsigned long long *free_sum; // free nodes of the visited tiles
+    unsigned long long *max_res;  // ordered bits of the max visit residual
+    int pass;                     // pass id (>= 1)
+    double tol;
+    double key_slack;             // wait only for neighbours with key < own key - key_slack
 };
 
 struct SweepLaunch {
@@ -112,6 +147,8 @@ struct SweepLaunch {
     int WY, WX;              // row-table window
     int check;               // 1: pure Jacobi residual, no update
     int precision;           // 32 | 64
+    int ordered;             // 1: k_sweep_ordered with `order` (one pass)
+    OrderArgs order;
 };
 
 void launch_tile_init(const DProblem &P, const TileGeom &g, const double *uhat,

@@ -16,6 +16,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -128,6 +129,7 @@ struct pdd_ctx {
     int labels_mode = 0;        // 0 none, 1 patchy, 2 static
     int n_patches = 0;
     int n_patch_slots = 0;
+    int static_px = 1, static_py = 1;
     // sweep configuration
     int path = 0, WY = 0, WX = 0, Hx = 0;
     TileGeom g{};
@@ -298,6 +300,12 @@ static size_t layout(pdd_ctx *c, void *ws, const pdd_problem *f, const pdd_probl
     T.patch_round = cv.take<int32_t>(kMaxPatches + 1);
     T.patch_res = cv.take<double>(kMaxPatches + 1);
     T.counters = cv.take<ActCounters>(1);
+    T.tile_key = cv.take<double>(tmax);
+    T.tile_group = cv.take<int32_t>(tmax);
+    T.order = cv.take<int32_t>(tmax);
+    T.done = cv.take<int>(tmax);
+    T.stamp = cv.take<long long>(tmax);
+    T.ocounters = cv.take<OrdCounters>(1);
     if (c) {
         c->F = F;
         c->Cc = Cc;
@@ -553,6 +561,8 @@ pdd_status pdd_build_static(pdd_ctx *ctx, int32_t px, int32_t py)
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(ctx->stream));
     ctx->labels_mode = 2;
+    ctx->static_px = px;
+    ctx->static_py = py;
     ctx->n_patches = px * py;
     ctx->prepared_kernel = -1;
     return PDD_OK;
@@ -805,6 +815,117 @@ __global__ void k_to_f32(const double *in, float *out, int64_t N)
         out[k] = (float)in[k];
 }
 
+// Ordered schedule: Gauss-Seidel passes over the tiles in key order (k_sweep_ordered), then a
+// full-grid Jacobi verification when a pass finds nothing left to do.
+static pdd_status ordered_loop(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats &S, int trace,
+                               bool &converged, double &last_verify, float &ms_sweep,
+                               float &ms_verify)
+{
+    cudaStream_t s = ctx->stream;
+    const int nt = ctx->n_tiles;
+    const TileGeom &g = ctx->g;
+    std::vector<double> key(nt);
+    std::vector<int32_t> fr(nt), grp;
+    CK(cudaStreamSynchronize(s));
+    CK(cudaMemcpy(fr.data(), ctx->T.tile_free, sizeof(int32_t) * nt, cudaMemcpyDeviceToHost));
+    if (o->mode == 0) {
+        // patchy: the nodes are taken in increasing u_hat, at tile granularity
+        CK(cudaMemcpy(key.data(), ctx->T.tile_minu, sizeof(double) * nt, cudaMemcpyDeviceToHost));
+    } else {
+        // static squares: each block in the default order "left to right and from top to bottom"
+        // (P:954-955), blocks independent of each other
+        grp.resize(nt);
+        const int n = ctx->fine.n, px = ctx->static_px, py = ctx->static_py;
+        for (int t = 0; t < nt; ++t) {
+            const int tx = t % g.tiles_x, ty = t / g.tiles_x;
+            const int ci = std::min(tx * g.TW + g.TW / 2, n - 1), cj = std::min(ty * g.TH + g.TH / 2, n - 1);
+            int bx = 0, by = 0;
+            while (bx + 1 < px && (int64_t)(bx + 1) * n / px <= ci) ++bx;
+            while (by + 1 < py && (int64_t)(by + 1) * n / py <= cj) ++by;
+            grp[t] = by * px + bx;
+            key[t] = (double)((int64_t)(g.tiles_y - 1 - ty) * g.tiles_x + tx);
+        }
+        CK(cudaMemcpy(ctx->T.tile_group, grp.data(), sizeof(int32_t) * nt, cudaMemcpyHostToDevice));
+    }
+    CK(cudaMemcpy(ctx->T.tile_key, key.data(), sizeof(double) * nt, cudaMemcpyHostToDevice));
+    std::vector<int32_t> ord;
+    ord.reserve(nt);
+    for (int t = 0; t < nt; ++t)
+        if (fr[t] > 0) ord.push_back(t);
+    std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return key[a] < key[b]; });
+    if (!ord.empty())
+        CK(cudaMemcpy(ctx->T.order, ord.data(), sizeof(int32_t) * ord.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemsetAsync(ctx->T.done, 0, sizeof(int) * nt, s));
+    CK(cudaMemsetAsync(ctx->T.stamp, 0, sizeof(long long) * nt, s));
+    CK(cudaMemsetAsync(ctx->T.ocounters, 0, sizeof(OrdCounters), s));
+    OrdCounters *oc = reinterpret_cast<OrdCounters *>(ctx->T.ocounters);
+    OrderArgs O{};
+    O.order = ctx->T.order;
+    O.n_order = (int)ord.size();
+    O.key = ctx->T.tile_key;
+    O.group = o->mode == 1 ? ctx->T.tile_group : nullptr;
+    O.tile_free = ctx->T.tile_free;
+    O.done = ctx->T.done;
+    O.stamp = ctx->T.stamp;
+    O.seq = &oc->seq;
+    O.counter = &oc->counter;
+    O.processed = &oc->processed;
+    O.free_sum = &oc->free_sum;
+    O.max_res = &oc->max_res;
+    O.tol = o->tol;
+    // patchy: tiles whose min u_hat differ by less than the slack do not wait for each other
+    // (near-equal keys are neighbours along a level set of u_hat, not upstream / downstream);
+    // opts.delta > 0 sets it, 0 = a quarter of the value change across a tile height at unit
+    // speed.  Static keys are integers: plain "strictly smaller".
+    O.key_slack = o->mode == 1 ? 0.0 : (o->delta > 0.0 ? o->delta : 0.25 * g.TH * ctx->fine.h * ctx->F.d.lmax);
+    OrdCounters h{};
+    int pass = 0;
+    while (S.rounds < o->max_rounds) {
+        O.pass = ++pass;
+        CK(cudaMemsetAsync(oc, 0, offsetof(OrdCounters, seq), s));
+        SweepLaunch L = make_launch(ctx, nullptr, 0, o->k_inner, 0, nullptr);
+        L.ordered = 1;
+        L.order = O;
+        CK(cudaEventRecord(ctx->ev[2], s));
+        CK(launch_sweep(L, s));
+        ctx->launches++;
+        CK(cudaEventRecord(ctx->ev[3], s));
+        CK(cudaMemcpyAsync(&h, oc, sizeof h, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]);
+        ms_sweep += ms;
+        S.rounds++;
+        if (trace)
+            fprintf(stderr, "[pdd] pass %d visited %d free %llu maxres %.3e %.3f ms\n", pass, h.processed,
+                    h.free_sum, bits_to_double(h.max_res), ms);
+        if (h.processed > 0) {
+            S.tiles_processed += h.processed;
+            S.node_updates += (long long)h.free_sum * o->k_inner;
+            continue;
+        }
+        // nothing left to do: full-grid Jacobi verification
+        CK(cudaEventRecord(ctx->ev[2], s));
+        SweepLaunch V = make_launch(ctx, ctx->T.all_list, ctx->n_tiles, 1, 1, nullptr);
+        CK(launch_sweep(V, s));
+        ctx->launches++;
+        CK(cudaEventRecord(ctx->ev[3], s));
+        S.rounds++;
+        S.verify_passes++;
+        pdd_status r = activate(ctx, 0, INFINITY, INFINITY, 0);
+        if (r != PDD_OK) return r;
+        cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]);
+        ms_verify += ms;
+        last_verify = bits_to_double(ctx->h_cnt->max_res);
+        if (trace) fprintf(stderr, "[pdd] verify residual %.3e\n", last_verify);
+        if (last_verify < o->tol) {
+            converged = true;
+            break;
+        }
+    }
+    return PDD_OK;
+}
+
 extern "C" {
 
 pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
@@ -832,22 +953,32 @@ pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
 
     double delta = o->delta;
     if (o->mode == 1) delta = -1.0;
-    if (delta == 0.0) delta = ctx->g.TW * ctx->fine.h * d.lmax;   // ~ one tile of travel at unit speed
+    // automatic bucket width: a quarter of the value change across one tile width at unit speed
+    if (delta == 0.0) delta = 0.25 * ctx->g.TW * ctx->fine.h * d.lmax;
     double thr = delta > 0.0 ? -1.0 : INFINITY;
 
     pdd_solve_stats S{};
     S.n_tiles = ctx->n_tiles;
     S.kernel_used = ctx->path;
     int cur = 0;
+    const char *tenv = std::getenv("PDD_TRACE");   // development: per-round trace every N rounds
+    const int trace = tenv ? std::max(1, std::atoi(tenv)) : 0;
     int round = 0;
     bool converged = false;
     double last_verify = INFINITY;
     float ms_sweep = 0.f, ms_verify = 0.f;
-    while (true) {
+    if (o->schedule == 1) {
+        pdd_status r = ordered_loop(ctx, o, S, trace, converged, last_verify, ms_sweep, ms_verify);
+        if (r != PDD_OK) return r;
+    }
+    while (o->schedule != 1) {
         if (S.rounds >= o->max_rounds) break;
         pdd_status r = activate(ctx, cur, o->tol, thr, round);
         if (r != PDD_OK) return r;
         const ActCounters c = *ctx->h_cnt;
+        if (trace && (round < 40 || round % trace == 0))
+            fprintf(stderr, "[pdd] round %d active %d free %lld maxres %.3e thr %.4f\n", round,
+                    c.count, (long long)c.free_sum, bits_to_double(c.max_res), thr);
         if (c.count > 0) {
             CK(cudaMemsetAsync(ctx->T.tile_chg, 0, sizeof(double) * ctx->n_tiles, s));
             CK(cudaEventRecord(ctx->ev[2], s));

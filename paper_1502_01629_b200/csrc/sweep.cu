@@ -35,8 +35,18 @@
 #include <math.h>
 #include <stdio.h>
 
+#include <algorithm>
+
 namespace pdd {
 
+#ifndef PDD_G_UNROLL
+#define PDD_G_UNROLL 2      // groups of 4 nodes unrolled per loop trip (path 3)
+#endif
+#ifndef PDD_MIN_BLOCKS
+#define PDD_MIN_BLOCKS 1    // __launch_bounds__ min CTAs per SM (register cap)
+#endif
+
+constexpr int kGUnroll = PDD_G_UNROLL;
 constexpr int TH = 32;          // tile rows
 constexpr int NW = 8;           // warps per CTA
 constexpr int RPW = TH / NW;    // rows per warp
@@ -284,142 +294,27 @@ __device__ __forceinline__ void row_table(const KP<real> &A, real *s_u, const re
     }
 }
 
-// Row-table stencil, fp32, G = 4 nodes per warp step (path 3).
-//  * window: per lane and control, WY rows x (WX + 3) columns in registers; each step loads the
-//    4 new columns of every window row with one 16-byte LDS.128 from the shifted copy in which
-//    that lane's address is aligned, and carries WX - 1 columns over from the previous step;
-//  * 4 x CPL independent FFMA chains per lane (ILP), WY*WX FFMAs per node and control;
-//  * transposed min-reduction over the 32 lanes for the 4 nodes at once: 6 SHFL for 4 nodes
-//    (2 exchange-halving stages, then a 3-stage butterfly), leaving node g's min in lanes
-//    8g..8g+7; lane 8g commits node g (Jacobi among the 4 nodes of a step).
-template <int CPL, int WY, int WX, bool CHECK>
-__device__ __forceinline__ void row_table4(const KP<float> &A, float *s_u, const float *s_ctrl,
-                                           int pitch, int cstride, int H, int i0, int ly,
-                                           int gj, float D, bool last, float &res, double Vref)
-{
-    constexpr int TW = 64;
-    constexpr int NWC = WX + 3;          // window columns per step
-    const int lane = threadIdx.x & 31;
-    const int n = A.P.n;
-    unsigned long long dmask, emask;
-    row_masks(A.P, TW, i0, gj, A.Hx, dmask, emask);
-    const unsigned long long skip = dmask | emask;
+#include "sweep_gs.cuh"
 
-    const RowEntry<float, WY, WX> *tab =
-        reinterpret_cast<const RowEntry<float, WY, WX> *>(A.rowtab) + (int64_t)gj * A.na_pad;
-    float Wt[CPL][WY * WX];
-    float c0[CPL];
-    const float *src[CPL];      // aligned load address of window row 0, column WX-1, at lx = 0
-    float win[CPL][WY][NWC];
-#pragma unroll
-    for (int c = 0; c < CPL; ++c) {
-        const int k = lane + 32 * c;
-        const RowEntry<float, WY, WX> &e = tab[k];
-        c0[c] = k < A.P.na ? D * e.E : rinf<float>();
-#pragma unroll
-        for (int m = 0; m < WY * WX; ++m) Wt[c][m] = e.W[m];
-        const int e0 = (ly + H + e.oy) * pitch + H + e.ox;      // element of window (0, 0)
-        const int q = (4 - ((e0 + WX - 1) & 3)) & 3;            // copy with aligned loads
-        src[c] = s_u + q * cstride + q + e0 + WX - 1;
-#pragma unroll
-        for (int r = 0; r < WY; ++r)
-#pragma unroll
-            for (int x = 0; x < WX - 1; ++x) win[c][r][x] = s_u[e0 + r * pitch + x];
-    }
-
-    float *rowp = s_u + (ly + H) * pitch + H;
-#pragma unroll 1
-    for (int g = 0; g < TW; g += 4) {
-#pragma unroll
-        for (int c = 0; c < CPL; ++c)
-#pragma unroll
-            for (int r = 0; r < WY; ++r) {
-                const float4 v = *reinterpret_cast<const float4 *>(src[c] + r * pitch + g);
-                win[c][r][WX - 1] = v.x;
-                win[c][r][WX] = v.y;
-                win[c][r][WX + 1] = v.z;
-                win[c][r][WX + 2] = v.w;
-            }
-        float m[4];
-#pragma unroll
-        for (int gg = 0; gg < 4; ++gg) m[gg] = rinf<float>();
-#pragma unroll
-        for (int c = 0; c < CPL; ++c) {
-#pragma unroll
-            for (int gg = 0; gg < 4; ++gg) {
-                float acc = c0[c];
-#pragma unroll
-                for (int r = 0; r < WY; ++r)
-#pragma unroll
-                    for (int x = 0; x < WX; ++x)
-                        acc = fmaf(Wt[c][r * WX + x], win[c][r][gg + x], acc);
-                m[gg] = fminf(m[gg], acc);
-            }
-        }
-        // carry the last WX - 1 columns into the next step's window
-#pragma unroll
-        for (int c = 0; c < CPL; ++c)
-#pragma unroll
-            for (int r = 0; r < WY; ++r)
-#pragma unroll
-                for (int x = 0; x < WX - 1; ++x) win[c][r][x] = win[c][r][x + 4];
-        // transposed reduction: lanes < 16 keep nodes {0,1}, lanes >= 16 keep {2,3}
-        const bool hi = lane & 16;
-        float k0 = hi ? m[2] : m[0], k1 = hi ? m[3] : m[1];
-        const float s0 = hi ? m[0] : m[2], s1 = hi ? m[1] : m[3];
-        k0 = fminf(k0, __shfl_xor_sync(FULL, s0, 16));
-        k1 = fminf(k1, __shfl_xor_sync(FULL, s1, 16));
-        const bool b8 = lane & 8;
-        float x = b8 ? k1 : k0;
-        x = fminf(x, __shfl_xor_sync(FULL, b8 ? k0 : k1, 8));
-        x = fminf(x, __shfl_xor_sync(FULL, x, 4));
-        x = fminf(x, __shfl_xor_sync(FULL, x, 2));
-        x = fminf(x, __shfl_xor_sync(FULL, x, 1));
-        // lane 8*gg holds node gg = 2*(lane >= 16) + (lane & 8 ? 1 : 0) = lane >> 3
-        if ((lane & 7) == 0) {
-            const int gg = lane >> 3;
-            const int lx = g + gg;
-            if (!((skip >> lx) & 1ull)) {
-                float *p = rowp + lx;
-                const float old = *p;
-                if (last) res = fmaxf(res, fabsf(x - old));
-                if (!CHECK) {
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) p[q * cstride + q] = x;
-                } else if (A.out) {
-                    A.out[(int64_t)gj * n + i0 + lx] = Vref + (double)x;
-                }
-            }
-        }
-    }
-    // nodes whose feet may be clamped in x: general stencil on copy 0, commit to all copies
-    unsigned long long em = emask & ~dmask;
-    while (em) {
-        const int lx = __ffsll((long long)em) - 1;
-        em &= em - 1;
-        const float best = general_node<float>(A.P, s_ctrl, rowp + lx, pitch, i0 + lx, gj, D);
-        commit_node<float, CHECK, 4>(rowp + lx, best, last, res, A.out, (int64_t)gj * n + i0 + lx,
-                                     Vref, cstride);
-    }
-}
-
-// ------------------------------------------------------------------ the tile kernel
+// ------------------------------------------------------------------ one tile visit
+// Stage tile + halo, relax k_inner times, write back.  Global V is read with ld.global.cg (L2):
+// in the ordered (persistent) schedule other CTAs update V during the launch.
 template <typename real, int PATH, int CPL, int WY, int WX, bool CHECK>
-__global__ void __launch_bounds__(NW * 32) k_sweep(KP<real> A)
+__device__ __forceinline__ void sweep_tile(const KP<real> &A, int t, unsigned char *smem_raw,
+                                           double *res_out, double *chg_out)
 {
     constexpr int TW = PATH == 2 ? TWOf<WY, WX>::value : TW_GENERAL;
     constexpr int NCOPY = PATH == 3 ? 4 : 1;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
     double *s_red = reinterpret_cast<double *>(smem_raw);            // NW
-    real *s_ctrl = reinterpret_cast<real *>(s_red + NW);              // 2 * 128
+    volatile int *s_prog = reinterpret_cast<volatile int *>(s_red + NW);   // TH progress counters
+    real *s_ctrl = reinterpret_cast<real *>(s_red + NW + TH / 2);     // 2 * 128
     real *s_u = s_ctrl + 256;
     const int H = A.g.H, pitch = A.g.pitch;
     const int n = A.P.n;
-    const int t = A.list[blockIdx.x];
     const int i0 = (t % A.g.tiles_x) * TW;
     const int j0 = (t / A.g.tiles_x) * TH;
     const int ci = min(i0 + TW / 2, n - 1), cj = min(j0 + TH / 2, n - 1);
-    const double Vref = A.V[(int64_t)cj * n + ci];
+    const double Vref = __ldcg(A.V + (int64_t)cj * n + ci);
 
     // stage tile + halo (coalesced fp64 row reads, converted relative to V_ref)
     const int W2 = TW + 2 * H, H2 = TH + 2 * H;
@@ -427,35 +322,39 @@ __global__ void __launch_bounds__(NW * 32) k_sweep(KP<real> A)
         const int r = e / W2, c = e - r * W2;
         const int gj = j0 - H + r, gi = i0 - H + c;
         real v = 0;
-        if (gj >= 0 && gj < n && gi >= 0 && gi < n) v = (real)(A.V[(int64_t)gj * n + gi] - Vref);
+        if (gj >= 0 && gj < n && gi >= 0 && gi < n)
+            v = (real)(__ldcg(A.V + (int64_t)gj * n + gi) - Vref);
 #pragma unroll
         for (int q = 0; q < NCOPY; ++q) s_u[q * A.g.cstride + q + r * pitch + c] = v;
     }
     for (int e = threadIdx.x; e < 2 * A.P.na; e += blockDim.x) s_ctrl[e] = (real)A.P.ctrl[e];
+    if (threadIdx.x < TH) s_prog[threadIdx.x] = 0;
     __syncthreads();
 
     // D = h l - (1 - beta) V_ref (constant cost; a cost field uses D per node in general path)
     const real D = (real)(A.P.h * A.P.lmax - (1.0 - A.P.beta) * Vref);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     real res = 0;
-    const int sweeps = CHECK ? 1 : A.k_inner;
-    for (int sw = 0; sw < sweeps; ++sw) {
-        const bool last = sw == sweeps - 1;
-        for (int rr = 0; rr < RPW; ++rr) {
-            const int ly = warp * RPW + ((sw & 1) ? RPW - 1 - rr : rr);
-            const int gj = j0 + ly;
-            if (gj >= n) continue;
-            if constexpr (PATH == 3 && sizeof(real) == 4)
-                row_table4<CPL, WY, WX, CHECK>(A, s_u, s_ctrl, pitch, A.g.cstride, H, i0, ly, gj,
-                                               D, last, res, Vref);
-            else if constexpr (PATH == 2)
-                row_table<real, CPL, WY, WX, CHECK>(A, s_u, s_ctrl, pitch, H, i0, ly, gj, D,
-                                                    last, res, Vref);
-            else
-                row_general<real, CHECK>(A, s_u, s_ctrl, pitch, H, TW, i0, ly, gj, D, last,
-                                         res, Vref);
+    if constexpr (PATH == 3 && sizeof(real) == 4) {
+        tile_gs4<CPL, WY, WX, CHECK>(A, s_u, s_ctrl, s_prog, pitch, A.g.cstride, H, i0, j0, D,
+                                     A.k_inner, res, Vref);
+    } else {
+        const int sweeps = CHECK ? 1 : A.k_inner;
+        for (int sw = 0; sw < sweeps; ++sw) {
+            const bool last = sw == sweeps - 1;
+            for (int rr = 0; rr < RPW; ++rr) {
+                const int ly = warp * RPW + ((sw & 1) ? RPW - 1 - rr : rr);
+                const int gj = j0 + ly;
+                if (gj >= n) continue;
+                if constexpr (PATH == 2)
+                    row_table<real, CPL, WY, WX, CHECK>(A, s_u, s_ctrl, pitch, H, i0, ly, gj, D,
+                                                        last, res, Vref);
+                else
+                    row_general<real, CHECK>(A, s_u, s_ctrl, pitch, H, TW, i0, ly, gj, D, last,
+                                             res, Vref);
+            }
+            if (!CHECK) __syncthreads();
         }
-        if (!CHECK) __syncthreads();
     }
 
     // tile residual of the last sweep (path 3 commits from lanes 0, 8, 16, 24)
@@ -463,12 +362,14 @@ __global__ void __launch_bounds__(NW * 32) k_sweep(KP<real> A)
     for (int o = 16; o > 0; o >>= 1) res = rmax(res, __shfl_xor_sync(FULL, res, o));
     if (lane == 0) s_red[warp] = (double)res;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        double m = 0.0;
-        for (int w = 0; w < NW; ++w) m = fmax(m, s_red[w]);
-        A.tile_res[t] = m;
+    double rmaxv = 0.0;
+    for (int w = 0; w < NW; ++w) rmaxv = fmax(rmaxv, s_red[w]);
+    if (threadIdx.x == 0) A.tile_res[t] = rmaxv;
+    if (res_out) *res_out = rmaxv;
+    if (CHECK) {
+        __syncthreads();
+        return;
     }
-    if (CHECK) return;
     __syncthreads();
 
     // write back changed interior nodes, net change of the visit
@@ -480,7 +381,7 @@ __global__ void __launch_bounds__(NW * 32) k_sweep(KP<real> A)
         const int64_t gidx = (int64_t)gj * n + gi;
         if (A.P.kind[gidx] != 0) continue;
         const real u = s_u[(ly + H) * pitch + lx + H];
-        const double vold = A.V[gidx];
+        const double vold = __ldcg(A.V + gidx);
         const real uold = (real)(vold - Vref);
         if (u != uold) {
             A.V[gidx] = Vref + (double)u;
@@ -491,10 +392,78 @@ __global__ void __launch_bounds__(NW * 32) k_sweep(KP<real> A)
     for (int o = 16; o > 0; o >>= 1) chg = fmax(chg, __shfl_xor_sync(FULL, chg, o));
     if (lane == 0) s_red[warp] = chg;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        double m = 0.0;
-        for (int w = 0; w < NW; ++w) m = fmax(m, s_red[w]);
-        A.tile_chg[t] = m;
+    double cm = 0.0;
+    for (int w = 0; w < NW; ++w) cm = fmax(cm, s_red[w]);
+    if (threadIdx.x == 0) A.tile_chg[t] = cm;
+    if (chg_out) *chg_out = cm;
+    __syncthreads();
+}
+
+// Round schedule: one CTA per listed tile (chaotic relaxation across the tiles of a launch).
+template <typename real, int PATH, int CPL, int WY, int WX, bool CHECK>
+__global__ void __launch_bounds__(NW * 32, PDD_MIN_BLOCKS) k_sweep(KP<real> A)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    sweep_tile<real, PATH, CPL, WY, WX, CHECK>(A, A.list[blockIdx.x], smem_raw, nullptr, nullptr);
+}
+
+// Ordered schedule (one pass): persistent CTAs take tiles in ascending key order (P:744-749,
+// u_hat for the patchy method; block-lexicographic for the static squares)
+// and visit a tile only after every neighbour with a smaller key (and the same group, when
+// groups are given) has finished its visit of this pass: a Gauss-Seidel pass over tiles in the
+// key order.  Deadlock-free: a tile waits only on tiles taken earlier from the same counter.
+// A tile is skipped (but still marked done) when its last residual is < tol and no neighbour
+// changed by >= tol after its last visit (visit stamps).
+template <typename real, int PATH, int CPL, int WY, int WX>
+__global__ void __launch_bounds__(NW * 32, PDD_MIN_BLOCKS) k_sweep_ordered(KP<real> A, OrderArgs O)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ int s_idx;
+    const int tid = threadIdx.x;
+    for (;;) {
+        if (tid == 0) s_idx = atomicAdd(O.counter, 1);
+        __syncthreads();
+        const int idx = s_idx;
+        if (idx >= O.n_order) break;
+        const int t = O.order[idx];
+        const int tx = t % A.g.tiles_x, ty = t / A.g.tiles_x;
+        const double kt = O.key[t];
+        const int gt = O.group ? O.group[t] : -1;
+        const long long st = ((volatile long long *)O.stamp)[t];
+        bool pred = false;
+        if (tid < 9) {
+            if (tid == 8) {
+                pred = ((volatile double *)A.tile_res)[t] >= O.tol;
+            } else {
+                const int k = tid < 4 ? tid : tid + 1;            // skip the centre
+                const int ax = tx + (k % 3) - 1, ay = ty + (k / 3) - 1;
+                if (ax >= 0 && ay >= 0 && ax < A.g.tiles_x && ay < A.g.tiles_y) {
+                    const int nb = ay * A.g.tiles_x + ax;
+                    if (O.key[nb] < kt - O.key_slack && (!O.group || O.group[nb] == gt)) {
+                        while (((volatile int *)O.done)[nb] < O.pass) __nanosleep(64);
+                        __threadfence();
+                    }
+                    pred = ((volatile double *)A.tile_chg)[nb] >= O.tol &&
+                           ((volatile long long *)O.stamp)[nb] > st;
+                }
+            }
+        }
+        const bool need = __syncthreads_or(pred) && O.tile_free[t] > 0;
+        if (need) {
+            double r = 0.0, c = 0.0;
+            sweep_tile<real, PATH, CPL, WY, WX, false>(A, t, smem_raw, &r, &c);
+            if (tid == 0) {
+                O.stamp[t] = (long long)atomicAdd(O.seq, 1ull) + 1;
+                atomicAdd(O.processed, 1);
+                atomicAdd(O.free_sum, (unsigned long long)O.tile_free[t]);
+                atomicMax(O.max_res, (unsigned long long)__double_as_longlong(r));
+            }
+        }
+        if (tid == 0) {
+            __threadfence();
+            ((volatile int *)O.done)[t] = O.pass;
+        }
+        __syncthreads();
     }
 }
 
@@ -513,9 +482,28 @@ static cudaError_t launch_one(const SweepLaunch &L, cudaStream_t s)
     A.rowtab = L.rowtab;
     A.na_pad = L.na_pad;
     A.Hx = L.Hx;
-    const size_t smem = NW * sizeof(double) + 256 * sizeof(real) +
+    const size_t smem = NW * sizeof(double) + TH * sizeof(int) + 256 * sizeof(real) +
                         (PATH == 3 ? (size_t)4 * L.g.cstride
                                    : (size_t)(TH + 2 * L.g.H) * L.g.pitch) * sizeof(real);
+    if (L.ordered && !CHECK) {
+        auto kern = k_sweep_ordered<real, PATH, CPL, WY, WX>;
+        if (smem > 48 * 1024) {
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)smem);
+            if (e != cudaSuccess) return e;
+        }
+        int per_sm = 0;
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NW * 32, smem);
+        if (e != cudaSuccess) return e;
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        int grid = std::max(1, per_sm) * sms;
+        if (grid > L.order.n_order) grid = L.order.n_order;
+        if (grid <= 0) return cudaSuccess;
+        kern<<<grid, NW * 32, smem, s>>>(A, L.order);
+        return cudaGetLastError();
+    }
     auto kern = k_sweep<real, PATH, CPL, WY, WX, CHECK>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -1,0 +1,202 @@
+// sweep_gs.cuh -- path 3 of k_sweep: fp32 row-table stencil, in-tile Gauss-Seidel sweeps in four
+// alternating orientations (included by sweep.cu; uses its helpers).
+//
+// Why: the paper's speed-up comes from processing nodes in a causal order, each node seeing the
+// freshest values of the nodes it depends on (2 / 26 sweeps instead of
+// 176 / 145).  Inside a tile we use fast-sweeping orientations (+x+y, -x+y, +x-y, -x-y for sweeps
+// 0, 1, 2, 3 mod 4): every sweep is an exact Gauss-Seidel pass in its orientation.  Fixed points
+// are unchanged (any order of a monotone contraction, R29).
+//
+// One sweep over the TH x 64 tile:
+//   * a warp processes a row 4 nodes ("group") at a time, lane = control (CPL controls per lane).
+//     Its controls' WY x (WX+3) window is loaded FRESH from shared memory for every group (so the
+//     previous group's nodes are seen updated) and the 4 x CPL candidate sums are accumulated at
+//     once (72 FFMA per group at C5: the bulk of the work, full ILP);
+//   * the 4 nodes are then finished IN SWEEP ORDER: node k's candidates are corrected for the new
+//     values of the nodes of the same group finished before it (their weights in node k's stencil
+//     are the row-table weights at relative column -1, -2, -3 (+x) or +1, +2, +3 (-x)), then a
+//     5-step __shfl_xor butterfly takes the min over controls -- exact Gauss-Seidel along x;
+//   * rows follow the sweep order through a software pipeline over the 8 warps (position jj of
+//     the sweep order belongs to warp jj % 8): position jj starts group gs only after position
+//     jj-1 has committed groups up to gs + lead - 1 (the window reaches < 4 + H columns ahead),
+//     signalled through per-position progress counters in shared memory -- Gauss-Seidel along y.
+// Window loads: copy q is chosen so that window column t = 0 is 16-byte aligned; columns 0..3
+// come from one LDS.128, columns 4.. from a second LDS.64 / LDS.128.
+
+template <int CPL, int WY, int WX, bool CHECK, bool XNEG>
+__device__ __forceinline__ void row_gs4(const KP<float> &A, float *s_u, const float *s_ctrl,
+                                        volatile int *s_prog, int pitch, int cstride, int H,
+                                        int i0, int ly, int gj, int jj, int base, int lead,
+                                        float D, bool last, float &res, double Vref)
+{
+    constexpr int TW = 64;
+    constexpr int NG = TW / 4;                 // groups per row
+    constexpr int NWC = WX + 3;                // window columns used per group
+    constexpr bool xneg = XNEG;
+    const int lane = threadIdx.x & 31;
+    const int n = A.P.n;
+    // ---- row setup (independent of other rows: overlaps the wait for jj - 1)
+    unsigned long long dmask, emask;
+    row_masks(A.P, TW, i0, gj, A.Hx, dmask, emask);
+    const unsigned long long skip = dmask | emask;
+    const RowEntry<float, WY, WX> *tab =
+        reinterpret_cast<const RowEntry<float, WY, WX> *>(A.rowtab) + (int64_t)gj * A.na_pad;
+    float Wt[CPL][WY * WX];
+    float c0[CPL];
+    float wc[CPL][3];          // weights of the 1st, 2nd, 3rd previous node of the row
+    const float *src[CPL];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+        const int kk = lane + 32 * c;
+        const RowEntry<float, WY, WX> &e = tab[kk];
+        c0[c] = kk < A.P.na ? D * e.E : rinf<float>();
+#pragma unroll
+        for (int m = 0; m < WY * WX; ++m) Wt[c][m] = e.W[m];
+        const int oy = e.oy, ox = e.ox;
+        const int e0 = (ly + H + oy) * pitch + H + ox;       // window (0,0) at lx = 0
+        const int q = (4 - (e0 & 3)) & 3;                    // column 0 aligned
+        src[c] = s_u + q * cstride + q + e0;
+        const int r0 = -oy;
+#pragma unroll
+        for (int d = 1; d <= 3; ++d) {
+            const int xw = (xneg ? d : -d) - ox;
+            wc[c][d - 1] = (r0 >= 0 && r0 < WY && xw >= 0 && xw < WX) ? e.W[r0 * WX + xw] : 0.f;
+        }
+    }
+    float *rowp = s_u + (ly + H) * pitch + H;
+    const int eo = (ly + H) * pitch + H;                      // node row, lx = 0
+    const int qo = (4 - (eo & 3)) & 3;
+    const float *oldp = s_u + qo * cstride + qo + eo;         // aligned old-value loads
+    for (int gs = 0; gs < NG; ++gs) {
+        const int G = xneg ? NG - 1 - gs : gs;
+        const int g = 4 * G;
+        if (!CHECK && jj > 0) {
+            const int need = base + min(gs + lead, NG);
+            while (s_prog[jj - 1] < need) __nanosleep(20);
+            __threadfence_block();
+        }
+        float win[CPL][WY][8];
+#pragma unroll
+        for (int c = 0; c < CPL; ++c)
+#pragma unroll
+            for (int r = 0; r < WY; ++r) {
+                const float *p = src[c] + r * pitch + g;
+                const float4 v = *reinterpret_cast<const float4 *>(p);
+                win[c][r][0] = v.x; win[c][r][1] = v.y; win[c][r][2] = v.z; win[c][r][3] = v.w;
+                if constexpr (NWC > 6) {
+                    const float4 w = *reinterpret_cast<const float4 *>(p + 4);
+                    win[c][r][4] = w.x; win[c][r][5] = w.y; win[c][r][6] = w.z; win[c][r][7] = w.w;
+                } else if constexpr (NWC > 4) {
+                    const float2 w = *reinterpret_cast<const float2 *>(p + 4);
+                    win[c][r][4] = w.x; win[c][r][5] = w.y;
+                }
+            }
+        float acc[CPL][4];
+#pragma unroll
+        for (int c = 0; c < CPL; ++c)
+#pragma unroll
+            for (int gg = 0; gg < 4; ++gg) {
+                float a = c0[c];
+#pragma unroll
+                for (int r = 0; r < WY; ++r)
+#pragma unroll
+                    for (int x = 0; x < WX; ++x)
+                        a = fmaf(Wt[c][r * WX + x], win[c][r][gg + x], a);
+                acc[c][gg] = a;
+            }
+        const float4 o4 = *reinterpret_cast<const float4 *>(oldp + g);
+        const float old[4] = {o4.x, o4.y, o4.z, o4.w};
+        float nv[4], dlt[4];
+        // finish the 4 nodes in sweep order with in-group Gauss-Seidel corrections
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+            const int gg = xneg ? 3 - s : s;
+            float m = rinf<float>();
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) {
+                float a = acc[c][gg];
+#pragma unroll
+                for (int d = 1; d <= s; ++d) a = fmaf(wc[c][d - 1], dlt[xneg ? gg + d : gg - d], a);
+                m = fminf(m, a);
+            }
+            m = warp_min(m);
+            const bool sk = (skip >> (g + gg)) & 1ull;
+            nv[gg] = m;
+            dlt[gg] = (sk || CHECK) ? 0.f : m - old[gg];
+        }
+        if (lane < 4) {
+            const int lx = g + lane;
+            if (!((skip >> lx) & 1ull)) {
+                const float x = lane == 0 ? nv[0] : lane == 1 ? nv[1] : lane == 2 ? nv[2] : nv[3];
+                const float ol = lane == 0 ? old[0] : lane == 1 ? old[1] : lane == 2 ? old[2] : old[3];
+                if (last) res = fmaxf(res, fabsf(x - ol));
+                float *p = rowp + lx;
+                if (!CHECK) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) p[q * cstride + q] = x;
+                } else if (A.out) {
+                    A.out[(int64_t)gj * n + i0 + lx] = Vref + (double)x;
+                }
+            }
+        }
+        // nodes of this group whose feet may be clamped in x: general stencil (these sit
+        // within H of the domain's x-boundary; their in-group order is not enforced)
+        unsigned long long em = (emask & ~dmask) & (0xfull << g);
+        if (em) {
+            __syncwarp();
+            while (em) {
+                const int lx = __ffsll((long long)em) - 1;
+                em &= em - 1;
+                const float best = general_node<float>(A.P, s_ctrl, rowp + lx, pitch, i0 + lx, gj, D);
+                commit_node<float, CHECK, 4>(rowp + lx, best, last, res, A.out,
+                                             (int64_t)gj * n + i0 + lx, Vref, cstride);
+            }
+        }
+        if (!CHECK) {
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence_block();
+                s_prog[jj] = base + gs + 1;
+            }
+        } else {
+            __syncwarp();
+        }
+    }
+}
+
+template <int CPL, int WY, int WX, bool CHECK>
+__device__ __forceinline__ void tile_gs4(const KP<float> &A, float *s_u, const float *s_ctrl,
+                                         volatile int *s_prog, int pitch, int cstride, int H,
+                                         int i0, int j0, float D, int k_inner, float &res,
+                                         double Vref)
+{
+    constexpr int NG = 16;
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int n = A.P.n;
+    const int lead = 1 + (3 + H) / 4;          // groups the previous row must be ahead
+    const int sweeps = CHECK ? 1 : k_inner;
+
+    for (int sw = 0; sw < sweeps; ++sw) {
+        const bool last = sw == sweeps - 1;
+        const int orient = sw & 3;
+        const bool xneg = orient & 1, yneg = orient & 2;
+        const int base = sw * NG;              // progress counters are monotone across sweeps
+        for (int k = 0; k < TH / NW; ++k) {
+            const int jj = warp + NW * k;      // position in this sweep's row order
+            const int ly = yneg ? TH - 1 - jj : jj;
+            const int gj = j0 + ly;
+            if (gj >= n) {
+                if (lane == 0) s_prog[jj] = base + NG;
+                continue;
+            }
+            if (xneg)
+                row_gs4<CPL, WY, WX, CHECK, true>(A, s_u, s_ctrl, s_prog, pitch, cstride, H, i0, ly,
+                                                  gj, jj, base, lead, D, last, res, Vref);
+            else
+                row_gs4<CPL, WY, WX, CHECK, false>(A, s_u, s_ctrl, s_prog, pitch, cstride, H, i0, ly,
+                                                   gj, jj, base, lead, D, last, res, Vref);
+        }
+        if (!CHECK) __syncthreads();
+    }
+}
