@@ -308,7 +308,10 @@ def main():
     peak = FP32_PEAK_TFLOPS if args.precision == 32 else FP64_PEAK_TFLOPS
     roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
             "frac": achieved / peak, "traffic": None,
-            "kernel": "k_sweep (row-table stencil)" if last["kernel_used"] == 2 else "k_sweep (general)",
+            "kernel": {1: "k_sweep path 1 (general stencil)",
+                       2: "k_sweep path 2 (row-table stencil, one node per warp step)",
+                       3: "k_sweep path 3 (row-table stencil, in-tile Gauss-Seidel, 4 nodes per step)"}
+                      .get(last["kernel_used"], "k_sweep"),
             "flop_per_node_update": flop_per_update,
             "kernel_node_updates_per_s": nu / max(t_sweep, 1e-12),
             "kernel_seconds_share_of_step": t_sweep / max(t_local, 1e-12),

@@ -147,7 +147,7 @@ __device__ __forceinline__ void row_gs4(const KP<float> &A, float *s_u, const fl
             while (em) {
                 const int lx = __ffsll((long long)em) - 1;
                 em &= em - 1;
-                const float best = general_node<float>(A.P, s_ctrl, rowp + lx, pitch, i0 + lx, gj, D);
+                const float best = general_node<float>(A.P, s_ctrl, rowp + lx, pitch, i0 + lx, gj, D, Vref);
                 commit_node<float, CHECK, 4>(rowp + lx, best, last, res, A.out,
                                              (int64_t)gj * n + i0 + lx, Vref, cstride);
             }

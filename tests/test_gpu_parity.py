@@ -131,3 +131,30 @@ def test_solve_parity(cfg, n, precision, mode):
     else:
         assert err <= 5e-5 * np.abs(ref["V"]).max(), err
     assert np.all(V[inst.kind == I.KIND_TARGET] == 0.0)
+
+
+@pytest.mark.parametrize("precision", [64, 32])
+def test_operator_parity_cost_field_and_random(precision):
+    """General stencil with a running-cost field, random speed field, drift, full 2x2 sigma,
+    targets and obstacles (every coefficient kind of the ABI except COL)."""
+    inst = I.random_instance(97, 21, n_a=24, p=2)
+    rng = np.random.default_rng(21)
+    inst.cost = I.Coef.field(rng.uniform(0.5, 2.0, inst.n * inst.n))
+    V = rng.uniform(0.0, 1.0, inst.n * inst.n)
+    V[inst.kind == I.KIND_TARGET] = 0.0
+    V[inst.kind == I.KIND_OBSTACLE] = 1.0 / inst.lam
+    ref, _ = O.apply(inst, V)
+    s = _solver(inst, precision)
+    out, res = s.apply_operator(V)
+    tol = 1e-12 if precision == 64 else 2e-6
+    assert np.abs(out - ref).max() < tol
+
+
+def test_solve_parity_random_general_fp64():
+    inst = I.random_instance(65, 22, n_a=16, p=1)
+    ref = O.jacobi(inst, tol=1e-14, max_sweeps=10**6)
+    s = _solver(inst, 64)
+    s.build_static(2, 2)
+    st = s.solve("static", tol=1e-13, k_inner=4)    # bound 1e-13/(1-beta) < 1e-11
+    assert st["converged"] == 1
+    assert np.abs(s.get_values() - ref["V"]).max() <= 1e-10
