@@ -91,9 +91,21 @@ def allreduce(val, op, world):
         return val
     import torch
     import torch.distributed as dist
-    t = torch.tensor([float(val)], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([float(val)], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=op)
     return float(t.item())
+
+
+def aggregate(node_updates, seconds, world):
+    """Replicas-only aggregation: value = all ranks' node-updates / the slowest rank's device
+    time (max over ranks; never a wall clock)."""
+    import torch.distributed as dist
+    if world == 1:
+        return node_updates, seconds, node_updates / seconds
+    t_max = allreduce(seconds, dist.ReduceOp.MAX, world)
+    nu = allreduce(node_updates, dist.ReduceOp.SUM, world)
+    return nu, t_max, nu / t_max
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -263,9 +275,7 @@ def main():
     launches = s.kernel_launches() - l0
     clk = clocks.stop()
     t_local = ev0.elapsed_time(ev1) * 1e-3
-    t_max = allreduce(t_local, dist.ReduceOp.MAX if world > 1 else None, world)
-    nu_all = allreduce(nu, dist.ReduceOp.SUM if world > 1 else None, world)
-    value = nu_all / t_max
+    nu_all, t_max, value = aggregate(nu, t_local, world)
     last = st
 
     # static decomposition on the same kernels (time-to-converge comparison)
