@@ -104,6 +104,7 @@ __device__ __forceinline__ void row_gs4(const KP<float> &A, float *s_u, const fl
                         a = fmaf(Wt[c][r * WX + x], win[c][r][gg + x], a);
                 acc[c][gg] = a;
             }
+        const unsigned sk4 = (unsigned)(skip >> g) & 0xfu;     // special nodes of this group
         const float4 o4 = *reinterpret_cast<const float4 *>(oldp + g);
         const float old[4] = {o4.x, o4.y, o4.z, o4.w};
         float nv[4], dlt[4];
@@ -119,14 +120,15 @@ __device__ __forceinline__ void row_gs4(const KP<float> &A, float *s_u, const fl
                 for (int d = 1; d <= s; ++d) a = fmaf(wc[c][d - 1], dlt[xneg ? gg + d : gg - d], a);
                 m = fminf(m, a);
             }
+            // (redux.sync.min is lowered to a shuffle tree on sm_100a: measured, no gain)
             m = warp_min(m);
-            const bool sk = (skip >> (g + gg)) & 1ull;
+            const bool sk = (sk4 >> gg) & 1u;
             nv[gg] = m;
             dlt[gg] = (sk || CHECK) ? 0.f : m - old[gg];
         }
         if (lane < 4) {
             const int lx = g + lane;
-            if (!((skip >> lx) & 1ull)) {
+            if (!((sk4 >> lane) & 1u)) {
                 const float x = lane == 0 ? nv[0] : lane == 1 ? nv[1] : lane == 2 ? nv[2] : nv[3];
                 const float ol = lane == 0 ? old[0] : lane == 1 ? old[1] : lane == 2 ? old[2] : old[3];
                 if (last) res = fmaxf(res, fabsf(x - ol));
