@@ -4,7 +4,8 @@
 A step = one pass of the whole hot path on config C5
 (8193^2 Zermelo navigation, 64 controls, 4 Markov branches, fp32 arithmetic): coarse solve on
 513^2 -> prolongation -> synthesis -> patch labels (256 patches) -> patchy fine solve until the
-full-grid Jacobi residual is < 1e-6 (verified).  Inputs are resident in HBM when the timed
+full-grid Jacobi residual is < 1e-7 (verified; at 1e-7 the fp32 V is within 6e-6 max|V| of the
+certified fp64 fixed point, R12).  Inputs are resident in HBM when the timed
 region starts (the problem arrays are uploaded once by pdd_create); V (fp64, 537 MB) and the
 other per-node arrays are larger than L2, so no flush is needed between steps.
 
@@ -59,7 +60,7 @@ def parse():
     ap.add_argument("--n", type=int, default=None, help="override grid size (not for the headline)")
     ap.add_argument("--precision", type=int, default=32)
     ap.add_argument("--k-inner", type=int, default=4)
-    ap.add_argument("--tol", type=float, default=1e-6)
+    ap.add_argument("--tol", type=float, default=1e-7)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-static", action="store_true")

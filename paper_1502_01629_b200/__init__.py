@@ -167,11 +167,14 @@ class Solver:
 
     def solve(self, mode="patchy", tol: float = 1e-6, k_inner: int = 4,
               max_rounds: int = 10**7, delta: float = 0.0, kernel: int = 0,
-              schedule: str = "rounds", raise_on_noconverge: bool = True) -> dict:
+              schedule: str = "rounds", raise_on_noconverge: bool = True,
+              early_exit: bool = True, bucket_policy: int = 0) -> dict:
         o = N.pdd_solve_opts()
         o.mode = MODE_PATCHY if mode in ("patchy", 0) else MODE_STATIC
         o.k_inner, o.tol, o.max_rounds, o.delta, o.kernel = int(k_inner), float(tol), int(max_rounds), float(delta), int(kernel)
         o.schedule = 1 if schedule in ("ordered", 1) else 0
+        o.reserved[0] = 0 if early_exit else 1
+        o.reserved[1] = int(bucket_policy)
         st = N.pdd_solve_stats()
         r = N.lib().pdd_solve(self._ctx, C.byref(o), C.byref(st))
         if r != N.PDD_OK and (raise_on_noconverge or r != N.PDD_E_NOCONVERGE):

@@ -100,6 +100,7 @@ struct OrdCounters {
     unsigned long long free_sum;
     unsigned long long max_res;
     unsigned long long seq;
+    unsigned long long updates;   // node-updates performed in the current pdd_solve
 };
 
 struct ActCounters {
@@ -149,6 +150,9 @@ struct SweepLaunch {
     int precision;           // 32 | 64
     int ordered;             // 1: k_sweep_ordered with `order` (one pass)
     OrderArgs order;
+    double early_tol;        // > 0: a tile visit stops after the first sweep changing < early_tol
+    const int32_t *tile_free;            // free nodes per tile (node-update accounting)
+    unsigned long long *nu_counter;      // += free nodes x sweeps done, per visit (or NULL)
 };
 
 void launch_tile_init(const DProblem &P, const TileGeom &g, const double *uhat,
@@ -160,6 +164,7 @@ void launch_activate(const TileGeom &g, TileState &T, int out_list, double tol, 
 cudaError_t launch_sweep(const SweepLaunch &L, cudaStream_t s);
 bool rowtab_supported(int WY, int WX, int cpl);
 int rowtab_tw(int WY, int WX);
+int sweep_tile_rows();
 size_t rowtab_entry_bytes(int precision, int WY, int WX);
 
 }  // namespace pdd

@@ -51,7 +51,10 @@ constexpr int kGUnroll = PDD_G_UNROLL;
 // warps) per SM without spills -- measured 1.6x faster than its unconstrained 137-register build
 template <int PATH>
 constexpr int min_blocks() { return PDD_MIN_BLOCKS > 0 ? PDD_MIN_BLOCKS : (PATH == 3 ? 3 : 1); }
-constexpr int TH = 32;          // tile rows
+#ifndef PDD_TH
+#define PDD_TH 32           // tile rows (multiple of NW)
+#endif
+constexpr int TH = PDD_TH;      // tile rows
 constexpr int NW = 8;           // warps per CTA
 constexpr int RPW = TH / NW;    // rows per warp
 constexpr int TW_GENERAL = 64;
@@ -61,6 +64,7 @@ template <int WY, int WX>
 struct TWOf { static constexpr int value = WX * (64 / WX); };   // multiple of WX, <= 64
 
 int rowtab_tw(int WY, int WX) { (void)WY; return WX * (64 / WX); }
+int sweep_tile_rows() { return TH; }
 
 bool rowtab_supported(int WY, int WX, int cpl)
 {
@@ -92,6 +96,9 @@ struct KP {
     const void *rowtab;
     int na_pad;
     int Hx;
+    double early_tol;     // path 3: stop the in-tile sweeps once a sweep changes less than this
+    const int32_t *tile_free;
+    unsigned long long *nu_counter;
 };
 
 __device__ __forceinline__ float rmin(float a, float b) { return fminf(a, b); }
@@ -342,9 +349,10 @@ __device__ __forceinline__ void sweep_tile(const KP<real> &A, int t, unsigned ch
     const real D = (real)(A.P.h * A.P.lmax - (1.0 - A.P.beta) * Vref);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     real res = 0;
+    int done_sweeps = CHECK ? 1 : A.k_inner;
     if constexpr (PATH == 3 && sizeof(real) == 4) {
-        tile_gs4<CPL, WY, WX, CHECK>(A, s_u, s_ctrl, s_prog, pitch, A.g.cstride, H, i0, j0, D,
-                                     A.k_inner, res, Vref);
+        done_sweeps = tile_gs4<CPL, WY, WX, CHECK>(A, s_u, s_ctrl, s_prog, s_red, pitch,
+                                                   A.g.cstride, H, i0, j0, D, A.k_inner, res, Vref);
     } else {
         const int sweeps = CHECK ? 1 : A.k_inner;
         for (int sw = 0; sw < sweeps; ++sw) {
@@ -401,7 +409,11 @@ __device__ __forceinline__ void sweep_tile(const KP<real> &A, int t, unsigned ch
     __syncthreads();
     double cm = 0.0;
     for (int w = 0; w < NW; ++w) cm = fmax(cm, s_red[w]);
-    if (threadIdx.x == 0) A.tile_chg[t] = cm;
+    if (threadIdx.x == 0) {
+        A.tile_chg[t] = cm;
+        if (A.nu_counter)   // node-updates actually performed (early exit aware)
+            atomicAdd(A.nu_counter, (unsigned long long)A.tile_free[t] * (unsigned long long)done_sweeps);
+    }
     if (chg_out) *chg_out = cm;
     __syncthreads();
 }
@@ -489,6 +501,9 @@ static cudaError_t launch_one(const SweepLaunch &L, cudaStream_t s)
     A.rowtab = L.rowtab;
     A.na_pad = L.na_pad;
     A.Hx = L.Hx;
+    A.early_tol = L.early_tol;
+    A.tile_free = L.tile_free;
+    A.nu_counter = L.nu_counter;
     const size_t smem = NW * sizeof(double) + TH * sizeof(int) + 256 * sizeof(real) +
                         (PATH == 3 ? (size_t)4 * L.g.cstride
                                    : (size_t)(TH + 2 * L.g.H) * L.g.pitch) * sizeof(real);

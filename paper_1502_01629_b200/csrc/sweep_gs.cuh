@@ -75,25 +75,25 @@ __device__ __forceinline__ void row_gs4(const KP<float> &A, float *s_u, const fl
             while (s_prog[jj - 1] < need) __nanosleep(20);
             __threadfence_block();
         }
-        float win[CPL][WY][8];
+        // candidate sums, one control at a time (the window of a control is dead once its four
+        // sums are formed: keeps the live set small enough for 3 CTAs / SM without remat)
+        float acc[CPL][4];
 #pragma unroll
-        for (int c = 0; c < CPL; ++c)
+        for (int c = 0; c < CPL; ++c) {
+            float win[WY][8];
 #pragma unroll
             for (int r = 0; r < WY; ++r) {
                 const float *p = src[c] + r * pitch + g;
                 const float4 v = *reinterpret_cast<const float4 *>(p);
-                win[c][r][0] = v.x; win[c][r][1] = v.y; win[c][r][2] = v.z; win[c][r][3] = v.w;
+                win[r][0] = v.x; win[r][1] = v.y; win[r][2] = v.z; win[r][3] = v.w;
                 if constexpr (NWC > 6) {
                     const float4 w = *reinterpret_cast<const float4 *>(p + 4);
-                    win[c][r][4] = w.x; win[c][r][5] = w.y; win[c][r][6] = w.z; win[c][r][7] = w.w;
+                    win[r][4] = w.x; win[r][5] = w.y; win[r][6] = w.z; win[r][7] = w.w;
                 } else if constexpr (NWC > 4) {
                     const float2 w = *reinterpret_cast<const float2 *>(p + 4);
-                    win[c][r][4] = w.x; win[c][r][5] = w.y;
+                    win[r][4] = w.x; win[r][5] = w.y;
                 }
             }
-        float acc[CPL][4];
-#pragma unroll
-        for (int c = 0; c < CPL; ++c)
 #pragma unroll
             for (int gg = 0; gg < 4; ++gg) {
                 float a = c0[c];
@@ -101,9 +101,10 @@ __device__ __forceinline__ void row_gs4(const KP<float> &A, float *s_u, const fl
                 for (int r = 0; r < WY; ++r)
 #pragma unroll
                     for (int x = 0; x < WX; ++x)
-                        a = fmaf(Wt[c][r * WX + x], win[c][r][gg + x], a);
+                        a = fmaf(Wt[c][r * WX + x], win[r][gg + x], a);
                 acc[c][gg] = a;
             }
+        }
         const unsigned sk4 = (unsigned)(skip >> g) & 0xfu;     // special nodes of this group
         const float4 o4 = *reinterpret_cast<const float4 *>(oldp + g);
         const float old[4] = {o4.x, o4.y, o4.z, o4.w};
@@ -167,10 +168,10 @@ __device__ __forceinline__ void row_gs4(const KP<float> &A, float *s_u, const fl
 }
 
 template <int CPL, int WY, int WX, bool CHECK>
-__device__ __forceinline__ void tile_gs4(const KP<float> &A, float *s_u, const float *s_ctrl,
-                                         volatile int *s_prog, int pitch, int cstride, int H,
-                                         int i0, int j0, float D, int k_inner, float &res,
-                                         double Vref)
+__device__ __forceinline__ int tile_gs4(const KP<float> &A, float *s_u, const float *s_ctrl,
+                                         volatile int *s_prog, double *s_red, int pitch,
+                                         int cstride, int H, int i0, int j0, float D, int k_inner,
+                                         float &res, double Vref)
 {
     constexpr int NG = 16;
     const int lane = threadIdx.x & 31;
@@ -180,7 +181,10 @@ __device__ __forceinline__ void tile_gs4(const KP<float> &A, float *s_u, const f
     const int sweeps = CHECK ? 1 : k_inner;
 
     for (int sw = 0; sw < sweeps; ++sw) {
-        const bool last = sw == sweeps - 1;
+        // every sweep tracks its residual: a tile that is converged w.r.t. its halo stops early
+        // (early_tol > 0) instead of spending the remaining in-tile sweeps
+        const bool last = true;
+        res = 0.f;
         const int orient = sw & 3;
         const bool xneg = orient & 1, yneg = orient & 2;
         const int base = sw * NG;              // progress counters are monotone across sweeps
@@ -199,6 +203,19 @@ __device__ __forceinline__ void tile_gs4(const KP<float> &A, float *s_u, const f
                 row_gs4<CPL, WY, WX, CHECK, false>(A, s_u, s_ctrl, s_prog, pitch, cstride, H, i0, ly,
                                                    gj, jj, base, lead, D, last, res, Vref);
         }
-        if (!CHECK) __syncthreads();
+        if (CHECK) break;
+        float r = res;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) r = fmaxf(r, __shfl_xor_sync(FULL, r, o));
+        if (lane == 0) s_red[warp] = (double)r;
+        __syncthreads();
+        if (A.early_tol > 0.0 && sw + 1 < sweeps) {
+            double m = 0.0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) m = fmax(m, s_red[w]);
+            __syncthreads();                   // s_red is reused by the next sweep
+            if (m < A.early_tol) return sw + 1;   // sweeps done
+        }
     }
+    return sweeps;
 }

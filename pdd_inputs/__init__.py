@@ -323,7 +323,9 @@ def _config_instance(cfg: str, n: int, n_coarse: Optional[int], *, coarse_level=
         inst.name = cfg + "-coarse"
         return inst
     inst.precision = 64 if cfg == "C1" else 32
-    inst.tol = 1e-9 if cfg == "C1" else 1e-6
+    # R12: fp32 runs stop at a verified residual < 1e-7; at C5 a residual of 1e-6 still leaves
+    # 8e-5 max|V| of error (amplification up to 1/(1-beta) = 4097), 1e-7 leaves 6e-6 max|V|
+    inst.tol = 1e-9 if cfg == "C1" else 1e-7
     if n_coarse is not None:
         if (n - 1) % (n_coarse - 1) != 0:
             raise ValueError("coarse grid must nest in the fine grid")

@@ -10,7 +10,7 @@ ap.add_argument("--cfg", default="C5"); ap.add_argument("--n", type=int, default
 ap.add_argument("--prec", type=int, default=32); ap.add_argument("--k", default="4")
 ap.add_argument("--modes", default="patchy,static"); ap.add_argument("--tol", type=float, default=1e-6)
 ap.add_argument("--kernel", type=int, default=0); ap.add_argument("--delta", default="0")
-ap.add_argument("--max_rounds", type=int, default=200000); ap.add_argument("--schedule", default="rounds")
+ap.add_argument("--max_rounds", type=int, default=200000); ap.add_argument("--schedule", default="rounds"); ap.add_argument("--policy", type=int, default=0)
 a = ap.parse_args()
 t = time.time(); inst = I.make_config(a.cfg, n=a.n); print("gen", time.time() - t, flush=True)
 t = time.time(); s = Solver(inst, precision=a.prec); torch.cuda.synchronize(); print("create", time.time() - t, flush=True)
@@ -22,7 +22,7 @@ for mode in a.modes.split(","):
     for k in map(int, a.k.split(",")):
         for d in map(float, a.delta.split(",")):
             t = time.time()
-            st = s.solve(mode, tol=a.tol, k_inner=k, kernel=a.kernel, delta=d, max_rounds=a.max_rounds, schedule=a.schedule, raise_on_noconverge=False)
+            st = s.solve(mode, tol=a.tol, k_inner=k, kernel=a.kernel, delta=d, max_rounds=a.max_rounds, schedule=a.schedule, bucket_policy=a.policy, raise_on_noconverge=False)
             wall = time.time() - t
             nu = st["node_updates"]
             print(json.dumps(dict(mode=mode, k=k, delta=d, wall=round(wall, 3), rounds=st["rounds"], conv=st["converged"],
