@@ -165,6 +165,10 @@ cudaError_t launch_sweep(const SweepLaunch &L, cudaStream_t s);
 bool rowtab_supported(int WY, int WX, int cpl);
 int rowtab_tw(int WY, int WX);
 int sweep_tile_rows();
+// Build the row-stencil table on the device; false if no supported window fits.
+bool rowtab_build_device(const DProblem &P, int napad, int H, int precision, int *scratch,
+                         void *tab, size_t tab_bytes, int &WY, int &WX, int &oxmin, int &oxmax,
+                         cudaStream_t s);
 size_t rowtab_entry_bytes(int precision, int WY, int WX);
 
 }  // namespace pdd

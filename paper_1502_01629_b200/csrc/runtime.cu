@@ -114,6 +114,7 @@ struct pdd_ctx {
     uint8_t *astar = nullptr;
     int16_t *labels = nullptr;
     int32_t *succ0 = nullptr, *succA = nullptr, *succB = nullptr;
+    float *f32buf = nullptr;
     unsigned long long *res_hist = nullptr;
     int *dev_int = nullptr;     // [0] sweeps_done, [1] jump changed flag
     void *rowtab = nullptr;
@@ -283,6 +284,7 @@ static size_t layout(pdd_ctx *c, void *ws, const pdd_problem *f, const pdd_probl
     int32_t *s0 = cp ? cv.take<int32_t>(N) : nullptr;
     int32_t *sA = cp ? cv.take<int32_t>(N) : nullptr;
     int32_t *sB = cp ? cv.take<int32_t>(N) : nullptr;
+    float *f32 = cv.take<float>(N);                     // fp32 staging for pdd_get_values
     int *di = cv.take<int>(8);
     const int napad = na_pad_of(f->n_controls);
     const size_t rtb = napad ? (size_t)n * napad * 160 : 0;   // >= sizeof(RowEntry<double,4,4>)
@@ -319,6 +321,7 @@ static size_t layout(pdd_ctx *c, void *ws, const pdd_problem *f, const pdd_probl
         c->succ0 = s0;
         c->succA = sA;
         c->succB = sB;
+        c->f32buf = f32;
         c->dev_int = di;
         c->rowtab = rt;
         c->rowtab_bytes = rtb;
@@ -572,125 +575,15 @@ pdd_status pdd_build_static(pdd_ctx *ctx, int32_t px, int32_t py)
 
 // ------------------------------------------------------------------------ sweep preparation
 
-// Row-uniform compact stencils (host, fp64): returns false when the problem is not row-uniform.
-template <typename real, int WY, int WX>
-static void fill_rowtab(const pdd_problem *p, const DProblem &d, int napad, int H,
-                        std::vector<unsigned char> &buf, int &oxmin, int &oxmax)
-{
-    const int n = p->n;
-    const int na = p->n_controls;
-    const int nb = p->p > 0 ? 2 * p->p : 1;
-    const double w = 1.0 / nb;
-    buf.assign((size_t)n * napad * sizeof(RowEntry<real, WY, WX>), 0);
-    auto *E = reinterpret_cast<RowEntry<real, WY, WX> *>(buf.data());
-    oxmin = 1 << 30;
-    oxmax = -(1 << 30);
-    const int imid = n / 2;
-    for (int j = 0; j < n; ++j) {
-        const double c = host_coef_at(p->speed, imid, j, n);
-        const double d1 = host_coef_at(p->drift[0], imid, j, n);
-        const double d2 = host_coef_at(p->drift[1], imid, j, n);
-        double off[2][2] = {{0, 0}, {0, 0}};
-        for (int k = 0; k < p->p; ++k) {
-            off[k][0] = d.sc * host_coef_at(p->sigma[k][0], imid, j, n);
-            off[k][1] = d.sc * host_coef_at(p->sigma[k][1], imid, j, n);
-        }
-        for (int a = 0; a < na; ++a) {
-            const double bx = d.q * (c * p->controls[2 * a] + d1);
-            const double by = d.q * (c * p->controls[2 * a + 1] + d2);
-            double acc[16][16];
-            for (auto &r : acc) for (double &v : r) v = 0.0;
-            double lam0 = 0.0;
-            int ymin = 99, xmin = 99;
-            struct Cn { int dy, dx; double w; } cn[16];
-            int ncn = 0;
-            for (int b = 0; b < nb; ++b) {
-                double xr = bx, yr = by;
-                if (p->p > 0) {
-                    const int kk = b >> 1;
-                    if (b & 1) { xr -= off[kk][0]; yr -= off[kk][1]; }
-                    else { xr += off[kk][0]; yr += off[kk][1]; }
-                }
-                yr = std::min(std::max(yr, (double)-j), (double)(n - 1 - j));
-                const double fx = std::floor(xr);
-                const double fy = std::min(std::floor(yr), (double)(n - 2 - j));
-                const double tx = xr - fx, ty = yr - fy;
-                const double ww[4] = {(1 - tx) * (1 - ty), tx * (1 - ty), (1 - tx) * ty, tx * ty};
-                for (int t = 0; t < 4; ++t) {
-                    const int dx = (int)fx + (t & 1), dy = (int)fy + (t >> 1);
-                    if (dx == 0 && dy == 0) { lam0 += w * ww[t]; continue; }
-                    cn[ncn++] = {dy, dx, w * ww[t]};
-                    ymin = std::min(ymin, dy);
-                    xmin = std::min(xmin, dx);
-                }
-            }
-            // window origin: keep inside the halo [-H, H]
-            int oy = std::min(ymin, H - (WY - 1));
-            int ox = std::min(xmin, H - (WX - 1));
-            oy = std::max(oy, -H);
-            ox = std::max(ox, -H);
-            const double Ek = 1.0 / (1.0 - d.beta * lam0);
-            RowEntry<real, WY, WX> &e = E[(size_t)j * napad + a];
-            e.oy = oy;
-            e.ox = ox;
-            e.E = (real)Ek;
-            for (int t = 0; t < ncn; ++t) {
-                const int r = cn[t].dy - oy, x = cn[t].dx - ox;
-                acc[r][x] += cn[t].w;
-            }
-            for (int r = 0; r < WY; ++r)
-                for (int x = 0; x < WX; ++x) e.W[r * WX + x] = (real)(d.beta * acc[r][x] * Ek);
-            oxmin = std::min(oxmin, ox);
-            oxmax = std::max(oxmax, ox);
-        }
-    }
-}
-
-// Smallest (WY, WX) window over all rows/controls; false if not row-uniform.
-static bool rowtab_window(const pdd_problem *p, const DProblem &d, int &WY, int &WX)
+// Row-uniform problem: every coefficient of the stencil depends on x2 only (and a constant cost).
+static bool row_uniform(const pdd_problem *p)
 {
     auto row_ok = [](const pdd_coef &c) { return c.kind == PDD_COEF_CONST || c.kind == PDD_COEF_ROW; };
     if (!row_ok(p->speed) || !row_ok(p->drift[0]) || !row_ok(p->drift[1])) return false;
     for (int k = 0; k < 2; ++k)
         for (int c = 0; c < 2; ++c)
             if (!row_ok(p->sigma[k][c])) return false;
-    if (p->cost.kind != PDD_COEF_CONST) return false;
-    if (na_pad_of(p->n_controls) == 0) return false;
-    const int n = p->n;
-    const int nb = p->p > 0 ? 2 * p->p : 1;
-    int ey = 0, ex = 0;
-    for (int j = 0; j < n; ++j) {
-        const double c = host_coef_at(p->speed, 0, j, n);
-        const double d1 = host_coef_at(p->drift[0], 0, j, n);
-        const double d2 = host_coef_at(p->drift[1], 0, j, n);
-        for (int a = 0; a < p->n_controls; ++a) {
-            const double bx = d.q * (c * p->controls[2 * a] + d1);
-            const double by = d.q * (c * p->controls[2 * a + 1] + d2);
-            int ymin = 1 << 30, ymax = -(1 << 30), xmin = 1 << 30, xmax = -(1 << 30);
-            for (int b = 0; b < nb; ++b) {
-                double xr = bx, yr = by;
-                if (p->p > 0) {
-                    const int kk = b >> 1;
-                    const double ox = d.sc * host_coef_at(p->sigma[kk][0], 0, j, n);
-                    const double oy = d.sc * host_coef_at(p->sigma[kk][1], 0, j, n);
-                    if (b & 1) { xr -= ox; yr -= oy; } else { xr += ox; yr += oy; }
-                }
-                yr = std::min(std::max(yr, (double)-j), (double)(n - 1 - j));
-                const int fx = (int)std::floor(xr);
-                const int fy = (int)std::min(std::floor(yr), (double)(n - 2 - j));
-                xmin = std::min(xmin, fx);
-                xmax = std::max(xmax, fx + 1);
-                ymin = std::min(ymin, fy);
-                ymax = std::max(ymax, fy + 1);
-            }
-            ey = std::max(ey, ymax - ymin + 1);
-            ex = std::max(ex, xmax - xmin + 1);
-        }
-    }
-    const int cand[3][2] = {{3, 3}, {2, 5}, {4, 4}};
-    for (auto &cw : cand)
-        if (ey <= cw[0] && ex <= cw[1]) { WY = cw[0]; WX = cw[1]; return true; }
-    return false;
+    return p->cost.kind == PDD_COEF_CONST;
 }
 
 static pdd_status prepare(pdd_ctx *ctx, int kernel_req)
@@ -701,11 +594,17 @@ static pdd_status prepare(pdd_ctx *ctx, int kernel_req)
     const int H = halo_of(p);
     if (H > 8) return fail(ctx, PDD_E_STENCIL, "foot points reach %.2f cells; tile halo limited to 8",
                            reach_cells(p));
-    int WY = 0, WX = 0;
+    int WY = 0, WX = 0, oxmin = 0, oxmax = 0;
     int path = 1;
     const int napad = na_pad_of(p->n_controls);
-    if (kernel_req != 1 && rowtab_window(p, d, WY, WX) && rowtab_supported(WY, WX, napad / 32))
-        path = 2;
+    if (kernel_req != 1 && napad && row_uniform(p)) {
+        // the compact row stencils are built on the device (k_rowtab_extent / k_rowtab_fill)
+        if (rowtab_build_device(d, napad, H, ctx->precision, ctx->dev_int + 2, ctx->rowtab,
+                                ctx->rowtab_bytes, WY, WX, oxmin, oxmax, ctx->stream) &&
+            rowtab_supported(WY, WX, napad / 32))
+            path = 2;
+        CK(cudaGetLastError());
+    }
     if ((kernel_req == 2 || kernel_req == 3) && path != 2)
         return fail(ctx, PDD_E_INVALID, "row-table stencil requested but the problem is not row-uniform");
     // fp32 row-table problems use the 4-nodes-per-step kernel (path 3) unless kernel 3 asks for
@@ -721,25 +620,7 @@ static pdd_status prepare(pdd_ctx *ctx, int kernel_req)
     g.H = H;
     g.tiles_x = (p->n + g.TW - 1) / g.TW;
     g.tiles_y = (p->n + g.TH - 1) / g.TH;
-    int mod = 4;
-    if (path == 2) {
-        std::vector<unsigned char> buf;
-        int oxmin = 0, oxmax = 0;
-        const bool f32 = ctx->precision == 32;
-#define PDD_FILL(WY_, WX_)                                                                      \
-        if (WY == WY_ && WX == WX_) {                                                           \
-            if (f32) fill_rowtab<float, WY_, WX_>(p, d, napad, H, buf, oxmin, oxmax);           \
-            else fill_rowtab<double, WY_, WX_>(p, d, napad, H, buf, oxmin, oxmax);              \
-        }
-        PDD_FILL(3, 3)
-        PDD_FILL(2, 5)
-        PDD_FILL(4, 4)
-#undef PDD_FILL
-        if (buf.size() > ctx->rowtab_bytes)
-            return fail(ctx, PDD_E_NOMEM, "row table of %zu bytes exceeds its workspace slot", buf.size());
-        CK(cudaMemcpy(ctx->rowtab, buf.data(), buf.size(), cudaMemcpyHostToDevice));
-        mod = std::max(1, oxmax - oxmin + 1);
-    }
+    const int mod = path == 2 ? std::max(1, oxmax - oxmin + 1) : 4;
     const int banks = ctx->precision == 32 ? 32 : 16;
     int pitch = g.TW + 2 * H;
     if (g4) {
@@ -1100,17 +981,14 @@ pdd_status pdd_get_values(pdd_ctx *ctx, void *dst, int32_t dst_on_device, int32_
     if (!ctx) return fail(nullptr, PDD_E_INVALID, "ctx is NULL");
     const size_t N = (size_t)ctx->fine.n * ctx->fine.n;
     if (as_fp64) return fetch(ctx, dst, ctx->V, sizeof(double) * N, dst_on_device);
-    if (!dst_on_device) {
-        std::vector<double> h(N);
-        pdd_status r = fetch(ctx, h.data(), ctx->V, sizeof(double) * N, 0);
-        if (r != PDD_OK) return r;
-        float *f = (float *)dst;
-        for (size_t k = 0; k < N; ++k) f[k] = (float)h[k];
-        return PDD_OK;
-    }
-    k_to_f32<<<4 * 148, 256, 0, ctx->stream>>>(ctx->V, (float *)dst, (int64_t)N);
+    if (!dst) return fail(ctx, PDD_E_INVALID, "dst is NULL");
+    // convert on the device; host destinations get one D2H copy of the fp32 staging buffer
+    float *f = dst_on_device ? (float *)dst : ctx->f32buf;
+    k_to_f32<<<4 * 148, 256, 0, ctx->stream>>>(ctx->V, f, (int64_t)N);
     ctx->launches++;
     CK(cudaGetLastError());
+    if (!dst_on_device)
+        CK(cudaMemcpyAsync(dst, f, sizeof(float) * N, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     return PDD_OK;
 }

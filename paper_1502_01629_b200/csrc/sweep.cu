@@ -39,14 +39,10 @@
 
 namespace pdd {
 
-#ifndef PDD_G_UNROLL
-#define PDD_G_UNROLL 2      // groups of 4 nodes unrolled per loop trip (path 3)
-#endif
 #ifndef PDD_MIN_BLOCKS
 #define PDD_MIN_BLOCKS 0    // override of the __launch_bounds__ min CTAs per SM (0 = per path)
 #endif
 
-constexpr int kGUnroll = PDD_G_UNROLL;
 // register cap per path: the GS row-table kernel (path 3) at 80 registers keeps 3 CTAs (24
 // warps) per SM without spills -- measured 1.6x faster than its unconstrained 137-register build
 template <int PATH>
@@ -711,6 +707,142 @@ void launch_activate(const TileGeom &g, TileState &T, int out_list, double tol, 
 {
     k_activate<<<(n_tiles + 255) / 256, 256, 0, s>>>(g, T, out_list, tol, tol_act, thr, round,
                                                      n_tiles);
+}
+
+}  // namespace pdd
+
+namespace pdd {
+
+// ------------------------------------------------------------------ row-table construction
+// One thread per (row j, control a): the 2p foot points of an interior node of row j, relative to
+// the node (x not clamped: nodes within H of the x-boundary use the general stencil; y clamped
+// to the box as the row dictates, R5), in fp64.  k_rowtab_extent finds the smallest window
+// (WY x WX) holding every control's non-self corners; k_rowtab_fill writes the branch-merged
+// compact stencil W = beta w lambda / (1 - beta Lambda0), E = 1/(1 - beta Lambda0).
+__device__ __forceinline__ void rt_feet(const DProblem &P, int j, int a, int b, double &xr,
+                                        double &yr)
+{
+    const int n = P.n;
+    const double c = coef_at(P.speed, 0, j, n);
+    const double d1 = coef_at(P.drift[0], 0, j, n);
+    const double d2 = coef_at(P.drift[1], 0, j, n);
+    xr = P.q * (c * P.ctrl[2 * a] + d1);
+    yr = P.q * (c * P.ctrl[2 * a + 1] + d2);
+    if (P.p > 0) {
+        const int kk = b >> 1;
+        const double ox = P.sc * coef_at(P.sigma[kk][0], 0, j, n);
+        const double oy = P.sc * coef_at(P.sigma[kk][1], 0, j, n);
+        if (b & 1) { xr -= ox; yr -= oy; } else { xr += ox; yr += oy; }
+    }
+    yr = fmin(fmax(yr, (double)-j), (double)(n - 1 - j));
+}
+
+__global__ void k_rowtab_extent(DProblem P, int *ext)
+{
+    const int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (id >= (int64_t)P.n * P.na) return;
+    const int j = (int)(id / P.na), a = (int)(id % P.na);
+    const int nb = P.p > 0 ? 2 * P.p : 1;
+    int ymin = 1 << 30, ymax = -(1 << 30), xmin = 1 << 30, xmax = -(1 << 30);
+    for (int b = 0; b < nb; ++b) {
+        double xr, yr;
+        rt_feet(P, j, a, b, xr, yr);
+        const int fx = (int)floor(xr);
+        const int fy = (int)fmin(floor(yr), (double)(P.n - 2 - j));
+        xmin = min(xmin, fx); xmax = max(xmax, fx + 1);
+        ymin = min(ymin, fy); ymax = max(ymax, fy + 1);
+    }
+    atomicMax(&ext[0], ymax - ymin + 1);
+    atomicMax(&ext[1], xmax - xmin + 1);
+}
+
+template <typename real, int WY, int WX>
+__global__ void k_rowtab_fill(DProblem P, int napad, int H, RowEntry<real, WY, WX> *tab, int *oxr)
+{
+    const int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (id >= (int64_t)P.n * napad) return;
+    const int j = (int)(id / napad), a = (int)(id % napad);
+    RowEntry<real, WY, WX> e;
+    e.oy = 0; e.ox = 0; e.E = 0;
+#pragma unroll
+    for (int m = 0; m < WY * WX; ++m) e.W[m] = 0;
+    if (a < P.na) {
+        const int nb = P.p > 0 ? 2 * P.p : 1;
+        const double w = 1.0 / nb;
+        int cdy[8 * 4], cdx[8 * 4];
+        double cw[8 * 4];
+        int ncn = 0, ymin = 1 << 30, xmin = 1 << 30;
+        double lam0 = 0.0;
+        for (int b = 0; b < nb; ++b) {
+            double xr, yr;
+            rt_feet(P, j, a, b, xr, yr);
+            const double fx = floor(xr);
+            const double fy = fmin(floor(yr), (double)(P.n - 2 - j));
+            const double tx = xr - fx, ty = yr - fy;
+            const double ww[4] = {(1 - tx) * (1 - ty), tx * (1 - ty), (1 - tx) * ty, tx * ty};
+            for (int t = 0; t < 4; ++t) {
+                const int dx = (int)fx + (t & 1), dy = (int)fy + (t >> 1);
+                if (dx == 0 && dy == 0) { lam0 += w * ww[t]; continue; }
+                cdy[ncn] = dy; cdx[ncn] = dx; cw[ncn] = w * ww[t]; ++ncn;
+                ymin = min(ymin, dy); xmin = min(xmin, dx);
+            }
+        }
+        int oy = max(min(ymin, H - (WY - 1)), -H);
+        int ox = max(min(xmin, H - (WX - 1)), -H);
+        const double Ek = 1.0 / (1.0 - P.beta * lam0);
+        double acc[WY * WX];
+#pragma unroll
+        for (int m = 0; m < WY * WX; ++m) acc[m] = 0.0;
+        for (int t = 0; t < ncn; ++t) {
+            const int r = cdy[t] - oy, x = cdx[t] - ox;
+            if (r >= 0 && r < WY && x >= 0 && x < WX) acc[r * WX + x] += cw[t];
+        }
+        e.oy = oy; e.ox = ox; e.E = (real)Ek;
+#pragma unroll
+        for (int m = 0; m < WY * WX; ++m) e.W[m] = (real)(P.beta * acc[m] * Ek);
+        atomicMin(&oxr[0], ox);
+        atomicMax(&oxr[1], ox);
+    }
+    tab[id] = e;
+}
+
+bool rowtab_build_device(const DProblem &P, int napad, int H, int precision, int *scratch,
+                         void *tab, size_t tab_bytes, int &WY, int &WX, int &oxmin, int &oxmax,
+                         cudaStream_t s)
+{
+    int h[4] = {0, 0, 1 << 30, -(1 << 30)};
+    if (cudaMemcpyAsync(scratch, h, sizeof h, cudaMemcpyHostToDevice, s) != cudaSuccess) return false;
+    const int64_t m = (int64_t)P.n * P.na;
+    k_rowtab_extent<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(P, scratch);
+    if (cudaMemcpyAsync(h, scratch, 2 * sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess) return false;
+    if (cudaStreamSynchronize(s) != cudaSuccess) return false;
+    const int cand[3][2] = {{3, 3}, {2, 5}, {4, 4}};
+    WY = WX = 0;
+    for (auto &cw : cand)
+        if (h[0] <= cw[0] && h[1] <= cw[1]) { WY = cw[0]; WX = cw[1]; break; }
+    if (!WY) return false;
+    const int64_t mt = (int64_t)P.n * napad;
+    if ((size_t)mt * rowtab_entry_bytes(precision, WY, WX) > tab_bytes) return false;
+    const unsigned grid = (unsigned)((mt + 127) / 128);
+#define PDD_RTF(WY_, WX_)                                                                        \
+    if (WY == WY_ && WX == WX_) {                                                                \
+        if (precision == 32)                                                                     \
+            k_rowtab_fill<float, WY_, WX_><<<grid, 128, 0, s>>>(                                 \
+                P, napad, H, reinterpret_cast<RowEntry<float, WY_, WX_> *>(tab), scratch + 2);   \
+        else                                                                                     \
+            k_rowtab_fill<double, WY_, WX_><<<grid, 128, 0, s>>>(                                \
+                P, napad, H, reinterpret_cast<RowEntry<double, WY_, WX_> *>(tab), scratch + 2);  \
+    }
+    PDD_RTF(3, 3)
+    PDD_RTF(2, 5)
+    PDD_RTF(4, 4)
+#undef PDD_RTF
+    if (cudaMemcpyAsync(h + 2, scratch + 2, 2 * sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess)
+        return false;
+    if (cudaStreamSynchronize(s) != cudaSuccess) return false;
+    oxmin = h[2];
+    oxmax = h[3];
+    return true;
 }
 
 }  // namespace pdd

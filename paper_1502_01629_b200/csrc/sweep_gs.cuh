@@ -23,6 +23,15 @@
 // Window loads: copy q is chosen so that window column t = 0 is 16-byte aligned; columns 0..3
 // come from one LDS.128, columns 4.. from a second LDS.64 / LDS.128.
 
+#ifndef PDD_SPIN_NS
+#define PDD_SPIN_NS 0     // 0: plain spin on the shared-memory progress counter
+#endif
+#if PDD_SPIN_NS > 0
+#define PDD_SPIN_PAUSE() __nanosleep(PDD_SPIN_NS)
+#else
+#define PDD_SPIN_PAUSE() ((void)0)
+#endif
+
 template <int CPL, int WY, int WX, bool CHECK, bool XNEG>
 __device__ __forceinline__ void row_gs4(const KP<float> &A, float *s_u, const float *s_ctrl,
                                         volatile int *s_prog, int pitch, int cstride, int H,
@@ -72,7 +81,7 @@ __device__ __forceinline__ void row_gs4(const KP<float> &A, float *s_u, const fl
         const int g = 4 * G;
         if (!CHECK && jj > 0) {
             const int need = base + min(gs + lead, NG);
-            while (s_prog[jj - 1] < need) __nanosleep(20);
+            while (s_prog[jj - 1] < need) PDD_SPIN_PAUSE();
             __threadfence_block();
         }
         // candidate sums, one control at a time (the window of a control is dead once its four
