@@ -31,12 +31,6 @@ constexpr size_t kAlign = 256;
 constexpr int kMaxPatches = 32768;
 constexpr int64_t kMaxCoarseSweeps = 1 << 20;
 
-struct HostCoefInfo {
-    int kind;
-    double value;
-    size_t count;   // doubles to copy
-};
-
 size_t coef_count(const pdd_coef &c, int n)
 {
     switch (c.kind) {
@@ -198,16 +192,6 @@ static double coef_max_abs(const pdd_coef &c, int n)
     double m = 0.0;
     for (size_t i = 0; i < cnt; ++i) m = std::max(m, std::fabs(c.data[i]));
     return m;
-}
-
-static double host_coef_at(const pdd_coef &c, int i, int j, int n)
-{
-    switch (c.kind) {
-    case 0: return c.value;
-    case 1: return c.data[j];
-    case 2: return c.data[i];
-    default: return c.data[(size_t)j * n + i];
-    }
 }
 
 // reach of the foot points in cells (R4): (h max|f| + sc max|sigma_j|)/dx
