@@ -159,8 +159,10 @@ void launch_tile_init(const DProblem &P, const TileGeom &g, const double *uhat,
                       const int16_t *labels, TileState &T, cudaStream_t s);
 void launch_set_values(const DProblem &P, int mode, const double *uhat, double *V,
                        cudaStream_t s);
+// slack >= 0: patchy upstream-ready rule (a tile waits for unconverged neighbours whose min u_hat
+// is lower by more than slack); < 0: off
 void launch_activate(const TileGeom &g, TileState &T, int out_list, double tol, double tol_act,
-                     double thr, int round, int n_tiles, cudaStream_t s);
+                     double thr, int round, int n_tiles, cudaStream_t s, double slack = -1.0);
 cudaError_t launch_sweep(const SweepLaunch &L, cudaStream_t s);
 bool rowtab_supported(int WY, int WX, int cpl);
 int rowtab_tw(int WY, int WX);

@@ -663,12 +663,13 @@ static double bits_to_double(unsigned long long b)
     return d;
 }
 
-static pdd_status activate(pdd_ctx *ctx, int out_list, double tol, double thr, int round)
+static pdd_status activate(pdd_ctx *ctx, int out_list, double tol, double thr, int round,
+                           double slack = -1.0)
 {
     cudaStream_t s = ctx->stream;
     CK(cudaMemsetAsync(ctx->T.counters, 0, sizeof(ActCounters), s));
     CK(cudaMemsetAsync(&reinterpret_cast<ActCounters *>(ctx->T.counters)->min_pending, 0xff, 8, s));
-    launch_activate(ctx->g, ctx->T, out_list, tol, tol, thr, round, ctx->n_tiles, s);
+    launch_activate(ctx->g, ctx->T, out_list, tol, tol, thr, round, ctx->n_tiles, s, slack);
     ctx->launches++;
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(ctx->h_cnt, ctx->T.counters, sizeof(ActCounters), cudaMemcpyDeviceToHost, s));
@@ -825,6 +826,14 @@ pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
     // (measured on C5: ~8 cells of front travel per round minimises time-to-converge)
     if (delta == 0.0) delta = ctx->g.TW * ctx->fine.h * d.lmax / 8.0;
     double thr = delta > 0.0 ? -1.0 : INFINITY;
+    // bucket policy 2 (patchy): no moving threshold; a tile is admitted once its upstream
+    // neighbours (min u_hat lower by more than a quarter tile of travel) have converged
+    double ready_slack = -1.0;
+    if (o->mode == 0 && o->reserved[1] == 2) {
+        ready_slack = o->delta > 0.0 ? o->delta : 0.25 * ctx->g.TH * ctx->fine.h * d.lmax;
+        thr = INFINITY;
+        delta = -1.0;
+    }
 
     pdd_solve_stats S{};
     S.n_tiles = ctx->n_tiles;
@@ -842,7 +851,7 @@ pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
     }
     while (o->schedule != 1) {
         if (S.rounds >= o->max_rounds) break;
-        pdd_status r = activate(ctx, cur, o->tol, thr, round);
+        pdd_status r = activate(ctx, cur, o->tol, thr, round, ready_slack);
         if (r != PDD_OK) return r;
         const ActCounters c = *ctx->h_cnt;
         if (trace && (round < 40 || round % trace == 0))
@@ -883,7 +892,7 @@ pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
         S.rounds++;
         S.verify_passes++;
         ++round;
-        r = activate(ctx, cur, o->tol, INFINITY, round);
+        r = activate(ctx, cur, o->tol, INFINITY, round, ready_slack);
         if (r != PDD_OK) return r;
         float ms = 0.f;
         cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]);

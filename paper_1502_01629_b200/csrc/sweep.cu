@@ -644,7 +644,7 @@ void launch_set_values(const DProblem &P, int mode, const double *uhat, double *
 }
 
 __global__ void k_activate(TileGeom g, TileState T, int out_list, double tol, double tol_act,
-                           double thr, int round, int n_tiles)
+                           double thr, int round, int n_tiles, double slack)
 {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     ActCounters *C = reinterpret_cast<ActCounters *>(T.counters);
@@ -664,6 +664,24 @@ __global__ void k_activate(TileGeom g, TileState T, int out_list, double tol, do
                         if ((dx | dy) == 0 || ax < 0 || ay < 0 || ax >= g.tiles_x || ay >= g.tiles_y)
                             continue;
                         if (T.tile_chg[ay * g.tiles_x + ax] >= tol_act) { need = true; break; }
+                    }
+            }
+            if (need && slack >= 0.0) {
+                // upstream-ready rule (patchy): wait while a neighbour whose min u_hat is lower by
+                // more than `slack` (an upstream tile in the causal order) has not
+                // converged yet -- the GPU form of processing the nodes in increasing u_hat
+                const double mu = T.tile_minu[t];
+                const int tx = t % g.tiles_x, ty = t / g.tiles_x;
+                for (int dy = -1; dy <= 1 && need; ++dy)
+                    for (int dx = -1; dx <= 1; ++dx) {
+                        const int ax = tx + dx, ay = ty + dy;
+                        if ((dx | dy) == 0 || ax < 0 || ay < 0 || ax >= g.tiles_x || ay >= g.tiles_y)
+                            continue;
+                        const int nb = ay * g.tiles_x + ax;
+                        if (T.tile_free[nb] > 0 && T.tile_minu[nb] < mu - slack && T.tile_res[nb] >= tol) {
+                            need = false;
+                            break;
+                        }
                     }
             }
             if (need) {
@@ -703,10 +721,10 @@ __global__ void k_activate(TileGeom g, TileState T, int out_list, double tol, do
 }
 
 void launch_activate(const TileGeom &g, TileState &T, int out_list, double tol, double tol_act,
-                     double thr, int round, int n_tiles, cudaStream_t s)
+                     double thr, int round, int n_tiles, cudaStream_t s, double slack)
 {
     k_activate<<<(n_tiles + 255) / 256, 256, 0, s>>>(g, T, out_list, tol, tol_act, thr, round,
-                                                     n_tiles);
+                                                     n_tiles, slack);
 }
 
 }  // namespace pdd

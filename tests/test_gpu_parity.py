@@ -158,3 +158,23 @@ def test_solve_parity_random_general_fp64():
     st = s.solve("static", tol=1e-13, k_inner=4)    # bound 1e-13/(1-beta) < 1e-11
     assert st["converged"] == 1
     assert np.abs(s.get_values() - ref["V"]).max() <= 1e-10
+
+
+@pytest.mark.parametrize("mode,schedule,policy", [
+    ("patchy", "ordered", 0), ("static", "ordered", 0), ("patchy", "rounds", 1),
+    ("patchy", "rounds", 2)])
+def test_schedules_reach_the_same_fixed_point(mode, schedule, policy):
+    """Every tile schedule (ordered Gauss-Seidel passes, Delta-stepping buckets, upstream-ready
+    admission) converges to the oracle's fixed point (R29)."""
+    inst = I.make_config("C5", n=513)
+    ref = O.jacobi(inst, tol=_tight_tol(inst, 2e-11), max_sweeps=10**6)
+    s = _solver(inst, 32)
+    if mode == "patchy":
+        s.coarse_solve(inst.tol_coarse)
+        s.synthesize()
+        s.build_patches(inst.n_patches)
+    else:
+        s.build_static(*inst.static_blocks)
+    st = s.solve(mode, tol=1e-7, k_inner=4, schedule=schedule, bucket_policy=policy)
+    assert st["converged"] == 1
+    assert np.abs(s.get_values() - ref["V"]).max() <= 5e-5 * np.abs(ref["V"]).max()
