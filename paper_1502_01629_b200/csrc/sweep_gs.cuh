@@ -32,6 +32,37 @@
 #define PDD_SPIN_PAUSE() ((void)0)
 #endif
 
+// Row-pipeline progress counters: release store by the producing warp (after __syncwarp, so the
+// whole warp's node commits are ordered before it), acquire load by the consumer -- lighter than
+// two CTA-wide sequentially consistent fences per group.
+#ifndef PDD_ACQREL
+#define PDD_ACQREL 1
+#endif
+__device__ __forceinline__ void prog_release(volatile int *p, int v)
+{
+#if PDD_ACQREL
+    const unsigned a = (unsigned)__cvta_generic_to_shared((const void *)p);
+    asm volatile("st.release.cta.shared.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+#else
+    __threadfence_block();
+    *p = v;
+#endif
+}
+
+__device__ __forceinline__ int prog_acquire(volatile int *p)
+{
+#if PDD_ACQREL
+    const unsigned a = (unsigned)__cvta_generic_to_shared((const void *)p);
+    int v;
+    asm volatile("ld.acquire.cta.shared.s32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+#else
+    const int v = *p;
+    __threadfence_block();
+    return v;
+#endif
+}
+
 template <int CPL, int WY, int WX, bool CHECK, bool XNEG>
 __device__ __forceinline__ void row_gs4(const KP<float> &A, float *s_u, const float *s_ctrl,
                                         volatile int *s_prog, int pitch, int cstride, int H,
@@ -81,8 +112,7 @@ __device__ __forceinline__ void row_gs4(const KP<float> &A, float *s_u, const fl
         const int g = 4 * G;
         if (!CHECK && jj > 0) {
             const int need = base + min(gs + lead, NG);
-            while (s_prog[jj - 1] < need) PDD_SPIN_PAUSE();
-            __threadfence_block();
+            while (prog_acquire(s_prog + jj - 1) < need) PDD_SPIN_PAUSE();
         }
         // candidate sums, one control at a time (the window of a control is dead once its four
         // sums are formed: keeps the live set small enough for 3 CTAs / SM without remat)
@@ -166,10 +196,7 @@ __device__ __forceinline__ void row_gs4(const KP<float> &A, float *s_u, const fl
         }
         if (!CHECK) {
             __syncwarp();
-            if (lane == 0) {
-                __threadfence_block();
-                s_prog[jj] = base + gs + 1;
-            }
+            if (lane == 0) prog_release(s_prog + jj, base + gs + 1);
         } else {
             __syncwarp();
         }
