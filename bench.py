@@ -299,18 +299,21 @@ def main():
         del s
         torch.cuda.synchronize()
         barrier(world)
-        t0 = time.perf_counter()
+        # device-timed (CUDA events on the stream; host gaps between the calls are inside the
+        # interval because the events complete in stream order)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
         e_nu = 0
         for _ in range(max(1, min(args.steps, 2))):
-            se = Solver(inst, precision=args.precision, device=str(dev), views=views)
+            se = Solver(inst, precision=args.precision, device=str(dev), views=views, stream=stream)
             st_e = pipeline_step(se, inst, args)
             se.get_values_into(hostV, on_device=False, as_fp64=(args.precision == 64))
             e_nu += st_e["node_updates"]
             se.close()
             del se
+        e1.record(stream)
         torch.cuda.synchronize()
-        t_e = allreduce(time.perf_counter() - t0, dist.ReduceOp.MAX if world > 1 else None, world)
-        e_nu = allreduce(e_nu, dist.ReduceOp.SUM if world > 1 else None, world)
+        e_nu, t_e, _ = aggregate(e_nu, e0.elapsed_time(e1) * 1e-3, world)
         e2e = {"value": e_nu / t_e, "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": int(hostV.numel() * hostV.element_size())}
 
