@@ -166,7 +166,7 @@ class Solver:
         self._ck(N.lib().pdd_build_static(self._ctx, int(px), int(py)))
 
     def solve(self, mode="patchy", tol: float = 1e-6, k_inner: int = 4,
-              max_rounds: int = 10**7, delta: float = 0.0, kernel: int = 0,
+              max_rounds: int = 200000, delta: float = 0.0, kernel: int = 0,
               schedule: str = "rounds", raise_on_noconverge: bool = True,
               early_exit: bool = True, bucket_policy: int = 0) -> dict:
         o = N.pdd_solve_opts()

@@ -748,6 +748,8 @@ static pdd_status ordered_loop(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_
     O.key_slack = o->mode == 1 ? 0.0 : (o->delta > 0.0 ? o->delta : 0.25 * g.TH * ctx->fine.h * ctx->F.d.lmax);
     OrdCounters h{};
     int pass = 0;
+    double best = INFINITY;
+    int stalled = 0;
     while (S.rounds < o->max_rounds) {
         O.pass = ++pass;
         CK(cudaMemsetAsync(oc, 0, offsetof(OrdCounters, seq), s));
@@ -790,6 +792,8 @@ static pdd_status ordered_loop(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_
             converged = true;
             break;
         }
+        if (last_verify < 0.9 * best) { best = last_verify; stalled = 0; }
+        else if (++stalled >= 8) break;   // below the arithmetic's noise floor: give up
     }
     return PDD_OK;
 }
@@ -842,6 +846,12 @@ pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
     const char *tenv = std::getenv("PDD_TRACE");   // development: per-round trace every N rounds
     const int trace = tenv ? std::max(1, std::atoi(tenv)) : 0;
     int round = 0;
+    double best_verify = INFINITY;
+    int stalled = 0;
+    // rounds between forced verifications: a tolerance below the noise floor keeps tiles
+    // re-activating each other forever; a legitimate sweep front needs far fewer rounds
+    const int verify_every = 4 * ctx->n_tiles + 1024;
+    int since_verify = 0;
     bool converged = false;
     double last_verify = INFINITY;
     float ms_sweep = 0.f, ms_verify = 0.f;
@@ -857,7 +867,7 @@ pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
         if (trace && (round < 40 || round % trace == 0))
             fprintf(stderr, "[pdd] round %d active %d free %lld maxres %.3e thr %.4f\n", round,
                     c.count, (long long)c.free_sum, bits_to_double(c.max_res), thr);
-        if (c.count > 0) {
+        if (c.count > 0 && since_verify < verify_every) {
             CK(cudaMemsetAsync(ctx->T.tile_chg, 0, sizeof(double) * ctx->n_tiles, s));
             CK(cudaEventRecord(ctx->ev[2], s));
             SweepLaunch L = make_launch(ctx, ctx->T.list[cur], c.count, o->k_inner, 0, nullptr);
@@ -875,14 +885,16 @@ pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
             // 1 = classic Delta-stepping, the next bucket opens when this one has settled
             if (delta > 0.0 && o->reserved[1] == 0) thr += delta;
             ++round;
+            ++since_verify;
             continue;
         }
         const double pend = bits_to_double(c.min_pending);
-        if (c.min_pending != 0xffffffffffffffffull && std::isfinite(pend)) {
+        if (c.count == 0 && c.min_pending != 0xffffffffffffffffull && std::isfinite(pend)) {
             thr = std::max(thr, pend) + (delta > 0.0 ? delta : 0.0);
             continue;
         }
-        // nothing active: full-grid Jacobi verification
+        // nothing active (or verify_every rounds since the last one): full-grid verification
+        since_verify = 0;
         CK(cudaEventRecord(ctx->ev[2], s));
         SweepLaunch L = make_launch(ctx, ctx->T.all_list, ctx->n_tiles, 1, 1, nullptr);
         CK(launch_sweep(L, s));
@@ -899,6 +911,11 @@ pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
         ms_verify += ms;
         last_verify = bits_to_double(ctx->h_cnt->max_res);
         if (ctx->h_cnt->count == 0) { converged = true; break; }
+        // stagnation guard: a tolerance below the arithmetic's noise floor (fp32: ~1 ulp of the
+        // tile-relative values) cannot be reached; stop after 8 verifications without a 10 %
+        // improvement of the best residual instead of iterating until max_rounds
+        if (last_verify < 0.9 * best_verify) { best_verify = last_verify; stalled = 0; }
+        else if (++stalled >= 8) break;
         thr = INFINITY;   // after a verification every offending tile is eligible
     }
     CK(cudaEventRecord(ctx->ev[1], s));
