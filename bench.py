@@ -59,7 +59,8 @@ def parse():
     ap.add_argument("--config", default="C5")
     ap.add_argument("--n", type=int, default=None, help="override grid size (not for the headline)")
     ap.add_argument("--precision", type=int, default=32)
-    ap.add_argument("--k-inner", type=int, default=4)
+    ap.add_argument("--k-inner", type=int, default=None,
+                    help="sweeps per tile visit (default: the API's per-mode default, 1 patchy / 4 static)")
     ap.add_argument("--tol", type=float, default=1e-7)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -357,7 +358,7 @@ def main():
                                    f" synthesis, {inst.n_patches} patch labels, fine solve to "
                                    f"tol {args.tol:g}) on {inst.n}^2",
                        "grid": inst.n, "controls": inst.n_controls, "branches": 2 * inst.p,
-                       "patches": inst.n_patches, "k_inner": args.k_inner,
+                       "patches": inst.n_patches, "k_inner": args.k_inner if args.k_inner is not None else {"patchy": 1, "static": 4},
                        "l2": "inputs larger than L2 (V fp64 %d MB)" % (inst.n * inst.n * 8 >> 20),
                        "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
             "time_to_converge": {"patchy_s": t_solve / args.steps,

@@ -165,12 +165,14 @@ class Solver:
     def build_static(self, px: int, py: int) -> None:
         self._ck(N.lib().pdd_build_static(self._ctx, int(px), int(py)))
 
-    def solve(self, mode="patchy", tol: float = 1e-6, k_inner: int = 4,
+    def solve(self, mode="patchy", tol: float = 1e-6, k_inner: Optional[int] = None,
               max_rounds: int = 200000, delta: float = 0.0, kernel: int = 0,
               schedule: str = "rounds", raise_on_noconverge: bool = True,
               early_exit: bool = True, bucket_policy: int = 0) -> dict:
         o = N.pdd_solve_opts()
         o.mode = MODE_PATCHY if mode in ("patchy", 0) else MODE_STATIC
+        if k_inner is None:   # sweeps per tile visit: measured best per mode
+            k_inner = 1 if o.mode == MODE_PATCHY else 4
         o.k_inner, o.tol, o.max_rounds, o.delta, o.kernel = int(k_inner), float(tol), int(max_rounds), float(delta), int(kernel)
         o.schedule = 1 if schedule in ("ordered", 1) else 0
         o.reserved[0] = 0 if early_exit else 1
@@ -237,7 +239,7 @@ class Solver:
         return int(N.lib().pdd_kernel_launches(self._ctx))
 
     # ------------------------------------------------------------------ convenience
-    def run_patchy(self, tol: float, k_inner: int = 4, tol_c: float = 1e-12, **kw) -> dict:
+    def run_patchy(self, tol: float, k_inner: Optional[int] = None, tol_c: float = 1e-12, **kw) -> dict:
         out = {"coarse": self.coarse_solve(tol_c)}
         self.synthesize()
         self.build_patches(self.inst.n_patches)

@@ -80,6 +80,9 @@ struct TileState {
     double *tile_res;        // last in-tile residual (or verification residual)
     double *tile_chg;        // net change of the last visit (0 if not visited this round)
     int16_t *tile_lab;       // up to 4 distinct patch labels per tile (-1 unused)
+    uint8_t *tile_orient;    // first in-tile sweep orientation (bit 0: -x, bit 1: -y)
+    int32_t *tile_stamp;     // sweep id that wrote tile_chg (valid iff == RoundCtl::sweep_id)
+    int32_t *tile_sweeps;    // in-tile sweeps done so far this solve (orientation schedule)
     int32_t *list[2];        // active tile lists
     int32_t *all_list;       // tiles with free nodes
     int32_t *patch_round;    // per patch: last round with an active tile
@@ -105,10 +108,29 @@ struct OrdCounters {
 
 struct ActCounters {
     int32_t count;
-    int32_t pad;
+    int32_t fetch;                    // device-driven rounds: next list entry to take
     long long free_sum;
     unsigned long long min_pending;   // ordered bits of the min u_hat of needy ineligible tiles
     unsigned long long max_res;       // ordered bits of the max tile residual
+};
+
+// Device-driven rounds: the host enqueues batches of (begin, activate, sweep, end) without
+// synchronising; this block carries the round state between the kernels of a batch.
+struct RoundCtl {
+    double thr;              // bucket threshold of the moving front (patchy), +inf: none
+    double delta;            // threshold step per round (<= 0: no front)
+    double dboost;           // cap of the under-fill boost of the step
+    int resident;            // sweep CTAs the GPU holds at once
+    int policy;              // opts.reserved[1]
+    int stop;                // 0 run, 1 nothing active / verification due (host verifies)
+    int round;               // activation round counter (patch bookkeeping)
+    int sweep_id;            // sweeps launched so far; tile_chg valid iff tile_stamp == sweep_id
+    int since_verify;        // sweep rounds since the last verification
+    int verify_every;        // force a verification after this many
+    int pad;
+    double upw;              // >= 0: only neighbours with min u_hat <= own + upw re-activate
+    long long rounds;        // sweep rounds (pdd_solve_stats.rounds share)
+    long long tiles;         // tiles processed
 };
 
 // Ordered schedule (k_sweep_ordered): one Gauss-Seidel pass over the tiles in key order.
@@ -152,17 +174,33 @@ struct SweepLaunch {
     OrderArgs order;
     double early_tol;        // > 0: a tile visit stops after the first sweep changing < early_tol
     const int32_t *tile_free;            // free nodes per tile (node-update accounting)
+    const uint8_t *tile_orient;          // per-tile first sweep orientation (or null: +x+y)
+    int oxor = 0xE4;                     // sweep s mod 4 uses orientation o0 ^ ((oxor >> 2s) & 3)
+    double early_rel = 0.0;              // relative early exit (0: off)
+    int k_coherent = 1 << 30;            // sweeps per visit of a coherent tile
     unsigned long long *nu_counter;      // += free nodes x sweeps done, per visit (or NULL)
+    RoundCtl *ctl = nullptr;             // device-driven round: persistent grid, list/count from
+    ActCounters *acnt = nullptr;         //   the activation counters, stamps tile_chg
+    int32_t *tile_stamp = nullptr;
+    int32_t *tile_sweeps = nullptr;      // orientation schedule continues across visits
 };
 
+// device-driven round kernels (one thread each) around the activation and the sweep
+void launch_round_begin(RoundCtl *ctl, ActCounters *c, cudaStream_t s);
+void launch_round_end(RoundCtl *ctl, const ActCounters *c, cudaStream_t s);
+void launch_round_reset(RoundCtl *ctl, double thr, cudaStream_t s);
+
 void launch_tile_init(const DProblem &P, const TileGeom &g, const double *uhat,
-                      const int16_t *labels, TileState &T, cudaStream_t s);
+                      const int16_t *labels, TileState &T, cudaStream_t s, double coh_thr = 2.0);
 void launch_set_values(const DProblem &P, int mode, const double *uhat, double *V,
                        cudaStream_t s);
 // slack >= 0: patchy upstream-ready rule (a tile waits for unconverged neighbours whose min u_hat
 // is lower by more than slack); < 0: off
+// ctl != NULL: tile_chg counts only where tile_stamp == ctl->sweep_id; with from_ctl, thr and
+// round come from ctl and nothing happens once ctl->stop is set (device-driven rounds)
 void launch_activate(const TileGeom &g, TileState &T, int out_list, double tol, double tol_act,
-                     double thr, int round, int n_tiles, cudaStream_t s, double slack = -1.0);
+                     double thr, int round, int n_tiles, cudaStream_t s, double slack = -1.0,
+                     const RoundCtl *ctl = nullptr, bool from_ctl = false);
 cudaError_t launch_sweep(const SweepLaunch &L, cudaStream_t s);
 bool rowtab_supported(int WY, int WX, int cpl);
 int rowtab_tw(int WY, int WX);

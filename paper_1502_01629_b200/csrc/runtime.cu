@@ -119,6 +119,8 @@ struct pdd_ctx {
     // host pinned
     ActCounters *h_cnt = nullptr;
     int *h_int = nullptr;
+    RoundCtl *rctl = nullptr;      // device round state (workspace)
+    RoundCtl *h_ctl = nullptr;     // pinned host mirror
     // state
     bool coarse_done = false, synth_done = false;
     int labels_mode = 0;        // 0 none, 1 patchy, 2 static
@@ -131,7 +133,9 @@ struct pdd_ctx {
     int n_tiles = 0;
     int prepared_kernel = -1;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t evp[2][64] = {};  // per-round sweep-kernel timing inside a batch (lazy)
     long long launches = 0;     // kernels enqueued by this context (all calls)
+    bool mode_patchy = false;   // the current pdd_solve runs the patchy decomposition
 };
 
 static pdd_status fail(pdd_ctx *c, pdd_status s, const char *fmt, ...)
@@ -280,6 +284,9 @@ static size_t layout(pdd_ctx *c, void *ws, const pdd_problem *f, const pdd_probl
     T.tile_res = cv.take<double>(tmax);
     T.tile_chg = cv.take<double>(tmax);
     T.tile_lab = cv.take<int16_t>(4 * (size_t)tmax);
+    T.tile_orient = cv.take<uint8_t>(tmax);
+    T.tile_stamp = cv.take<int32_t>(tmax);
+    T.tile_sweeps = cv.take<int32_t>(tmax);
     T.list[0] = cv.take<int32_t>(tmax);
     T.list[1] = cv.take<int32_t>(tmax);
     T.all_list = cv.take<int32_t>(tmax);
@@ -292,7 +299,9 @@ static size_t layout(pdd_ctx *c, void *ws, const pdd_problem *f, const pdd_probl
     T.done = cv.take<int>(tmax);
     T.stamp = cv.take<long long>(tmax);
     T.ocounters = cv.take<OrdCounters>(1);
+    RoundCtl *rctl = cv.take<RoundCtl>(1);
     if (c) {
+        c->rctl = rctl;
         c->F = F;
         c->Cc = Cc;
         c->V = V;
@@ -388,13 +397,14 @@ pdd_status pdd_create(const pdd_problem *fine, const pdd_problem *coarse, int32_
     layout(ctx, base, fine, coarse);
     // host pinned scratch
     {
-        cudaError_t e = cudaHostAlloc((void **)&ctx->h_cnt, sizeof(ActCounters) + 64, 0);
+        cudaError_t e = cudaHostAlloc((void **)&ctx->h_cnt, sizeof(ActCounters) + 64 + sizeof(RoundCtl), 0);
         if (e != cudaSuccess) {
             pdd_status st = fail(nullptr, PDD_E_CUDA, "cudaHostAlloc: %s", cudaGetErrorString(e));
             delete ctx;
             return st;
         }
         ctx->h_int = reinterpret_cast<int *>(ctx->h_cnt + 1);
+        ctx->h_ctl = reinterpret_cast<RoundCtl *>(reinterpret_cast<char *>(ctx->h_cnt) + sizeof(ActCounters) + 64);
     }
     for (int k = 0; k < 4; ++k) cudaEventCreate(&ctx->ev[k]);
     s = copy_problem(ctx, fine, ctx->F, true);
@@ -422,6 +432,9 @@ void pdd_destroy(pdd_ctx *ctx)
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     for (int k = 0; k < 4; ++k)
         if (ctx->ev[k]) cudaEventDestroy(ctx->ev[k]);
+    for (int a = 0; a < 2; ++a)
+        for (int k = 0; k < 64; ++k)
+            if (ctx->evp[a][k]) cudaEventDestroy(ctx->evp[a][k]);
     if (ctx->h_cnt) cudaFreeHost(ctx->h_cnt);
     delete ctx;
 }
@@ -652,6 +665,14 @@ static SweepLaunch make_launch(pdd_ctx *ctx, const int32_t *list, int n_list, in
     L.check = check;
     L.precision = ctx->precision;
     L.tile_free = ctx->T.tile_free;
+    // patchy tiles know their downstream orientation from u_hat: two sweeps along it, then the
+    // x- and y-flipped ones; static tiles (no u_hat) cycle through all four (P:952-986 analogue)
+    const bool oriented = ctx->mode_patchy && !std::getenv("PDD_NO_ORIENT");   // env: A/B only
+    L.tile_orient = oriented ? ctx->T.tile_orient : nullptr;
+    L.oxor = oriented ? 0x90 : 0xE4;
+    if (const char *e = std::getenv("PDD_EREL")) L.early_rel = std::atof(e);   // A/B only
+    if (const char *e = std::getenv("PDD_KCOH")) L.k_coherent = std::atoi(e);   // A/B only
+    if (const char *e = std::getenv("PDD_OXOR")) L.oxor = (int)std::strtol(e, nullptr, 0);
     L.nu_counter = &reinterpret_cast<OrdCounters *>(ctx->T.ocounters)->updates;
     return L;
 }
@@ -669,7 +690,7 @@ static pdd_status activate(pdd_ctx *ctx, int out_list, double tol, double thr, i
     cudaStream_t s = ctx->stream;
     CK(cudaMemsetAsync(ctx->T.counters, 0, sizeof(ActCounters), s));
     CK(cudaMemsetAsync(&reinterpret_cast<ActCounters *>(ctx->T.counters)->min_pending, 0xff, 8, s));
-    launch_activate(ctx->g, ctx->T, out_list, tol, tol, thr, round, ctx->n_tiles, s, slack);
+    launch_activate(ctx->g, ctx->T, out_list, tol, tol, thr, round, ctx->n_tiles, s, slack, ctx->rctl);
     ctx->launches++;
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(ctx->h_cnt, ctx->T.counters, sizeof(ActCounters), cudaMemcpyDeviceToHost, s));
@@ -816,8 +837,13 @@ pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
     cudaStream_t s = ctx->stream;
     const DProblem &d = ctx->F.d;
     CK(cudaEventRecord(ctx->ev[0], s));
+    ctx->mode_patchy = o->mode == 0;
     launch_set_values(d, o->mode == 0 ? 0 : 1, ctx->uhat, ctx->V, s);
-    launch_tile_init(d, ctx->g, o->mode == 0 ? ctx->uhat : nullptr, ctx->labels, ctx->T, s);
+    // coherent tile: >= 90 % of its u_hat differences share the tile's sign in x and in y
+    // (measured: 0.8 .. 0.99 all within noise on C2 / C4 / C5)
+    const char *cenv = std::getenv("PDD_COH");     // A/B: coherence threshold (> 1: never)
+    launch_tile_init(d, ctx->g, o->mode == 0 ? ctx->uhat : nullptr, ctx->labels, ctx->T, s,
+                     cenv ? std::atof(cenv) : 0.9);
     ctx->launches += 2;
     CK(cudaMemsetAsync(ctx->T.patch_round, 0xff, sizeof(int32_t) * (ctx->n_patches + 1), s));
     CK(cudaMemsetAsync(ctx->T.patch_res, 0, sizeof(double) * (ctx->n_patches + 1), s));
@@ -828,11 +854,23 @@ pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
     if (o->mode == 1) delta = -1.0;
     // automatic bucket width: the value change across 1/8 of a tile width at unit speed
     // (measured on C5: ~8 cells of front travel per round minimises time-to-converge)
-    if (delta == 0.0) delta = ctx->g.TW * ctx->fine.h * d.lmax / 8.0;
+    if (delta == 0.0) {
+        const char *e = std::getenv("PDD_DSCALE");      // A/B only
+        delta = ctx->g.TW * ctx->fine.h * d.lmax / 8.0 * (e ? std::atof(e) : 1.0);
+    }
     double thr = delta > 0.0 ? -1.0 : INFINITY;
     // bucket policy 2 (patchy): no moving threshold; a tile is admitted once its upstream
     // neighbours (min u_hat lower by more than a quarter tile of travel) have converged
     double ready_slack = -1.0;
+    const char *benv = std::getenv("PDD_DBOOST");    // development override of the front boost cap
+    const double dboost = benv ? std::max(1.0, std::atof(benv)) : 1.0;
+    int resident = 148;
+    {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&resident, cudaDevAttrMultiProcessorCount, dev);
+        resident *= ctx->path == 3 ? 3 : 2;   // sweep CTAs resident per SM (launch_one's bounds)
+    }
     if (o->mode == 0 && o->reserved[1] == 2) {
         ready_slack = o->delta > 0.0 ? o->delta : 0.25 * ctx->g.TH * ctx->fine.h * d.lmax;
         thr = INFINITY;
@@ -845,13 +883,11 @@ pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
     int cur = 0;
     const char *tenv = std::getenv("PDD_TRACE");   // development: per-round trace every N rounds
     const int trace = tenv ? std::max(1, std::atoi(tenv)) : 0;
-    int round = 0;
     double best_verify = INFINITY;
     int stalled = 0;
     // rounds between forced verifications: a tolerance below the noise floor keeps tiles
     // re-activating each other forever; a legitimate sweep front needs far fewer rounds
     const int verify_every = 4 * ctx->n_tiles + 1024;
-    int since_verify = 0;
     bool converged = false;
     double last_verify = INFINITY;
     float ms_sweep = 0.f, ms_verify = 0.f;
@@ -859,64 +895,100 @@ pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
         pdd_status r = ordered_loop(ctx, o, S, trace, converged, last_verify, ms_sweep, ms_verify);
         if (r != PDD_OK) return r;
     }
+    // Device-driven rounds (schedule 0): batches of (begin, activate, sweep, end) are enqueued
+    // without a host round trip; the RoundCtl block carries the front threshold and the stop
+    // flag between them.  The host syncs once per batch and runs the verification pass.
+    if (o->schedule != 1) {
+        RoundCtl c0{};
+        c0.thr = thr;
+        c0.delta = delta;
+        c0.dboost = dboost;
+        c0.resident = resident;
+        c0.policy = o->reserved[1];
+        c0.verify_every = verify_every;
+        const char *ue = std::getenv("PDD_UPW");      // A/B: upstream-only re-activation slack
+        c0.upw = ue ? std::atof(ue) * ctx->g.TH * ctx->fine.h * d.lmax : -1.0;
+        *ctx->h_ctl = c0;
+        CK(cudaMemcpyAsync(ctx->rctl, ctx->h_ctl, sizeof(RoundCtl), cudaMemcpyHostToDevice, s));
+        CK(cudaMemsetAsync(ctx->T.tile_stamp, 0xff, sizeof(int32_t) * ctx->n_tiles, s));
+        CK(cudaMemsetAsync(ctx->T.tile_sweeps, 0, sizeof(int32_t) * ctx->n_tiles, s));
+    }
+    int batch = trace ? 1 : 4;
+    const char *te = std::getenv("PDD_TACT");   // A/B: neighbour-change activation threshold / tol
+    const double tact = te ? std::atof(te) : 1.0;
+    long long rounds_prev = 0;
     while (o->schedule != 1) {
         if (S.rounds >= o->max_rounds) break;
-        pdd_status r = activate(ctx, cur, o->tol, thr, round, ready_slack);
-        if (r != PDD_OK) return r;
-        const ActCounters c = *ctx->h_cnt;
-        if (trace && (round < 40 || round % trace == 0))
-            fprintf(stderr, "[pdd] round %d active %d free %lld maxres %.3e thr %.4f\n", round,
-                    c.count, (long long)c.free_sum, bits_to_double(c.max_res), thr);
-        if (c.count > 0 && since_verify < verify_every) {
-            CK(cudaMemsetAsync(ctx->T.tile_chg, 0, sizeof(double) * ctx->n_tiles, s));
-            CK(cudaEventRecord(ctx->ev[2], s));
-            SweepLaunch L = make_launch(ctx, ctx->T.list[cur], c.count, o->k_inner, 0, nullptr);
-            L.early_tol = o->reserved[0] ? 0.0 : o->tol;   // reserved[0] = 1 disables early exit
-            CK(launch_sweep(L, s));
-            ctx->launches++;
-            CK(cudaEventRecord(ctx->ev[3], s));
-            CK(cudaEventSynchronize(ctx->ev[3]));
-            float ms = 0.f;
-            cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]);
-            ms_sweep += ms;
-            S.rounds++;
-            S.tiles_processed += c.count;
-            // bucket policy (reserved[1]): 0 = the threshold advances every round (moving front),
-            // 1 = classic Delta-stepping, the next bucket opens when this one has settled
-            if (delta > 0.0 && o->reserved[1] == 0) thr += delta;
-            ++round;
-            ++since_verify;
-            continue;
-        }
-        const double pend = bits_to_double(c.min_pending);
-        if (c.count == 0 && c.min_pending != 0xffffffffffffffffull && std::isfinite(pend)) {
-            thr = std::max(thr, pend) + (delta > 0.0 ? delta : 0.0);
-            continue;
-        }
-        // nothing active (or verify_every rounds since the last one): full-grid verification
-        since_verify = 0;
         CK(cudaEventRecord(ctx->ev[2], s));
-        SweepLaunch L = make_launch(ctx, ctx->T.all_list, ctx->n_tiles, 1, 1, nullptr);
-        CK(launch_sweep(L, s));
+        SweepLaunch L = make_launch(ctx, ctx->T.list[cur], ctx->n_tiles, o->k_inner, 0, nullptr);
+        L.early_tol = o->reserved[0] ? 0.0 : o->tol;   // reserved[0] = 1 disables early exit
+        L.ctl = ctx->rctl;
+        L.acnt = reinterpret_cast<ActCounters *>(ctx->T.counters);
+        L.tile_stamp = ctx->T.tile_stamp;
+        if (!std::getenv("PDD_NO_SCONT")) L.tile_sweeps = ctx->T.tile_sweeps;   // env: A/B only
+        const long long room = o->max_rounds - S.rounds;
+        const int nb = (int)std::min<long long>(batch, std::max<long long>(room, 1));
+        if (!ctx->evp[0][0])
+            for (int a = 0; a < 2; ++a)
+                for (int k = 0; k < 64; ++k) CK(cudaEventCreate(&ctx->evp[a][k]));
+        for (int b = 0; b < nb; ++b) {
+            launch_round_begin(ctx->rctl, L.acnt, s);
+            launch_activate(ctx->g, ctx->T, cur, o->tol, o->tol * tact, 0.0, 0, ctx->n_tiles, s,
+                            ready_slack, ctx->rctl, true);
+            CK(cudaEventRecord(ctx->evp[0][b], s));
+            CK(launch_sweep(L, s));
+            CK(cudaEventRecord(ctx->evp[1][b], s));
+            launch_round_end(ctx->rctl, L.acnt, s);
+            ctx->launches += 4;
+        }
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(ctx->ev[3], s));
+        CK(cudaMemcpyAsync(ctx->h_ctl, ctx->rctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(ctx->h_cnt, L.acnt, sizeof(ActCounters), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]);
+        for (int b = 0; b < nb; ++b) {   // the sweep kernels alone (a stopped round's is ~0)
+            float mk = 0.f;
+            cudaEventElapsedTime(&mk, ctx->evp[0][b], ctx->evp[1][b]);
+            ms_sweep += mk;
+        }
+        const RoundCtl hc = *ctx->h_ctl;
+        S.rounds += hc.rounds - rounds_prev;
+        rounds_prev = hc.rounds;
+        S.tiles_processed = hc.tiles;
+        if (trace)
+            fprintf(stderr, "[pdd] batch %d rounds %lld active %d free %lld maxres %.3e thr %.4f stop %d %.4f ms\n",
+                    nb, hc.rounds, ctx->h_cnt->count, (long long)ctx->h_cnt->free_sum,
+                    bits_to_double(ctx->h_cnt->max_res), hc.thr, hc.stop, ms);
+        if (!hc.stop) {
+            batch = trace ? 1 : std::min(2 * batch, 64);
+            continue;
+        }
+        batch = trace ? 1 : 4;
+        // nothing active (or verify_every rounds since the last one): full-grid verification
+        CK(cudaEventRecord(ctx->ev[2], s));
+        SweepLaunch V = make_launch(ctx, ctx->T.all_list, ctx->n_tiles, 1, 1, nullptr);
+        CK(launch_sweep(V, s));
         ctx->launches++;
-        CK(cudaMemsetAsync(ctx->T.tile_chg, 0, sizeof(double) * ctx->n_tiles, s));
+        launch_round_reset(ctx->rctl, INFINITY, s);   // after a verification every offending
+        ctx->launches++;                              // tile is eligible; old changes superseded
         CK(cudaEventRecord(ctx->ev[3], s));
         S.rounds++;
         S.verify_passes++;
-        ++round;
-        r = activate(ctx, cur, o->tol, INFINITY, round, ready_slack);
+        pdd_status r = activate(ctx, cur, o->tol, INFINITY, 0, ready_slack);
         if (r != PDD_OK) return r;
-        float ms = 0.f;
+        ms = 0.f;
         cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]);
         ms_verify += ms;
         last_verify = bits_to_double(ctx->h_cnt->max_res);
+        if (trace) fprintf(stderr, "[pdd] verify residual %.3e active %d\n", last_verify, ctx->h_cnt->count);
         if (ctx->h_cnt->count == 0) { converged = true; break; }
         // stagnation guard: a tolerance below the arithmetic's noise floor (fp32: ~1 ulp of the
         // tile-relative values) cannot be reached; stop after 8 verifications without a 10 %
         // improvement of the best residual instead of iterating until max_rounds
         if (last_verify < 0.9 * best_verify) { best_verify = last_verify; stalled = 0; }
         else if (++stalled >= 8) break;
-        thr = INFINITY;   // after a verification every offending tile is eligible
     }
     CK(cudaEventRecord(ctx->ev[1], s));
     CK(cudaEventSynchronize(ctx->ev[1]));

@@ -95,6 +95,14 @@ struct KP {
     double early_tol;     // path 3: stop the in-tile sweeps once a sweep changes less than this
     const int32_t *tile_free;
     unsigned long long *nu_counter;
+    const uint8_t *tile_orient;
+    int oxor;             // packed 2-bit orientation xor per sweep mod 4
+    double early_rel;     // also stop once a sweep changes less than this x the first sweep
+    int k_coherent;       // in-tile sweeps of a coherent tile (tile_orient bit 2)
+    const RoundCtl *ctl;  // device-driven round (k_sweep_dyn), else NULL
+    ActCounters *acnt;
+    int32_t *tile_stamp;
+    int32_t *tile_sweeps;
 };
 
 __device__ __forceinline__ float rmin(float a, float b) { return fminf(a, b); }
@@ -347,8 +355,14 @@ __device__ __forceinline__ void sweep_tile(const KP<real> &A, int t, unsigned ch
     real res = 0;
     int done_sweeps = CHECK ? 1 : A.k_inner;
     if constexpr (PATH == 3 && sizeof(real) == 4) {
+        const int ot = A.tile_orient ? A.tile_orient[t] : 0;
+        const int kin = (ot & 4) ? min(A.k_inner, A.k_coherent) : A.k_inner;
+        // a coherent tile restarts from its downstream orientation on every visit; any other
+        // tile continues the orientation cycle where its last visit stopped
+        const int sbase = (A.tile_sweeps && !(ot & 4)) ? A.tile_sweeps[t] : 0;
         done_sweeps = tile_gs4<CPL, WY, WX, CHECK>(A, s_u, s_ctrl, s_prog, s_red, pitch,
-                                                   A.g.cstride, H, i0, j0, D, A.k_inner, res, Vref);
+                                                   A.g.cstride, H, i0, j0, D, kin, res, Vref, ot & 3,
+                                                   sbase);
     } else {
         const int sweeps = CHECK ? 1 : A.k_inner;
         for (int sw = 0; sw < sweeps; ++sw) {
@@ -407,6 +421,8 @@ __device__ __forceinline__ void sweep_tile(const KP<real> &A, int t, unsigned ch
     for (int w = 0; w < NW; ++w) cm = fmax(cm, s_red[w]);
     if (threadIdx.x == 0) {
         A.tile_chg[t] = cm;
+        if (A.tile_stamp) A.tile_stamp[t] = A.ctl->sweep_id + 1;
+        if (A.tile_sweeps) A.tile_sweeps[t] += done_sweeps;
         if (A.nu_counter)   // node-updates actually performed (early exit aware)
             atomicAdd(A.nu_counter, (unsigned long long)A.tile_free[t] * (unsigned long long)done_sweeps);
     }
@@ -420,6 +436,28 @@ __global__ void __launch_bounds__(NW * 32, min_blocks<PATH>()) k_sweep(KP<real> 
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     sweep_tile<real, PATH, CPL, WY, WX, CHECK>(A, A.list[blockIdx.x], smem_raw, nullptr, nullptr);
+}
+
+// Device-driven round: persistent CTAs take the activated tiles one at a time (dynamic fetch),
+// the count is the activation's -- no host round trip between activation and sweep.
+template <typename real, int PATH, int CPL, int WY, int WX>
+__global__ void __launch_bounds__(NW * 32, min_blocks<PATH>()) k_sweep_dyn(KP<real> A)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ int s_t;
+    if (A.ctl->stop) return;
+    const int count = A.acnt->count;
+    for (;;) {
+        if (threadIdx.x == 0) {
+            const int i = atomicAdd(&A.acnt->fetch, 1);
+            s_t = i < count ? A.list[i] : -1;
+        }
+        __syncthreads();
+        const int t = s_t;
+        __syncthreads();
+        if (t < 0) return;
+        sweep_tile<real, PATH, CPL, WY, WX, false>(A, t, smem_raw, nullptr, nullptr);
+    }
 }
 
 // Ordered schedule (one pass): persistent CTAs take tiles in ascending key order (P:744-749,
@@ -499,6 +537,14 @@ static cudaError_t launch_one(const SweepLaunch &L, cudaStream_t s)
     A.Hx = L.Hx;
     A.early_tol = L.early_tol;
     A.tile_free = L.tile_free;
+    A.tile_orient = L.tile_orient;
+    A.oxor = L.oxor;
+    A.early_rel = L.early_rel;
+    A.k_coherent = L.k_coherent;
+    A.ctl = L.ctl;
+    A.acnt = L.acnt;
+    A.tile_stamp = L.tile_stamp;
+    A.tile_sweeps = L.tile_sweeps;
     A.nu_counter = L.nu_counter;
     const size_t smem = NW * sizeof(double) + TH * sizeof(int) + 256 * sizeof(real) +
                         (PATH == 3 ? (size_t)4 * L.g.cstride
@@ -520,6 +566,28 @@ static cudaError_t launch_one(const SweepLaunch &L, cudaStream_t s)
         if (grid > L.order.n_order) grid = L.order.n_order;
         if (grid <= 0) return cudaSuccess;
         kern<<<grid, NW * 32, smem, s>>>(A, L.order);
+        return cudaGetLastError();
+    }
+    if (L.ctl && !CHECK) {
+        auto kern = k_sweep_dyn<real, PATH, CPL, WY, WX>;
+        static int per_sm = -1, sms = 0;    // per instantiation: occupancy is fixed
+        if (per_sm < 0) {
+            if (smem > 48 * 1024) {
+                cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     (int)smem);
+                if (e != cudaSuccess) return e;
+            }
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NW * 32, smem);
+            if (e != cudaSuccess) return e;
+            per_sm = std::max(1, per_sm);
+        }
+        int grid = per_sm * sms;
+        if (grid > L.n_list) grid = L.n_list;     // n_list: upper bound of the count
+        if (grid <= 0) return cudaSuccess;
+        kern<<<grid, NW * 32, smem, s>>>(A);
         return cudaGetLastError();
     }
     auto kern = k_sweep<real, PATH, CPL, WY, WX, CHECK>;
@@ -572,11 +640,13 @@ cudaError_t launch_sweep(const SweepLaunch &L, cudaStream_t s)
 
 // ------------------------------------------------------------------ tile bookkeeping
 __global__ void k_tile_init(DProblem P, TileGeom g, const double *uhat, const int16_t *labels,
-                            TileState T)
+                            TileState T, double coh_thr)
 {
     __shared__ int s_free;
     __shared__ unsigned long long s_min;
     __shared__ int s_lab[4];
+    __shared__ double s_dx, s_dy;
+    __shared__ int s_sx[2], s_sy[2];     // u_hat differences by sign (x pairs, y pairs)
     const int t = blockIdx.x;
     const int i0 = (t % g.tiles_x) * g.TW, j0 = (t / g.tiles_x) * g.TH;
     const int n = P.n;
@@ -584,10 +654,14 @@ __global__ void k_tile_init(DProblem P, TileGeom g, const double *uhat, const in
         s_free = 0;
         s_min = 0xffffffffffffffffull;
         for (int k = 0; k < 4; ++k) s_lab[k] = -1;
+        s_dx = 0.0;
+        s_dy = 0.0;
+        s_sx[0] = s_sx[1] = s_sy[0] = s_sy[1] = 0;
     }
     __syncthreads();
     int cnt = 0;
-    double mn = INFINITY;
+    double mn = INFINITY, dx = 0.0, dy = 0.0;
+    int sx[2] = {0, 0}, sy[2] = {0, 0};
     for (int e = threadIdx.x; e < g.TW * g.TH; e += blockDim.x) {
         const int ly = e / g.TW, lx = e - ly * g.TW;
         const int gi = i0 + lx, gj = j0 + ly;
@@ -595,7 +669,21 @@ __global__ void k_tile_init(DProblem P, TileGeom g, const double *uhat, const in
         const int64_t k = (int64_t)gj * n + gi;
         if (P.kind[k] != 0) continue;
         ++cnt;
-        if (uhat) mn = fmin(mn, uhat[k]);
+        if (uhat) {
+            mn = fmin(mn, uhat[k]);
+            // direction in which u_hat grows = direction information travels (values depend on
+            // smaller neighbouring values): the first in-tile sweep follows it
+            if (lx + 1 < g.TW && gi + 1 < n && P.kind[k + 1] == 0) {
+                const double d = uhat[k + 1] - uhat[k];
+                dx += d;
+                sx[d < 0.0] += 1;
+            }
+            if (ly + 1 < g.TH && gj + 1 < n && P.kind[k + n] == 0) {
+                const double d = uhat[k + n] - uhat[k];
+                dy += d;
+                sy[d < 0.0] += 1;
+            }
+        }
         if (labels) {
             const int lab = labels[k];
             if (lab >= 0) {
@@ -607,6 +695,14 @@ __global__ void k_tile_init(DProblem P, TileGeom g, const double *uhat, const in
         }
     }
     atomicAdd(&s_free, cnt);
+    if (uhat) {
+        atomicAdd(&s_dx, dx);
+        atomicAdd(&s_dy, dy);
+        atomicAdd(&s_sx[0], sx[0]);
+        atomicAdd(&s_sx[1], sx[1]);
+        atomicAdd(&s_sy[0], sy[0]);
+        atomicAdd(&s_sy[1], sy[1]);
+    }
     if (mn < INFINITY) atomicMin(&s_min, (unsigned long long)__double_as_longlong(fmax(mn, 0.0)));
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -615,13 +711,19 @@ __global__ void k_tile_init(DProblem P, TileGeom g, const double *uhat, const in
         T.tile_res[t] = s_free > 0 ? INFINITY : 0.0;
         T.tile_chg[t] = 0.0;
         for (int k = 0; k < 4; ++k) T.tile_lab[4 * t + k] = (int16_t)s_lab[k];
+        // coherent tile: (nearly) every u_hat difference has the tile's sign in x and in y, so
+        // one sweep in that orientation carries information across the whole tile
+        const int ox = s_dx < 0.0, oy = s_dy < 0.0;
+        const int nx = s_sx[0] + s_sx[1], ny = s_sy[0] + s_sy[1];
+        const bool coh = nx > 0 && ny > 0 && s_sx[ox] >= coh_thr * nx && s_sy[oy] >= coh_thr * ny;
+        T.tile_orient[t] = (uint8_t)(ox | (oy << 1) | (coh ? 4 : 0));
     }
 }
 
 void launch_tile_init(const DProblem &P, const TileGeom &g, const double *uhat,
-                      const int16_t *labels, TileState &T, cudaStream_t s)
+                      const int16_t *labels, TileState &T, cudaStream_t s, double coh_thr)
 {
-    k_tile_init<<<g.tiles_x * g.tiles_y, 256, 0, s>>>(P, g, uhat, labels, T);
+    k_tile_init<<<g.tiles_x * g.tiles_y, 256, 0, s>>>(P, g, uhat, labels, T, coh_thr);
 }
 
 __global__ void k_set_values(DProblem P, int mode, const double *uhat, double *V)
@@ -644,8 +746,16 @@ void launch_set_values(const DProblem &P, int mode, const double *uhat, double *
 }
 
 __global__ void k_activate(TileGeom g, TileState T, int out_list, double tol, double tol_act,
-                           double thr, int round, int n_tiles, double slack)
+                           double thr, int round, int n_tiles, double slack, const RoundCtl *ctl,
+                           bool from_ctl)
 {
+    if (from_ctl) {
+        if (ctl->stop) return;
+        thr = ctl->thr;
+        round = ctl->round;
+    }
+    const int sid = ctl ? ctl->sweep_id : 0;
+    const double upw = ctl ? ctl->upw : -1.0;
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     ActCounters *C = reinterpret_cast<ActCounters *>(T.counters);
     bool take = false;
@@ -663,7 +773,12 @@ __global__ void k_activate(TileGeom g, TileState T, int out_list, double tol, do
                         const int ax = tx + dx, ay = ty + dy;
                         if ((dx | dy) == 0 || ax < 0 || ay < 0 || ax >= g.tiles_x || ay >= g.tiles_y)
                             continue;
-                        if (T.tile_chg[ay * g.tiles_x + ax] >= tol_act) { need = true; break; }
+                        const int nb = ay * g.tiles_x + ax;
+                        if (T.tile_chg[nb] >= tol_act && (!ctl || T.tile_stamp[nb] == sid) &&
+                            (upw < 0.0 || T.tile_minu[nb] <= T.tile_minu[t] + upw)) {
+                            need = true;
+                            break;
+                        }
                     }
             }
             if (need && slack >= 0.0) {
@@ -721,11 +836,67 @@ __global__ void k_activate(TileGeom g, TileState T, int out_list, double tol, do
 }
 
 void launch_activate(const TileGeom &g, TileState &T, int out_list, double tol, double tol_act,
-                     double thr, int round, int n_tiles, cudaStream_t s, double slack)
+                     double thr, int round, int n_tiles, cudaStream_t s, double slack,
+                     const RoundCtl *ctl, bool from_ctl)
 {
     k_activate<<<(n_tiles + 255) / 256, 256, 0, s>>>(g, T, out_list, tol, tol_act, thr, round,
-                                                     n_tiles, slack);
+                                                     n_tiles, slack, ctl, from_ctl);
 }
+
+// ------------------------------------------------------------------ device-driven rounds
+__global__ void k_round_begin(RoundCtl *ctl, ActCounters *c)
+{
+    if (ctl->stop) return;
+    if (ctl->since_verify >= ctl->verify_every) {   // overdue verification
+        ctl->stop = 1;
+        return;
+    }
+    c->count = 0;
+    c->fetch = 0;
+    c->free_sum = 0;
+    c->min_pending = 0xffffffffffffffffull;
+    c->max_res = 0;
+}
+
+__global__ void k_round_end(RoundCtl *ctl, const ActCounters *c)
+{
+    if (ctl->stop) return;
+    const int count = c->count;
+    if (count > 0) {
+        ctl->rounds += 1;
+        ctl->tiles += count;
+        ctl->sweep_id += 1;
+        ctl->since_verify += 1;
+        ctl->round += 1;
+        // bucket policy 0: the front advances every round, faster while the round under-fills
+        // the GPU (same latency as a full wave); policy 1: the bucket opens when it has settled
+        if (ctl->delta > 0.0 && ctl->policy == 0) {
+            const double fill = (double)ctl->resident / (double)count;
+            ctl->thr += ctl->delta * fmin(ctl->dboost, fmax(1.0, fill));
+        }
+        return;
+    }
+    const unsigned long long pb = c->min_pending;
+    const double pend = __longlong_as_double((long long)pb);
+    if (pb != 0xffffffffffffffffull && isfinite(pend)) {
+        ctl->thr = fmax(ctl->thr, pend) + (ctl->delta > 0.0 ? ctl->delta : 0.0);
+        return;
+    }
+    ctl->stop = 1;        // nothing active: the host runs the full-grid verification
+}
+
+__global__ void k_round_reset(RoundCtl *ctl, double thr)
+{
+    ctl->stop = 0;
+    ctl->thr = thr;
+    ctl->since_verify = 0;
+    ctl->sweep_id += 1;   // the verification supersedes every recorded tile change
+    ctl->round += 1;
+}
+
+void launch_round_begin(RoundCtl *ctl, ActCounters *c, cudaStream_t s) { k_round_begin<<<1, 1, 0, s>>>(ctl, c); }
+void launch_round_end(RoundCtl *ctl, const ActCounters *c, cudaStream_t s) { k_round_end<<<1, 1, 0, s>>>(ctl, c); }
+void launch_round_reset(RoundCtl *ctl, double thr, cudaStream_t s) { k_round_reset<<<1, 1, 0, s>>>(ctl, thr); }
 
 }  // namespace pdd
 

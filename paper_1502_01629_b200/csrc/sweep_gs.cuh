@@ -207,7 +207,7 @@ template <int CPL, int WY, int WX, bool CHECK>
 __device__ __forceinline__ int tile_gs4(const KP<float> &A, float *s_u, const float *s_ctrl,
                                          volatile int *s_prog, double *s_red, int pitch,
                                          int cstride, int H, int i0, int j0, float D, int k_inner,
-                                         float &res, double Vref)
+                                         float &res, double Vref, int o0, int sbase)
 {
     constexpr int NG = 16;
     const int lane = threadIdx.x & 31;
@@ -215,13 +215,14 @@ __device__ __forceinline__ int tile_gs4(const KP<float> &A, float *s_u, const fl
     const int n = A.P.n;
     const int lead = 1 + (3 + H) / 4;          // groups the previous row must be ahead
     const int sweeps = CHECK ? 1 : k_inner;
+    double first = 0.0;                        // change of the visit's first sweep
 
     for (int sw = 0; sw < sweeps; ++sw) {
         // every sweep tracks its residual: a tile that is converged w.r.t. its halo stops early
         // (early_tol > 0) instead of spending the remaining in-tile sweeps
         const bool last = true;
         res = 0.f;
-        const int orient = sw & 3;
+        const int orient = ((A.oxor >> (2 * ((sbase + sw) & 3))) & 3) ^ o0;   // o0: downstream first
         const bool xneg = orient & 1, yneg = orient & 2;
         const int base = sw * NG;              // progress counters are monotone across sweeps
         for (int k = 0; k < TH / NW; ++k) {
@@ -250,7 +251,8 @@ __device__ __forceinline__ int tile_gs4(const KP<float> &A, float *s_u, const fl
 #pragma unroll
             for (int w = 0; w < NW; ++w) m = fmax(m, s_red[w]);
             __syncthreads();                   // s_red is reused by the next sweep
-            if (m < A.early_tol) return sw + 1;   // sweeps done
+            if (sw == 0) first = m;
+            if (m < A.early_tol || m < A.early_rel * first) return sw + 1;   // sweeps done
         }
     }
     return sweeps;
