@@ -16,8 +16,9 @@ e2e        = same metric through the C ABI with HOST buffers: every step creates
              from pinned host arrays (H2D inside the timed region), runs the pipeline and copies
              V back to pinned host memory (D2H).
 roofline   = the sweep kernel (k_sweep): algorithmic fp32 flop per node-update
-             F = N_A * 2p * 4 * 2 (each of the 2p N_A bilinear reconstructions is a 4-term
-             multiply-add) times the updates of the timed region / the summed
+             F = N_A * (15 * 2p + 10) (4480 at C5; the bilinear reconstructions
+             alone, N_A 2p x 4 FMA = 2048, are reported as frac_bilinear_only) times the
+             updates of the timed region / the summed
              duration of the sweep launches (CUDA events on the launching stream); peak = FP32
              FMA rate derived from the guide's unit counts: 148 SMs x 128 lanes x 2 flop x
              1965 MHz = 74.4 TFLOP/s ("bound": "alu").
@@ -318,11 +319,20 @@ def main():
         e2e = {"value": e_nu / t_e, "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": int(hostV.numel() * hostV.element_size())}
 
-    flop_per_update = inst.n_controls * 2 * max(1, inst.p) * 4 * 2
+    # F = N_A (15 * 2p + 10) algorithmic flop per node-update (per branch: 2 FADD
+    # offset, 2 FADD frac, 3 lerps = 3 FADD + 3 FFMA, 1 accumulate, 1 Lambda0 op; per control: 2
+    # FFMA base offset, numerator and denominator FFMA, div, min); the conservative count of the
+    # bilinear reconstructions alone (N_A 2p x 4 FMA) is reported beside it
+    nbr = 2 * inst.p if inst.p > 0 else 1
+    flop_per_update = inst.n_controls * (15 * nbr + 10)
+    flop_bilinear = inst.n_controls * nbr * 4 * 2
     achieved = flop_per_update * nu / max(t_sweep, 1e-12) / 1e12
     peak = FP32_PEAK_TFLOPS if args.precision == 32 else FP64_PEAK_TFLOPS
     roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
             "frac": achieved / peak, "traffic": None,
+            "flop_basis": "SURVEY.md 8(d): F = N_A (15 * 2p + 10) per node-update",
+            "flop_per_node_update_bilinear_only": flop_bilinear,
+            "frac_bilinear_only": flop_bilinear * nu / max(t_sweep, 1e-12) / 1e12 / peak,
             "kernel": {1: "k_sweep path 1 (general stencil)",
                        2: "k_sweep path 2 (row-table stencil, one node per warp step)",
                        3: "k_sweep path 3 (row-table stencil, in-tile Gauss-Seidel, 4 nodes per step)"}

@@ -122,6 +122,60 @@ __global__ void k_coarse_sweep(DProblem P, const double *__restrict__ Vin, doubl
         atomicMax(&res_hist[sweep], (unsigned long long)__double_as_longlong(res));
 }
 
+// The same Jacobi sweep restricted to the tiles (CT x CT nodes, one CTA each) whose 3 x 3 tile
+// neighbourhood changed in the previous sweep; every other tile copies Vin -> Vout.  Exact (bit
+// for bit the result of k_coarse_sweep): a node's update reads only nodes within its stencil
+// reach (< CT cells, checked by the host), so if none of them changed since the last sweep its
+// new value is the value the last sweep wrote, i.e. Vin.  Ahead of the front (V0, stationary) and
+// behind it (converged) most tiles are skipped.  fprev / fout: per-tile "changed" flags of the
+// previous / this sweep (fprev unused at sweep 0).
+constexpr int CT = 16;
+__global__ void __launch_bounds__(CT * CT) k_coarse_sweep_tiles(
+    DProblem P, const double *__restrict__ Vin, double *__restrict__ Vout, double tol,
+    unsigned long long *res_hist, int sweep, int *sweeps_done, const uint8_t *fprev,
+    uint8_t *fout, int tiles_x)
+{
+    if (sweep > 0 && __longlong_as_double((long long)res_hist[sweep - 1]) < tol) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(sweeps_done, 1);
+    __shared__ int s_act;
+    const int n = P.n;
+    const int tx = blockIdx.x % tiles_x, ty = blockIdx.x / tiles_x;
+    const int tiles_y = (n + CT - 1) / CT;
+    if (threadIdx.x == 0) {
+        int act = sweep == 0;
+        for (int dy = -1; dy <= 1 && !act; ++dy)
+            for (int dx = -1; dx <= 1; ++dx) {
+                const int ax = tx + dx, ay = ty + dy;
+                if (ax >= 0 && ay >= 0 && ax < tiles_x && ay < tiles_y && fprev[ay * tiles_x + ax]) {
+                    act = 1;
+                    break;
+                }
+            }
+        s_act = act;
+    }
+    __syncthreads();
+    const int i = tx * CT + (int)(threadIdx.x % CT), j = ty * CT + (int)(threadIdx.x / CT);
+    double res = 0.0;
+    int changed = 0;
+    if (i < n && j < n) {
+        const int64_t k = (int64_t)j * n + i;
+        const double vin = Vin[k];
+        if (!s_act || P.kind[k] != 0) {
+            Vout[k] = vin;
+        } else {
+            const double v = canon_node_update(P, Vin, i, j);
+            Vout[k] = v;
+            res = fabs(DSUB(v, vin));
+            changed = __double_as_longlong(v) != __double_as_longlong(vin);
+        }
+    }
+    changed = __syncthreads_or(changed);
+    if (threadIdx.x == 0) fout[blockIdx.x] = (uint8_t)(changed != 0);
+    for (int o = 16; o > 0; o >>= 1) res = fmax(res, __shfl_xor_sync(0xffffffffu, res, o));
+    if ((threadIdx.x & 31) == 0 && res > 0.0)
+        atomicMax(&res_hist[sweep], (unsigned long long)__double_as_longlong(res));
+}
+
 __global__ void k_prolong(int nc, const double *__restrict__ uc, int n, int r, double *__restrict__ out)
 {
     const int64_t N = (int64_t)n * n;
@@ -269,6 +323,17 @@ void launch_coarse_sweep(const DProblem &P, const double *Vin, double *Vout, dou
     k_coarse_sweep<<<grid_for(N, 128), 128, 0, s>>>(P, Vin, Vout, tol, res_hist, sweep,
                                                      sweeps_done);
 }
+
+void launch_coarse_sweep_tiles(const DProblem &P, const double *Vin, double *Vout, double tol,
+                               unsigned long long *res_hist, int sweep, int *sweeps_done,
+                               const uint8_t *fprev, uint8_t *fout, cudaStream_t s)
+{
+    const int tx = (P.n + CT - 1) / CT;
+    k_coarse_sweep_tiles<<<tx * tx, CT * CT, 0, s>>>(P, Vin, Vout, tol, res_hist, sweep,
+                                                     sweeps_done, fprev, fout, tx);
+}
+
+int coarse_tile() { return CT; }
 
 void launch_prolong(int nc, const double *uc, int n, double *out, cudaStream_t s)
 {

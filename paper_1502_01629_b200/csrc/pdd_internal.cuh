@@ -58,6 +58,11 @@ void launch_init_values(const DProblem &P, double *V, cudaStream_t s);
 void launch_coarse_sweep(const DProblem &P, const double *Vin, double *Vout, double tol,
                          unsigned long long *res_hist, int sweep, int *sweeps_done,
                          cudaStream_t s);
+// active-tile form of the same sweep (bit-identical; fprev/fout: per-tile change flags)
+void launch_coarse_sweep_tiles(const DProblem &P, const double *Vin, double *Vout, double tol,
+                               unsigned long long *res_hist, int sweep, int *sweeps_done,
+                               const uint8_t *fprev, uint8_t *fout, cudaStream_t s);
+int coarse_tile();
 void launch_prolong(int nc, const double *uc, int n, double *out, cudaStream_t s);
 void launch_synthesize(const DProblem &P, const double *uhat, uint8_t *astar, cudaStream_t s);
 void launch_successor(const DProblem &P, double M, const uint8_t *astar, int32_t *succ,

@@ -110,6 +110,8 @@ struct pdd_ctx {
     int32_t *succ0 = nullptr, *succA = nullptr, *succB = nullptr;
     float *f32buf = nullptr;
     unsigned long long *res_hist = nullptr;
+    uint8_t *cflag = nullptr;   // coarse active-tile change flags, 2 x tiles
+    bool coarse_tiled = false;  // coarse reach < tile: active-tile sweeps
     int *dev_int = nullptr;     // [0] sweeps_done, [1] jump changed flag
     void *rowtab = nullptr;
     size_t rowtab_bytes = 0;
@@ -267,6 +269,8 @@ static size_t layout(pdd_ctx *c, void *ws, const pdd_problem *f, const pdd_probl
     double *uc0 = cp ? cv.take<double>((size_t)cp->n * cp->n) : nullptr;
     double *uc1 = cp ? cv.take<double>((size_t)cp->n * cp->n) : nullptr;
     unsigned long long *rh = cp ? cv.take<unsigned long long>(kMaxCoarseSweeps) : nullptr;
+    const int ctn = cp ? (cp->n + coarse_tile() - 1) / coarse_tile() : 0;
+    uint8_t *cflag = cp ? cv.take<uint8_t>(2 * (size_t)ctn * ctn) : nullptr;
     uint8_t *astar = cv.take<uint8_t>(N);
     int16_t *labels = cv.take<int16_t>(N);
     int32_t *s0 = cp ? cv.take<int32_t>(N) : nullptr;
@@ -309,6 +313,7 @@ static size_t layout(pdd_ctx *c, void *ws, const pdd_problem *f, const pdd_probl
         c->uc[0] = uc0;
         c->uc[1] = uc1;
         c->res_hist = rh;
+        c->cflag = cflag;
         c->astar = astar;
         c->labels = labels;
         c->succ0 = s0;
@@ -390,6 +395,9 @@ pdd_status pdd_create(const pdd_problem *fine, const pdd_problem *coarse, int32_
     ctx->fine = *fine;
     ctx->has_coarse = coarse != nullptr;
     if (coarse) ctx->coarse = *coarse;
+    // active-tile coarse sweeps need the stencil reach (+ the bilinear corner) inside one tile
+    // (computed here: the host arrays of the problem are valid only during this call)
+    ctx->coarse_tiled = coarse && reach_cells(coarse) + 2.0 < (double)coarse_tile();
     // aligned base
     char *base = (char *)workspace;
     const size_t mis = (size_t)((uintptr_t)base % kAlign);
@@ -457,11 +465,20 @@ pdd_status pdd_coarse_solve(pdd_ctx *ctx, double tol_c, int64_t max_sweeps, pdd_
     int done = 0;
     bool converged = false;
     int64_t batch = 8;
+    const bool tiled = ctx->coarse_tiled && !std::getenv("PDD_COARSE_FULL");   // env: A/B only
     while (issued < max_sweeps) {
         const int64_t b = std::min<int64_t>(batch, max_sweeps - issued);
-        for (int64_t q = 0; q < b; ++q, ++issued)
-            launch_coarse_sweep(Pc, ctx->uc[issued & 1], ctx->uc[(issued + 1) & 1], tol_c,
-                                ctx->res_hist, (int)issued, ctx->dev_int, s);
+        const size_t ctn = (size_t)((Pc.n + coarse_tile() - 1) / coarse_tile());
+        for (int64_t q = 0; q < b; ++q, ++issued) {
+            if (tiled)
+                launch_coarse_sweep_tiles(Pc, ctx->uc[issued & 1], ctx->uc[(issued + 1) & 1], tol_c,
+                                          ctx->res_hist, (int)issued, ctx->dev_int,
+                                          ctx->cflag + ((issued + 1) & 1) * ctn * ctn,
+                                          ctx->cflag + (issued & 1) * ctn * ctn, s);
+            else
+                launch_coarse_sweep(Pc, ctx->uc[issued & 1], ctx->uc[(issued + 1) & 1], tol_c,
+                                    ctx->res_hist, (int)issued, ctx->dev_int, s);
+        }
         ctx->launches += b;
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(ctx->h_int, ctx->dev_int, sizeof(int), cudaMemcpyDeviceToHost, s));

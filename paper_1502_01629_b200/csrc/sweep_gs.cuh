@@ -160,8 +160,7 @@ __device__ __forceinline__ void row_gs4(const KP<float> &A, float *s_u, const fl
                 for (int d = 1; d <= s; ++d) a = fmaf(wc[c][d - 1], dlt[xneg ? gg + d : gg - d], a);
                 m = fminf(m, a);
             }
-            // (redux.sync.min is lowered to a shuffle tree on sm_100a: measured, no gain)
-            m = warp_min(m);
+            m = warp_min(m);     // fp32: one integer REDUX (warp_min<float>)
             const bool sk = (sk4 >> gg) & 1u;
             nv[gg] = m;
             dlt[gg] = (sk || CHECK) ? 0.f : m - old[gg];
