@@ -16,8 +16,9 @@
  *
  * The scheme (P:366-375 with the self-dependency removal P:433-491, discounted as in
  * BASELINE.json, R1-R3): for a free node x_i,
- *   V(x_i) = min_k ( h l(x_i) + beta R'_k ) / ( 1 - beta Lambda0_k ),  beta = 1/(1 + lambda h),
- * foot points x_i + h f(x_i, a_k) +- sqrt(h p) sigma_j(x_i) (j < p; one foot point when p = 0),
+ *   V(x_i) = min_k ( h l(x_i, a_k) + beta R'_k ) / ( 1 - beta Lambda0_k ),  beta = 1/(1 + lambda h),
+ * foot points x_i + h f(x_i, a_k) +- sqrt(h p) sigma_j(x_i, a_k) (j < p; one foot point when
+ * p = 0; sigma_j depends on a_k only with sigma_mode 1),
  * f(x, a) = c(x) a + d(x); R'_k / Lambda0_k = branch-averaged bilinear weight of the corners
  * other than x_i / of x_i itself; feet are clamped to the box (R5).  Target nodes hold V = 0,
  * obstacle nodes V = 1/lambda (R8).
@@ -48,7 +49,8 @@ extern "C" {
 typedef enum {
     PDD_OK = 0,
     PDD_E_INVALID = 1,    /* bad argument: n < 3, hi <= lo, N_A outside 1..128, p outside 0..2,
-                             lambda <= 0, l <= 0, sizes that do not nest, NULL pointers */
+                             lambda < 0, obstacles with lambda = 0, l <= 0, sigma_mode 1 with
+                             p != 1, sizes that do not nest, NULL pointers */
     PDD_E_NOCONVERGE = 2, /* max rounds / sweeps reached; values stay fetchable */
     PDD_E_IO = 3,         /* reserved */
     PDD_E_CUDA = 4,       /* a CUDA call failed; see pdd_last_error */
@@ -77,7 +79,9 @@ typedef struct {
     double lo, hi;          /* square box [lo, hi]^2                                        */
     double dx;              /* (hi - lo)/(n - 1), given explicitly (both sides use this value) */
     double h;               /* time step of the SL scheme (R13: h = dx in BASELINE configs) */
-    double lambda;          /* discount > 0; beta = 1/(1 + lambda h)                        */
+    double lambda;          /* discount >= 0; beta = 1/(1 + lambda h).  lambda = 0: the paper's
+                               exit-time problems (g = 0 on target nodes, e.g. the
+                               boundary ring); V starts at 1e6 (R11), no obstacles */
     int32_t n_controls;     /* N_A, 1..128                                      */
     const double *controls; /* 2*N_A values (a1, a2) per control                            */
     pdd_coef speed;         /* c(x)                                                         */
@@ -89,6 +93,12 @@ typedef struct {
     const uint8_t *kind;    /* n*n: 0 free, 1 target (V = 0), 2 obstacle (V = 1/lambda)     */
     const int16_t *sector;  /* n*n: Gamma_p id of target nodes (R17), ignored elsewhere; may be
                                NULL on the coarse grid or when no patches are built           */
+    /* General nonlinear terms (readings R32, R33):                     */
+    int32_t sigma_mode;     /* 0: noise columns sigma_j(x) as above; 1: ONE column along the
+                               control, sigma(x, a) = s(x) a with s = sigma[0][0] (p must be 1;
+                               the paper's sigma_3(x,a) = d_eps(x) a)                         */
+    const double *cost_ctrl;/* N_A values m(a_k) or NULL: running cost l(x, a_k) = l(x) + m(a_k)
+                               (the paper's l_3); l(x) + min m must stay > 0                  */
 } pdd_problem;
 
 typedef struct pdd_ctx pdd_ctx;

@@ -52,7 +52,8 @@ class _Problem(C.Structure):
                 ("lam", C.c_double), ("na", C.c_int32), ("ctrl", C.POINTER(C.c_double)),
                 ("speed", _Coef), ("drift", _Coef * 2), ("p", C.c_int32),
                 ("sigma", (_Coef * 2) * 2), ("cost", _Coef), ("diffusion_scale", C.c_int32),
-                ("kind", C.POINTER(C.c_uint8))]
+                ("kind", C.POINTER(C.c_uint8)), ("sigma_mode", C.c_int32),
+                ("cost_ctrl", C.POINTER(C.c_double))]
 
 
 _lib = None
@@ -124,6 +125,12 @@ class Problem:
         kind = np.ascontiguousarray(inst.kind, dtype=np.uint8)
         self._keep.append(kind)
         s.kind = _ptr(kind, C.c_uint8)
+        s.sigma_mode = int(getattr(inst, "sigma_mode", 0))
+        cc = getattr(inst, "cost_ctrl", None)
+        if cc is not None:
+            cc = np.ascontiguousarray(cc, dtype=np.float64)
+            self._keep.append(cc)
+            s.cost_ctrl = _ptr(cc, C.c_double)
         self.s = s
 
     def _coef(self, c):

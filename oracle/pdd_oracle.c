@@ -54,7 +54,20 @@ typedef struct {
     orc_coef cost;       /* l(x) */
     int32_t diffusion_scale; /* 0: sqrt(h p), 1: sqrt(h) */
     const uint8_t *kind; /* 0 free, 1 target (V = 0), 2 obstacle (V = 1/lambda) */
+    /* general nonlinear terms (readings R32/R33):
+     * sigma_mode 1: one noise column along the control, sigma(x,a) = s(x) a with s = sigma[0][0]
+     *               (the paper's sigma_3(x,a) = d_eps(x) a; p must be 1);
+     * cost_ctrl:    per-control additive cost m(a_k), l(x,a) = l(x) + m(a) (the paper's l_3),
+     *               NULL = 0. */
+    int32_t sigma_mode;
+    const double *cost_ctrl;
 } orc_problem;
+
+/* running cost l(x_i, a_k) (R33) */
+static double cost_of(const orc_problem *P, double lx, int a)
+{
+    return P->cost_ctrl ? lx + P->cost_ctrl[a] : lx;
+}
 
 static double coef_at(const orc_coef *c, int i, int j, int n)
 {
@@ -104,6 +117,12 @@ void orc_init_v0(const orc_problem *P, double *V)
             double l = coef_at(&P->cost, i, j, n);
             if (l > lmax) lmax = l;
         }
+    if (P->cost_ctrl) {
+        double mmax = -INFINITY;
+        for (int a = 0; a < P->na; ++a)
+            if (P->cost_ctrl[a] > mmax) mmax = P->cost_ctrl[a];
+        lmax = lmax + mmax;
+    }
     double beta = orc_beta(P);
     double v0 = P->lambda > 0.0 ? (P->h * lmax) / (1.0 - beta) : 1e6;
     for (int64_t k = 0; k < (int64_t)n * n; ++k)
@@ -172,9 +191,15 @@ double orc_node_update(const orc_problem *P, const double *V, int i, int j, int 
         off[k][0] = sc * coef_at(&P->sigma[k][0], i, j, n);
         off[k][1] = sc * coef_at(&P->sigma[k][1], i, j, n);
     }
+    const double sa = P->sigma_mode == 1 ? sc * coef_at(&P->sigma[0][0], i, j, n) : 0.0;
     double best = INFINITY;
     int32_t arg = -1;
     for (int a = 0; a < P->na; ++a) {
+        if (P->sigma_mode == 1) {   /* sigma(x,a) = s(x) a: the column follows the control */
+            off[0][0] = sa * P->ctrl[2 * a];
+            off[0][1] = sa * P->ctrl[2 * a + 1];
+        }
+        const double la = cost_of(P, l, a);
         const double f1 = c * P->ctrl[2 * a] + d1;
         const double f2 = c * P->ctrl[2 * a + 1] + d2;
         const double bx = q * f1;
@@ -200,8 +225,8 @@ double orc_node_update(const orc_problem *P, const double *V, int i, int j, int 
             rp = rp + w * sum;
         }
         double v;
-        if (scheme == 0) v = (P->h * l + beta * rp) / (1.0 - beta * lam0);
-        else v = P->h * l + beta * (rp + lam0 * V[self]);
+        if (scheme == 0) v = (P->h * la + beta * rp) / (1.0 - beta * lam0);
+        else v = P->h * la + beta * (rp + lam0 * V[self]);
         if (v < best) { best = v; arg = a; }
     }
     if (argmin_out) *argmin_out = arg;
@@ -231,8 +256,13 @@ void orc_node_lambdas(const orc_problem *P, const double *V, int i, int j, doubl
             double gx = (double)i + bx, gy = (double)j + by;
             if (P->p > 0) {
                 const int k = b >> 1;
-                const double ox = sc * coef_at(&P->sigma[k][0], i, j, n);
-                const double oy = sc * coef_at(&P->sigma[k][1], i, j, n);
+                double ox = sc * coef_at(&P->sigma[k][0], i, j, n);
+                double oy = sc * coef_at(&P->sigma[k][1], i, j, n);
+                if (P->sigma_mode == 1) {
+                    const double sa = sc * coef_at(&P->sigma[0][0], i, j, n);
+                    ox = sa * P->ctrl[2 * a];
+                    oy = sa * P->ctrl[2 * a + 1];
+                }
                 if ((b & 1) == 0) { gx = gx + ox; gy = gy + oy; }
                 else              { gx = gx - ox; gy = gy - oy; }
             }
@@ -406,7 +436,7 @@ static int32_t synth_one(const orc_problem *P, const uhat_src *U, int i, int j)
         s = s + wg[1] * uhat_at(U, n, cr[1]);
         s = s + wg[2] * uhat_at(U, n, cr[2]);
         s = s + wg[3] * uhat_at(U, n, cr[3]);
-        const double v = P->h * l + beta * s;
+        const double v = P->h * cost_of(P, l, a) + beta * s;
         if (v < best) { best = v; arg = a; }
     }
     return arg;

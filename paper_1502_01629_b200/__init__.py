@@ -75,6 +75,11 @@ class _ProblemView:
         if with_sector and sector is not None:
             sec = self._arr(np.asarray(sector).astype(np.int16).reshape(-1), pin)
             s.sector = sec.ctypes.data_as(C.POINTER(C.c_int16))
+        s.sigma_mode = int(getattr(inst, "sigma_mode", 0))
+        cc = getattr(inst, "cost_ctrl", None)
+        if cc is not None:
+            cca = self._arr(np.asarray(cc, dtype=np.float64).reshape(-1), pin)
+            s.cost_ctrl = cca.ctypes.data_as(C.POINTER(C.c_double))
         self.s = s
 
     def _arr(self, a: np.ndarray, pin: bool):

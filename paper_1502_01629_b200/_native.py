@@ -35,7 +35,8 @@ class pdd_problem(C.Structure):
                 ("controls", C.POINTER(C.c_double)), ("speed", pdd_coef),
                 ("drift", pdd_coef * 2), ("p", C.c_int32), ("sigma", (pdd_coef * 2) * 2),
                 ("cost", pdd_coef), ("diffusion_scale", C.c_int32),
-                ("kind", C.POINTER(C.c_uint8)), ("sector", C.POINTER(C.c_int16))]
+                ("kind", C.POINTER(C.c_uint8)), ("sector", C.POINTER(C.c_int16)),
+                ("sigma_mode", C.c_int32), ("cost_ctrl", C.POINTER(C.c_double))]
 
 
 class pdd_solve_opts(C.Structure):

@@ -75,9 +75,9 @@ __device__ double canon_node_update(const DProblem &P, const double *V, int i, i
     const double d1 = coef_at(P.drift[0], i, j, n);
     const double d2 = coef_at(P.drift[1], i, j, n);
     const double l = coef_at(P.cost, i, j, n);
-    const double hl = DMUL(P.h, l);
     double best = INFINITY;
     for (int a = 0; a < P.na; ++a) {
+        const double hl = DMUL(P.h, P.cost_ctrl ? DADD(l, P.cost_ctrl[a]) : l);   // R33
         const double f1 = DADD(DMUL(c, P.ctrl[2 * a]), d1);
         const double f2 = DADD(DMUL(c, P.ctrl[2 * a + 1]), d2);
         const double gx = DADD((double)i, DMUL(P.q, f1));
@@ -209,10 +209,11 @@ __global__ void k_synthesize(DProblem P, const double *__restrict__ uhat, uint8_
         const double c = coef_at(P.speed, i, j, n);
         const double d1 = coef_at(P.drift[0], i, j, n);
         const double d2 = coef_at(P.drift[1], i, j, n);
-        const double hl = DMUL(P.h, coef_at(P.cost, i, j, n));
+        const double lx = coef_at(P.cost, i, j, n);
         double best = INFINITY;
         int arg = -1;
         for (int a = 0; a < P.na; ++a) {
+            const double hl = DMUL(P.h, P.cost_ctrl ? DADD(lx, P.cost_ctrl[a]) : lx);   // R33
             const double f1 = DADD(DMUL(c, P.ctrl[2 * a]), d1);
             const double f2 = DADD(DMUL(c, P.ctrl[2 * a + 1]), d2);
             const double gx = DADD((double)i, DMUL(P.q, f1));

@@ -39,7 +39,16 @@ struct DProblem {
     DCoef speed, drift[2], sigma[2][2], cost;
     int p;
     const uint8_t *kind;
+    int sigma_mode;          // 1: sigma(x, a) = s(x) a, s = sigma[0][0], p = 1 (R32)
+    const double *cost_ctrl; // N_A additive costs m(a_k) or NULL (R33)
+    double lmax_x;           // max_x l(x) (lmax above includes max m, for V0 and the front step)
 };
+
+// running cost l(x_i, a_k) = l(x_i) + m(a_k) (R33), canonical order of the oracle's cost_of
+__host__ __device__ __forceinline__ double cost_at(const DProblem &P, double lx, int a)
+{
+    return P.cost_ctrl ? lx + P.cost_ctrl[a] : lx;
+}
 
 // Row-table stencil entry (row-uniform coefficients): for one grid row j and one control k,
 // the branch-merged compact stencil of an interior node relative to the node:
@@ -210,6 +219,8 @@ cudaError_t launch_sweep(const SweepLaunch &L, cudaStream_t s);
 bool rowtab_supported(int WY, int WX, int cpl);
 int rowtab_tw(int WY, int WX);
 int sweep_tile_rows();
+// compile-time shared-memory geometry of the path-3 kernel (rows pitch, copy stride, max halo)
+void p3_geometry(int &pitch, int &cstride, int &hmax);
 // Build the row-stencil table on the device; false if no supported window fits.
 bool rowtab_build_device(const DProblem &P, int napad, int H, int precision, int *scratch,
                          void *tab, size_t tab_bytes, int &WY, int &WX, int &oxmin, int &oxmax,

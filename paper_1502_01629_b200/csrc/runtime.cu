@@ -62,6 +62,7 @@ struct ProbBufs {
     double *coef[8] = {nullptr};   // speed, drift0, drift1, s00, s01, s10, s11, cost
     uint8_t *kind = nullptr;
     int16_t *sector = nullptr;
+    double *cost_ctrl = nullptr;   // N_A (or null)
 };
 
 const pdd_coef *coef_ptr(const pdd_problem *p, int k)
@@ -88,6 +89,7 @@ void carve_problem(Carver &cv, const pdd_problem *p, ProbBufs &b, bool with_sect
     }
     b.kind = cv.take<uint8_t>((size_t)n * n);
     b.sector = with_sector ? cv.take<int16_t>((size_t)n * n) : nullptr;
+    b.cost_ctrl = p->cost_ctrl ? cv.take<double>((size_t)p->n_controls) : nullptr;
 }
 
 int na_pad_of(int na) { return na <= 32 ? 32 : (na <= 64 ? 64 : 0); }
@@ -167,7 +169,11 @@ static pdd_status validate(const pdd_problem *p, const char *what)
     if (!(p->hi > p->lo)) return fail(nullptr, PDD_E_INVALID, "%s: hi <= lo", what);
     if (!(p->dx > 0.0) || !(p->h > 0.0))
         return fail(nullptr, PDD_E_INVALID, "%s: dx and h must be > 0", what);
-    if (!(p->lambda > 0.0)) return fail(nullptr, PDD_E_INVALID, "%s: lambda must be > 0", what);
+    if (!(p->lambda >= 0.0)) return fail(nullptr, PDD_E_INVALID, "%s: lambda must be >= 0", what);
+    if (p->sigma_mode != 0 && p->sigma_mode != 1)
+        return fail(nullptr, PDD_E_INVALID, "%s: sigma_mode must be 0 or 1", what);
+    if (p->sigma_mode == 1 && p->p != 1)
+        return fail(nullptr, PDD_E_INVALID, "%s: sigma_mode 1 (sigma(x,a) = s(x) a) needs p = 1", what);
     if (p->n_controls < 1 || p->n_controls > 128)
         return fail(nullptr, PDD_E_INVALID, "%s: N_A = %d outside 1..128", what, p->n_controls);
     if (!p->controls) return fail(nullptr, PDD_E_INVALID, "%s: controls is NULL", what);
@@ -179,15 +185,29 @@ static pdd_status validate(const pdd_problem *p, const char *what)
         if (c->kind != PDD_COEF_CONST && !c->data)
             return fail(nullptr, PDD_E_INVALID, "%s: coefficient %d has NULL data", what, k);
     }
-    // l > 0
+    // l(x, a) = l(x) + m(a) > 0 (R33)
+    double mmin = 0.0;
+    if (p->cost_ctrl) {
+        mmin = INFINITY;
+        for (int k = 0; k < p->n_controls; ++k) {
+            if (!std::isfinite(p->cost_ctrl[k]))
+                return fail(nullptr, PDD_E_INVALID, "%s: cost_ctrl must be finite", what);
+            mmin = std::min(mmin, p->cost_ctrl[k]);
+        }
+    }
     const pdd_coef &l = p->cost;
     const size_t cnt = coef_count(l, p->n);
     if (cnt == 0) {
-        if (!(l.value > 0.0)) return fail(nullptr, PDD_E_INVALID, "%s: running cost must be > 0", what);
+        if (!(l.value + mmin > 0.0)) return fail(nullptr, PDD_E_INVALID, "%s: running cost must be > 0", what);
     } else {
         for (size_t i = 0; i < cnt; ++i)
-            if (!(l.data[i] > 0.0)) return fail(nullptr, PDD_E_INVALID, "%s: running cost must be > 0", what);
+            if (!(l.data[i] + mmin > 0.0)) return fail(nullptr, PDD_E_INVALID, "%s: running cost must be > 0", what);
     }
+    // exit problems (lambda = 0): the obstacle value 1/lambda does not exist (R8)
+    if (p->lambda == 0.0)
+        for (size_t k = 0; k < (size_t)p->n * p->n; ++k)
+            if (p->kind[k] == 2)
+                return fail(nullptr, PDD_E_INVALID, "%s: obstacles need lambda > 0", what);
     return PDD_OK;
 }
 
@@ -211,9 +231,12 @@ static double reach_cells(const pdd_problem *p)
     double smax = 0.0;
     if (p->p > 0) {
         const double sc = p->diffusion_scale == 0 ? std::sqrt(p->h * p->p) : std::sqrt(p->h);
-        for (int k = 0; k < p->p; ++k)
-            smax = std::max(smax, sc * std::hypot(coef_max_abs(p->sigma[k][0], p->n),
-                                                  coef_max_abs(p->sigma[k][1], p->n)));
+        if (p->sigma_mode == 1)
+            smax = sc * coef_max_abs(p->sigma[0][0], p->n) * amax;
+        else
+            for (int k = 0; k < p->p; ++k)
+                smax = std::max(smax, sc * std::hypot(coef_max_abs(p->sigma[k][0], p->n),
+                                                      coef_max_abs(p->sigma[k][1], p->n)));
     }
     return (p->h * fmax + smax) / p->dx;
 }
@@ -240,8 +263,18 @@ static void make_dproblem(const pdd_problem *p, ProbBufs &b)
     const size_t cl = coef_count(p->cost, p->n);
     if (!cl) lmax = p->cost.value;
     else for (size_t i = 0; i < cl; ++i) lmax = std::max(lmax, p->cost.data[i]);
+    d.lmax_x = lmax;
+    if (p->cost_ctrl) {
+        double mmax = -INFINITY;
+        for (int k = 0; k < p->n_controls; ++k) mmax = std::max(mmax, p->cost_ctrl[k]);
+        lmax = lmax + mmax;
+    }
     d.lmax = lmax;
-    d.v0 = (p->h * lmax) / (1.0 - d.beta);     // canonical: same expression as the oracle
+    // canonical: same expressions as the oracle; exit problems (lambda = 0) start at the "very
+    // big value" of P:818-819 (R11)
+    d.v0 = p->lambda > 0.0 ? (p->h * lmax) / (1.0 - d.beta) : 1e6;
+    d.sigma_mode = p->sigma_mode;
+    d.cost_ctrl = b.cost_ctrl;
     d.na = p->n_controls;
     d.ctrl = b.ctrl;
     DCoef *dc[8] = {&d.speed, &d.drift[0], &d.drift[1], &d.sigma[0][0], &d.sigma[0][1],
@@ -362,6 +395,9 @@ static pdd_status copy_problem(pdd_ctx *ctx, const pdd_problem *p, ProbBufs &b, 
                                     cudaMemcpyHostToDevice, ctx->stream));
     }
     CK(cudaMemcpyAsync(b.kind, p->kind, (size_t)n * n, cudaMemcpyHostToDevice, ctx->stream));
+    if (p->cost_ctrl)
+        CK(cudaMemcpyAsync(b.cost_ctrl, p->cost_ctrl, sizeof(double) * p->n_controls,
+                           cudaMemcpyHostToDevice, ctx->stream));
     if (sector && b.sector)
         CK(cudaMemcpyAsync(b.sector, p->sector, sizeof(int16_t) * n * n, cudaMemcpyHostToDevice,
                            ctx->stream));
@@ -623,7 +659,9 @@ static pdd_status prepare(pdd_ctx *ctx, int kernel_req)
         return fail(ctx, PDD_E_INVALID, "row-table stencil requested but the problem is not row-uniform");
     // fp32 row-table problems use the 4-nodes-per-step kernel (path 3) unless kernel 3 asks for
     // the one-node-per-step variant (path 2, kept for A/B measurements and fp64)
-    const bool g4 = path == 2 && ctx->precision == 32 && kernel_req != 3;
+    int p3_pitch = 0, p3_cstride = 0, p3_hmax = 0;
+    p3_geometry(p3_pitch, p3_cstride, p3_hmax);
+    const bool g4 = path == 2 && ctx->precision == 32 && kernel_req != 3 && H <= p3_hmax;
     ctx->path = g4 ? 3 : path;
     ctx->WY = WY;
     ctx->WX = WX;
@@ -638,12 +676,12 @@ static pdd_status prepare(pdd_ctx *ctx, int kernel_req)
     const int banks = ctx->precision == 32 ? 32 : 16;
     int pitch = g.TW + 2 * H;
     if (g4) {
-        // 16-byte rows; consecutive window rows land in different 16-byte bank groups
-        while (pitch % 4 != 0 || ((pitch / 4) & 1) == 0) ++pitch;
-        const int rows = g.TH + 2 * H;
-        int cs = rows * pitch + 4;
-        while (cs % 4 != 0 || ((cs / 4) % 8) != 2) ++cs;   // spread the 4 copies over bank groups
-        g.cstride = cs;
+        // the kernel's compile-time geometry: 16-byte rows, consecutive window rows in different
+        // 16-byte bank groups, the 4 shifted copies spread over bank groups
+        pitch = p3_pitch;
+        g.cstride = p3_cstride;
+        if (pitch < g.TW + 2 * H || p3_cstride < (g.TH + 2 * H) * pitch + 4)
+            return fail(ctx, PDD_E_STENCIL, "path-3 shared-memory geometry too small for halo %d", H);
     } else {
         while (pitch % banks != mod % banks) ++pitch;
         g.cstride = 0;

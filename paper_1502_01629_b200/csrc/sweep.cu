@@ -60,6 +60,7 @@ template <int WY, int WX>
 struct TWOf { static constexpr int value = WX * (64 / WX); };   // multiple of WX, <= 64
 
 int rowtab_tw(int WY, int WX) { (void)WY; return WX * (64 / WX); }
+void p3_geometry(int &pitch, int &cstride, int &hmax);
 int sweep_tile_rows() { return TH; }
 
 bool rowtab_supported(int WY, int WX, int cpl)
@@ -170,10 +171,18 @@ __device__ __forceinline__ real general_node(const DProblem &P, const real *__re
     (void)beta;
     // a running-cost field needs D = h l(x_i) - (1 - beta) V_ref per node (fp64 then rounded)
     if (P.cost.kind != 0) D = (real)(P.h * coef_at(P.cost, gi, gj, n) - (1.0 - P.beta) * Vref);
+    // sigma(x, a) = s(x) a (sigma_mode 1, R32): the single noise column follows the control
+    const real sa = P.sigma_mode == 1 ? (real)(P.sc * coef_at(P.sigma[0][0], gi, gj, n)) : (real)0;
     real best = rinf<real>();
     for (int k = lane; k < P.na; k += 32) {
         const real bx = q * (c * s_ctrl[2 * k] + d1);
         const real by = q * (c * s_ctrl[2 * k + 1] + d2);
+        if (P.sigma_mode == 1) {
+            off[0][0] = sa * s_ctrl[2 * k];
+            off[0][1] = sa * s_ctrl[2 * k + 1];
+        }
+        // l(x, a_k) = l(x) + m(a_k) (R33)
+        const real Dk = P.cost_ctrl ? D + (real)(P.h * __ldg(P.cost_ctrl + k)) : D;
         real R = 0, L0 = 0;
         for (int b = 0; b < nb; ++b) {
             real xr = bx, yr = by;
@@ -196,7 +205,7 @@ __device__ __forceinline__ real general_node(const DProblem &P, const real *__re
             R += val - ws * uself;
             L0 += ws;
         }
-        const real v = (D + bw * R) / ((real)1 - bw * L0);
+        const real v = (Dk + bw * R) / ((real)1 - bw * L0);
         best = rmin(best, v);
     }
     return warp_min(best);
@@ -279,7 +288,8 @@ __device__ __forceinline__ void row_table(const KP<real> &A, real *s_u, const re
     for (int c = 0; c < CPL; ++c) {
         const int k = lane + 32 * c;
         const RowEntry<real, WY, WX> &e = tab[k];
-        c0[c] = k < A.P.na ? D * e.E : rinf<real>();
+        const real Dk = (k < A.P.na && A.P.cost_ctrl) ? D + (real)(A.P.h * A.P.cost_ctrl[k]) : D;   // R33
+        c0[c] = k < A.P.na ? Dk * e.E : rinf<real>();
 #pragma unroll
         for (int m = 0; m < WY * WX; ++m) Wt[c][m] = e.W[m];
         base[c] = (ly + H + e.oy) * pitch + H + e.ox;
@@ -332,6 +342,8 @@ __device__ __forceinline__ void row_table(const KP<real> &A, real *s_u, const re
 
 #include "sweep_gs.cuh"
 
+constexpr bool kRawMinRef = PDD_RAWMIN != 0;   // fp32 path 3: V_ref = staged min (sweep_gs.cuh)
+
 // ------------------------------------------------------------------ one tile visit
 // Stage tile + halo, relax k_inner times, write back.  Global V is read with ld.global.cg (L2):
 // in the ordered (persistent) schedule other CTAs update V during the launch.
@@ -349,26 +361,64 @@ __device__ __forceinline__ void sweep_tile(const KP<real> &A, int t, unsigned ch
     const int n = A.P.n;
     const int i0 = (t % A.g.tiles_x) * TW;
     const int j0 = (t / A.g.tiles_x) * TH;
-    const int ci = min(i0 + TW / 2, n - 1), cj = min(j0 + TH / 2, n - 1);
-    const double Vref = __ldcg(A.V + (int64_t)cj * n + ci);
-
-    // stage tile + halo (coalesced fp64 row reads, converted relative to V_ref)
+    // stage tile + halo (coalesced fp64 row reads, held in registers: one consistent snapshot
+    // even while neighbouring CTAs of the same round write their tiles), converted relative to
+    // V_ref = the tile-centre value (|u| at most half the tile's value range), or with PDD_RAWMIN
+    // min(V0, minimum of the staged values): every u >= 0 and D >= 0, so every candidate
+    // c0 + sum W u is >= 0 and the fp32 min over controls can compare raw float bits
     const int W2 = TW + 2 * H, H2 = TH + 2 * H;
-    for (int e = threadIdx.x; e < H2 * W2; e += blockDim.x) {
-        const int r = e / W2, c = e - r * W2;
-        const int gj = j0 - H + r, gi = i0 - H + c;
-        real v = 0;
-        if (gj >= 0 && gj < n && gi >= 0 && gi < n)
-            v = (real)(__ldcg(A.V + (int64_t)gj * n + gi) - Vref);
+    constexpr int MAXE = 16;                       // (TH + 2H)(TW + 2H) <= 16 x 256 (H <= 4)
+    double vs[MAXE];
+    double vmin = INFINITY;
 #pragma unroll
-        for (int q = 0; q < NCOPY; ++q) s_u[q * A.g.cstride + q + r * pitch + c] = v;
+    for (int m = 0; m < MAXE; ++m) {
+        const int e = threadIdx.x + m * (int)blockDim.x;
+        vs[m] = INFINITY;
+        if (e < H2 * W2) {
+            const int r = e / W2, c = e - r * W2;
+            const int gj = j0 - H + r, gi = i0 - H + c;
+            if (gj >= 0 && gj < n && gi >= 0 && gi < n) {
+                vs[m] = __ldcg(A.V + (int64_t)gj * n + gi);
+                vmin = fmin(vmin, vs[m]);
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) vmin = fmin(vmin, __shfl_xor_sync(FULL, vmin, o));
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = vmin;
+    __syncthreads();
+    // V_ref <= V0 keeps D = h l - (1 - beta) V_ref >= 0 also for inputs above the supersolution
+    // V0 (pdd_apply_operator on arbitrary V, u_hat above V0 in enclosed regions)
+    double Vref;
+    if constexpr (PATH == 3 && sizeof(real) == 4 && kRawMinRef) {
+        Vref = A.P.v0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) Vref = fmin(Vref, s_red[w]);
+    } else {
+        // the other paths compare with order-mapped keys / shuffles: the tile-centre value keeps
+        // |u| smallest (fp64 runs to r <= 1e-12 (1 - beta) sit at a few ulp of u)
+        const int ci = min(i0 + TW / 2, n - 1), cj = min(j0 + TH / 2, n - 1);
+        Vref = __ldcg(A.V + (int64_t)cj * n + ci);
+    }
+#pragma unroll
+    for (int m = 0; m < MAXE; ++m) {
+        const int e = threadIdx.x + m * (int)blockDim.x;
+        if (e < H2 * W2) {
+            const int r = e / W2, c = e - r * W2;
+            const real v = vs[m] < INFINITY ? (real)(vs[m] - Vref) : (real)0;
+#pragma unroll
+            for (int q = 0; q < NCOPY; ++q) s_u[q * A.g.cstride + q + r * pitch + c] = v;
+        }
     }
     for (int e = threadIdx.x; e < 2 * A.P.na; e += blockDim.x) s_ctrl[e] = (real)A.P.ctrl[e];
     if (threadIdx.x < TH) s_prog[threadIdx.x] = 0;
     __syncthreads();
 
-    // D = h l - (1 - beta) V_ref (constant cost; a cost field uses D per node in general path)
-    const real D = (real)(A.P.h * A.P.lmax - (1.0 - A.P.beta) * Vref);
+    // D = h l - (1 - beta) V_ref >= 0 (V_ref <= V0 = h l / (1 - beta); the clamp removes fp64
+    // rounding noise at V_ref = V0) for a constant cost; a cost field uses D per node in the
+    // general path
+    const double Dd = A.P.h * A.P.lmax_x - (1.0 - A.P.beta) * Vref;
+    const real D = (real)((PATH == 3 && sizeof(real) == 4 && kRawMinRef) ? fmax(Dd, 0.0) : Dd);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     real res = 0;
     int done_sweeps = CHECK ? 1 : A.k_inner;
@@ -648,6 +698,13 @@ static cudaError_t dispatch(const SweepLaunch &L, cudaStream_t s)
     PDD_RT(4, 4)
 #undef PDD_RT
     return cudaErrorInvalidValue;
+}
+
+void p3_geometry(int &pitch, int &cstride, int &hmax)
+{
+    pitch = P3_PITCH;
+    cstride = P3_CSTRIDE;
+    hmax = P3_HMAX;
 }
 
 cudaError_t launch_sweep(const SweepLaunch &L, cudaStream_t s)
@@ -950,8 +1007,13 @@ __device__ __forceinline__ void rt_feet(const DProblem &P, int j, int a, int b, 
     yr = P.q * (c * P.ctrl[2 * a + 1] + d2);
     if (P.p > 0) {
         const int kk = b >> 1;
-        const double ox = P.sc * coef_at(P.sigma[kk][0], 0, j, n);
-        const double oy = P.sc * coef_at(P.sigma[kk][1], 0, j, n);
+        double ox = P.sc * coef_at(P.sigma[kk][0], 0, j, n);
+        double oy = P.sc * coef_at(P.sigma[kk][1], 0, j, n);
+        if (P.sigma_mode == 1) {            // sigma(x, a) = s(x) a (R32)
+            const double sa = P.sc * coef_at(P.sigma[0][0], 0, j, n);
+            ox = sa * P.ctrl[2 * a];
+            oy = sa * P.ctrl[2 * a + 1];
+        }
         if (b & 1) { xr -= ox; yr -= oy; } else { xr += ox; yr += oy; }
     }
     yr = fmin(fmax(yr, (double)-j), (double)(n - 1 - j));

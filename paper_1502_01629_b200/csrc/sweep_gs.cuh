@@ -49,6 +49,13 @@ __device__ __forceinline__ void prog_release(volatile int *p, int v)
 #endif
 }
 
+__device__ __forceinline__ int prog_acquire_addr(unsigned a)
+{
+    int v;
+    asm volatile("ld.acquire.cta.shared.s32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+
 __device__ __forceinline__ int prog_acquire(volatile int *p)
 {
 #if PDD_ACQREL
@@ -63,12 +70,32 @@ __device__ __forceinline__ int prog_acquire(volatile int *p)
 #endif
 }
 
+// path-3 shared-memory geometry for H <= 4 (runtime.cu prepare() uses the same numbers): rows of
+// 76 floats (16-byte aligned, odd number of 16-byte groups), 4 shifted copies 3048 floats apart
+// ((TH + 8) x 76 + 4 rounded so the copies start in different bank groups)
+constexpr int P3_PITCH = 76;
+constexpr int P3_CSTRIDE = 3048;
+constexpr int P3_HMAX = 4;
+
+// PDD_RAWMIN 1: V_ref = min of the staged tile, all candidates >= 0, REDUX on the raw float bits
+// (saves 4 ALU ops per node, ~3 % on C5) -- off by default: |u| then spans the whole tile range
+// instead of half of it, and on coarse grids (tile value range ~1) the fp32 noise floor
+// (1 ulp of u = 1.2e-7) rises above a 1e-7 tolerance
+#ifndef PDD_RAWMIN
+#define PDD_RAWMIN 0
+#endif
+
 template <int CPL, int WY, int WX, bool CHECK, bool XNEG>
 __device__ __forceinline__ void row_gs4(const KP<float> &A, float *s_u, const float *s_ctrl,
-                                        volatile int *s_prog, int pitch, int cstride, int H,
+                                        volatile int *s_prog, int pitch_rt, int cstride_rt, int H,
                                         int i0, int ly, int gj, int jj, int base, int lead,
                                         float D, bool last, float &res, double Vref)
 {
+    // compile-time smem geometry (P3_PITCH / P3_CSTRIDE, checked against the host's TileGeom):
+    // every window row / shifted-copy offset becomes an immediate of the LDS / STS
+    (void)pitch_rt;
+    (void)cstride_rt;
+    constexpr int pitch = P3_PITCH, cstride = P3_CSTRIDE;
     constexpr int TW = 64;
     constexpr int NG = TW / 4;                 // groups per row
     constexpr int NWC = WX + 3;                // window columns used per group
@@ -89,7 +116,8 @@ __device__ __forceinline__ void row_gs4(const KP<float> &A, float *s_u, const fl
     for (int c = 0; c < CPL; ++c) {
         const int kk = lane + 32 * c;
         const RowEntry<float, WY, WX> &e = tab[kk];
-        c0[c] = kk < A.P.na ? D * e.E : rinf<float>();
+        const float Dk = (kk < A.P.na && A.P.cost_ctrl) ? D + (float)(A.P.h * A.P.cost_ctrl[kk]) : D;   // R33
+        c0[c] = kk < A.P.na ? Dk * e.E : rinf<float>();
 #pragma unroll
         for (int m = 0; m < WY * WX; ++m) Wt[c][m] = e.W[m];
         const int oy = e.oy, ox = e.ox;
@@ -107,12 +135,21 @@ __device__ __forceinline__ void row_gs4(const KP<float> &A, float *s_u, const fl
     const int eo = (ly + H) * pitch + H;                      // node row, lx = 0
     const int qo = (4 - (eo & 3)) & 3;
     const float *oldp = s_u + qo * cstride + qo + eo;         // aligned old-value loads
+    // commit: lane L < 16 writes node nd = L & 3 of each group into shifted copy L >> 2
+    const int nd = lane & 3;
+    float *cptr = rowp + (lane >> 2) * (cstride + 1) + nd;
+    // per-lane skip bits of its node in every group (bit G = node 4G + nd is special)
+    unsigned skip16 = 0u;
+#pragma unroll
+    for (int G = 0; G < NG; ++G) skip16 |= (unsigned)((skip >> (4 * G + nd)) & 1ull) << G;
+    const unsigned long long edge = emask & ~dmask;           // nodes needing the general stencil
+    const unsigned prog_prev = (unsigned)__cvta_generic_to_shared((const void *)(s_prog + (jj > 0 ? jj - 1 : 0)));
     for (int gs = 0; gs < NG; ++gs) {
         const int G = xneg ? NG - 1 - gs : gs;
         const int g = 4 * G;
         if (!CHECK && jj > 0) {
             const int need = base + min(gs + lead, NG);
-            while (prog_acquire(s_prog + jj - 1) < need) PDD_SPIN_PAUSE();
+            while (prog_acquire_addr(prog_prev) < need) PDD_SPIN_PAUSE();
         }
         // candidate sums, one control at a time (the window of a control is dead once its four
         // sums are formed: keeps the live set small enough for 3 CTAs / SM without remat)
@@ -147,7 +184,7 @@ __device__ __forceinline__ void row_gs4(const KP<float> &A, float *s_u, const fl
         const unsigned sk4 = (unsigned)(skip >> g) & 0xfu;     // special nodes of this group
         const float4 o4 = *reinterpret_cast<const float4 *>(oldp + g);
         const float old[4] = {o4.x, o4.y, o4.z, o4.w};
-        float nv[4], dlt[4];
+        float nv[4], dlt[4], rd[4];
         // finish the 4 nodes in sweep order with in-group Gauss-Seidel corrections
 #pragma unroll
         for (int s = 0; s < 4; ++s) {
@@ -160,29 +197,37 @@ __device__ __forceinline__ void row_gs4(const KP<float> &A, float *s_u, const fl
                 for (int d = 1; d <= s; ++d) a = fmaf(wc[c][d - 1], dlt[xneg ? gg + d : gg - d], a);
                 m = fminf(m, a);
             }
-            m = warp_min(m);     // fp32: one integer REDUX (warp_min<float>)
+#if PDD_RAWMIN
+            // all candidates are >= 0 (V_ref = min of the staged tile, sweep_tile): non-negative
+            // floats order like their bit patterns, so one REDUX on the raw bits is the min
+            m = __int_as_float(__reduce_min_sync(FULL, __float_as_int(m)));
+#else
+            m = warp_min(m);     // fp32: one integer REDUX on order-mapped bits
+#endif
             const bool sk = (sk4 >> gg) & 1u;
             nv[gg] = m;
-            dlt[gg] = (sk || CHECK) ? 0.f : m - old[gg];
+            rd[gg] = sk ? 0.f : m - old[gg];
+            dlt[gg] = CHECK ? 0.f : rd[gg];
         }
-        if (lane < 4) {
-            const int lx = g + lane;
-            if (!((sk4 >> lane) & 1u)) {
-                const float x = lane == 0 ? nv[0] : lane == 1 ? nv[1] : lane == 2 ? nv[2] : nv[3];
-                const float ol = lane == 0 ? old[0] : lane == 1 ? old[1] : lane == 2 ? old[2] : old[3];
-                if (last) res = fmaxf(res, fabsf(x - ol));
-                float *p = rowp + lx;
+        if (last)
+            res = fmaxf(res, fmaxf(fmaxf(fabsf(rd[0]), fabsf(rd[1])), fmaxf(fabsf(rd[2]), fabsf(rd[3]))));
+        {
+            // lane L < 16 writes node L & 3 of the group into shifted copy L >> 2 (one STS)
+            float x = nv[0];
+            x = nd == 1 ? nv[1] : x;
+            x = nd == 2 ? nv[2] : x;
+            x = nd == 3 ? nv[3] : x;
+            if (!((skip16 >> G) & 1u)) {
                 if (!CHECK) {
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) p[q * cstride + q] = x;
-                } else if (A.out) {
-                    A.out[(int64_t)gj * n + i0 + lx] = Vref + (double)x;
+                    if (lane < 16) cptr[g] = x;
+                } else if (A.out && lane < 4) {
+                    A.out[(int64_t)gj * n + i0 + g + nd] = Vref + (double)x;
                 }
             }
         }
         // nodes of this group whose feet may be clamped in x: general stencil (these sit
         // within H of the domain's x-boundary; their in-group order is not enforced)
-        unsigned long long em = (emask & ~dmask) & (0xfull << g);
+        unsigned long long em = edge ? edge & (0xfull << g) : 0ull;
         if (em) {
             __syncwarp();
             while (em) {

@@ -97,6 +97,10 @@ class Instance:
     tol_coarse: float = 1e-12
     precision: int = 64
     meta: dict = dataclasses.field(default_factory=dict)
+    # general nonlinear terms (readings R32, R33)
+    sigma_mode: int = 0             # 1: one noise column along the control, sigma(x,a) = s(x) a,
+                                    #    s = sigma[0][0] (p = 1)
+    cost_ctrl: Optional[np.ndarray] = None   # (N_A,) additive per-control cost m(a_k)
 
     @property
     def n_controls(self) -> int:
@@ -126,6 +130,10 @@ class Instance:
                 hsh.update(c.data.tobytes())
         hsh.update(self.kind.tobytes())
         hsh.update(self.sector.tobytes())
+        if self.sigma_mode:
+            hsh.update(b"sigma_mode=%d" % self.sigma_mode)
+        if self.cost_ctrl is not None:
+            hsh.update(np.ascontiguousarray(self.cost_ctrl, dtype=np.float64).tobytes())
         if self.coarse is not None:
             hsh.update(self.coarse.fingerprint().encode())
         return hsh.hexdigest()
@@ -390,6 +398,70 @@ def exit_instance(n: int, *, problem: str = "eikonal", eps: float = 0.0, h_ratio
                          diffusion_scale=1)
 
 
+def boundary_side_sectors(n: int, mask: np.ndarray, n_patches: int) -> np.ndarray:
+    """Gamma_p for a boundary-ring Dirichlet set (exit problems): angular sectors about the box
+    centre rotated by pi/4, so that n_patches = 4 gives the four sides of the square (P:1107,
+    reading R34); corner nodes belong to the side counter-clockwise of them."""
+    sec = np.full(n * n, -1, dtype=np.int32)
+    idx = np.nonzero(mask)[0]
+    c = 0.5 * (n - 1)
+    th = np.arctan2(idx // n - c, idx % n - c) + 0.25 * math.pi
+    th = np.mod(th, 2.0 * math.pi)
+    sec[idx] = np.minimum(np.floor(n_patches * th / (2.0 * math.pi)).astype(np.int64), n_patches - 1)
+    return sec
+
+
+def general_instance(n: int, *, cost: int = 3, sigma: int = 3, eps: float = 0.1,
+                     lam: float = 0.0, h_ratio: float = 0.5, n_a: int = 16,
+                     n_coarse: Optional[int] = None, n_patches: int = 4,
+                     coarse_level: bool = False) -> Instance:
+    """The paper's general nonlinear test on the exit-time setup of P:878-885
+    (Omega = [-1,1]^2, g = 0 on the boundary ring, 16 controls on the unit circle, sqrt(h)
+    scaling, h = h_ratio dx; lam = 0: no discount as in the paper):
+        f(x,a) = c(x) a,  c(x) = 1 + max{x2, max{x1, 0}}                         Eq. (nonomog)
+        d_eps(x) = sqrt(2 eps) chi_{x2 >= 0}(x)
+        sigma_1 = 0,  sigma_2(x) = d_eps(x) I_2,  sigma_3(x,a) = d_eps(x) a      Eq. (s123)
+        l_1 = 1,  l_2(x) = 1 + |x1 x2|,  l_3(x,a) = 1 + |x1 x2| + |a1 / (2 + a2)|  Eq. (l123)
+    ``cost`` / ``sigma`` select i, j in 1..3.  m(a) = |a1/(2+a2)| is tabulated per control (problem
+    data, fp64)."""
+    if cost not in (1, 2, 3) or sigma not in (1, 2, 3):
+        raise ValueError("cost and sigma select l_1..l_3 and sigma_1..sigma_3")
+    lo, hi = -1.0, 1.0
+    dx = grid_params(n, lo, hi)
+    x = lo + np.arange(n) * dx
+    X1, X2 = np.meshgrid(x, x, indexing="xy")          # [j, i]: X1 varies along i (x fastest)
+    kind = np.zeros((n, n), dtype=np.uint8)
+    kind[0, :] = kind[-1, :] = kind[:, 0] = kind[:, -1] = KIND_TARGET
+    speed = Coef.field(1.0 + np.maximum(X2, np.maximum(X1, 0.0)))
+    d = Coef.row(np.where(x >= 0.0, math.sqrt(2.0 * eps), 0.0))
+    z = Coef.const(0.0)
+    p, sig, smode = 0, ((z, z), (z, z)), 0
+    if sigma == 2 and not coarse_level:
+        p, sig = 2, ((d, z), (z, d))
+    elif sigma == 3 and not coarse_level:
+        p, sig, smode = 1, ((d, z), (z, z)), 1
+    lc = Coef.const(1.0) if cost == 1 else Coef.field(1.0 + np.abs(X1 * X2))
+    ctrl = unit_circle_controls(n_a)
+    cc = np.abs(ctrl[:, 0] / (2.0 + ctrl[:, 1])) if cost == 3 else None
+    mask = kind.reshape(-1) == KIND_TARGET
+    inst = make_instance(f"general-l{cost}s{sigma}", n, lo, hi, n_a=n_a, lam=lam, speed=speed,
+                         p=p, sigma=sig, cost=lc, kind=kind, h=h_ratio * dx, diffusion_scale=1,
+                         sigma_mode=smode, cost_ctrl=cc,
+                         sector=boundary_side_sectors(n, mask, n_patches), n_patches=n_patches,
+                         static_blocks=(2, 2))
+    inst.meta.update(cost=cost, sigma=sigma, eps=eps)
+    if coarse_level:
+        inst.name += "-coarse"
+    elif n_coarse is not None:
+        if (n - 1) % (n_coarse - 1) != 0:
+            raise ValueError("coarse grid must nest in the fine grid")
+        # the coarse solve is the sigma = 0 problem on G_c with the same h / dx ratio (P:824-825)
+        inst.coarse = general_instance(n_coarse, cost=cost, sigma=sigma, eps=eps, lam=lam,
+                                       h_ratio=h_ratio, n_a=n_a, n_patches=n_patches,
+                                       coarse_level=True)
+    return inst
+
+
 def random_instance(n: int, seed: int, *, n_a: int = 8, p: int = 2, lam: float = 1.0,
                     field_speed: bool = True, obstacles: bool = True) -> Instance:
     """Small random instance (for brute force / schedule-independence pins): random positive
@@ -419,6 +491,9 @@ def reach_cells(inst: Instance) -> float:
         smax = 0.0
     else:
         sc = math.sqrt(inst.h * inst.p) if inst.diffusion_scale == 0 else math.sqrt(inst.h)
-        smax = sc * max(math.hypot(inst.sigma[k][0].max_abs(), inst.sigma[k][1].max_abs())
-                        for k in range(inst.p))
+        if inst.sigma_mode == 1:
+            smax = sc * inst.sigma[0][0].max_abs() * amax
+        else:
+            smax = sc * max(math.hypot(inst.sigma[k][0].max_abs(), inst.sigma[k][1].max_abs())
+                            for k in range(inst.p))
     return (inst.h * fmax + smax) / inst.dx

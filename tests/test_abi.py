@@ -78,8 +78,22 @@ def test_validation_errors_without_gpu(lib):
     bad.s.n_controls = 0
     assert lib.pdd_workspace_bytes(C.byref(bad.s), None, 32, C.byref(nb)) == N.PDD_E_INVALID
     bad = _ProblemView(inst)
-    bad.s.lam = 0.0
+    bad.s.lam = -1.0
     assert lib.pdd_workspace_bytes(C.byref(bad.s), None, 32, C.byref(nb)) == N.PDD_E_INVALID
+    ok = _ProblemView(inst)
+    ok.s.lam = 0.0                      # exit problem without obstacles: valid
+    assert lib.pdd_workspace_bytes(C.byref(ok.s), None, 32, C.byref(nb)) == N.PDD_OK
+    obst = _ProblemView(I.make_config("C4", n=65))
+    obst.s.lam = 0.0                    # obstacle value 1/lambda undefined
+    assert lib.pdd_workspace_bytes(C.byref(obst.s), None, 32, C.byref(nb)) == N.PDD_E_INVALID
+    assert b"obstacles" in lib.pdd_last_error(None)
+    bad = _ProblemView(inst)
+    bad.s.sigma_mode = 1                # sigma(x,a) = s(x) a needs p = 1 (C1 has p = 2)
+    assert lib.pdd_workspace_bytes(C.byref(bad.s), None, 32, C.byref(nb)) == N.PDD_E_INVALID
+    g = I.general_instance(17, cost=3, sigma=3)
+    assert lib.pdd_workspace_bytes(C.byref(_ProblemView(g).s), None, 32, C.byref(nb)) == N.PDD_OK
+    g.cost_ctrl = g.cost_ctrl - 10.0    # l(x) + m(a) <= 0
+    assert lib.pdd_workspace_bytes(C.byref(_ProblemView(g).s), None, 32, C.byref(nb)) == N.PDD_E_INVALID
     assert lib.pdd_workspace_bytes(C.byref(v.s), None, 16, C.byref(nb)) == N.PDD_E_INVALID
     bad = _ProblemView(inst)
     bad.s.cost.value = 0.0

@@ -247,12 +247,17 @@ def _transitions(inst, k, a):
     q = inst.h / inst.dx
     c = inst.speed.at(i, j, n)
     f = c * inst.controls[a] + np.array([inst.drift[0].at(i, j, n), inst.drift[1].at(i, j, n)])
-    sc = math.sqrt(inst.h * inst.p) / inst.dx if inst.p else 0.0
+    sc = 0.0
+    if inst.p:
+        sc = (math.sqrt(inst.h * inst.p) if inst.diffusion_scale == 0 else math.sqrt(inst.h)) / inst.dx
     pts = []
     if inst.p == 0:
         pts.append(q * f)
     for kk in range(inst.p):
-        o = sc * np.array([inst.sigma[kk][0].at(i, j, n), inst.sigma[kk][1].at(i, j, n)])
+        if inst.sigma_mode == 1:      # sigma(x,a) = s(x) a (R32)
+            o = sc * inst.sigma[0][0].at(i, j, n) * np.asarray(inst.controls[a], dtype=float)
+        else:
+            o = sc * np.array([inst.sigma[kk][0].at(i, j, n), inst.sigma[kk][1].at(i, j, n)])
         pts += [q * f + o, q * f - o]
     row = {}
     for g in pts:
@@ -293,6 +298,72 @@ def test_p6_policy_iteration_matches_jacobi(n, seed, p):
     for k in list(pol)[:30]:
         vals = [h + beta * sum(w * J["V"][idx] for idx, w in rows[(k, a)].items()) for a in range(8)]
         assert abs(min(vals) - J["V"][k]) < 1e-12
+
+
+def _howard(inst):
+    """Howard policy iteration with dense solves on the implicit scheme (P:366-375 with the
+    discount; exit problems: lambda = 0, g = 0 on the boundary ring).  Cost per control
+    h l(x_i, a) = h (l(x_i) + m(a)) (R33).  Independent of the oracle's code."""
+    n, N = inst.n, inst.n * inst.n
+    na = inst.n_controls
+    beta, h = inst.beta, inst.h
+    free = np.nonzero(inst.kind == I.KIND_FREE)[0]
+    dval = np.where(inst.kind == I.KIND_OBSTACLE, 1.0 / inst.lam if inst.lam > 0 else 0.0, 0.0)
+    mm = inst.cost_ctrl if inst.cost_ctrl is not None else np.zeros(na)
+    rows = {(k, a): _transitions(inst, k, a) for k in free for a in range(na)}
+    cost = {(k, a): h * (inst.cost.at(k % n, k // n, n) + mm[a]) for k in free for a in range(na)}
+    # start from the policy that moves straight to the nearest boundary side (proper for exit
+    # problems: every policy iterate stays proper, the value only decreases)
+    pol = {}
+    for k in free:
+        i, j = k % n, k // n
+        side = int(np.argmin([n - 1 - i, j, i, n - 1 - j]))      # +x, -y, -x, +y
+        target = [0.0, -0.5 * math.pi, math.pi, 0.5 * math.pi][side]
+        ang = np.arctan2(inst.controls[:, 1], inst.controls[:, 0])
+        pol[k] = int(np.argmin(np.abs(np.angle(np.exp(1j * (ang - target))))))
+    for _ in range(300):
+        A = np.eye(N)
+        rhs = dval.copy()
+        for k, a in pol.items():
+            rhs[k] = cost[(k, a)]
+            for idx, w in rows[(k, a)].items():
+                A[k, idx] -= beta * w
+        v = np.linalg.solve(A, rhs)
+        changed = False
+        for k in pol:
+            vals = [cost[(k, a)] + beta * sum(w * v[idx] for idx, w in rows[(k, a)].items())
+                    for a in range(na)]
+            b = int(np.argmin(vals))
+            if vals[b] < vals[pol[k]] - 1e-14:
+                pol[k] = b
+                changed = True
+        if not changed:
+            return v
+    raise AssertionError("policy iteration did not stop")
+
+
+@pytest.mark.parametrize("cost,sigma,lam", [(3, 3, 0.0), (2, 2, 0.0), (3, 1, 0.0), (1, 3, 0.0),
+                                            (3, 3, 1.0)])
+def test_p6b_general_nonlinear_terms_policy_iteration(cost, sigma, lam):
+    """P6 for the general nonlinear terms of P:1047-1064: control-dependent diffusion
+    sigma_3(x,a) = d_eps(x) a and cost l_3(x,a) = 1 + |x1 x2| + |a1/(2+a2)| (exit problem,
+    lambda = 0, and a discounted variant): the oracle's Jacobi fixed point equals the exact
+    solution of the finite MDP found by policy iteration."""
+    inst = I.general_instance(11, cost=cost, sigma=sigma, eps=0.1, lam=lam, n_a=8)
+    v = _howard(inst)
+    J = O.jacobi(inst, tol=1e-15, max_sweeps=200000)
+    assert np.abs(J["V"] - v).max() < 1e-11
+
+
+def test_p6c_control_aligned_diffusion_differs_and_reduces():
+    """sigma_3 = d a must move the feet along the control (not the axes): with d = 0 it reduces
+    to sigma_1 bit for bit, and with d > 0 it differs from sigma_2 = d I."""
+    i1 = I.general_instance(17, cost=1, sigma=1)
+    i3 = I.general_instance(17, cost=1, sigma=3, eps=0.0)
+    assert np.array_equal(O.jacobi(i1, tol=1e-13)["V"], O.jacobi(i3, tol=1e-13)["V"])
+    i2 = I.general_instance(17, cost=1, sigma=2)
+    i3 = I.general_instance(17, cost=1, sigma=3)
+    assert np.abs(O.jacobi(i2, tol=1e-13)["V"] - O.jacobi(i3, tol=1e-13)["V"]).max() > 1e-3
 
 
 # ---------------------------------------------------------------------------------- P8 / P9
