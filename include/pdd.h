@@ -204,6 +204,30 @@ pdd_status pdd_get_successors(pdd_ctx *ctx, int32_t *dst, int32_t dst_on_device)
  * an active tile (n_patches + 1 entries, the last one for orphans). */
 pdd_status pdd_get_patch_rounds(pdd_ctx *ctx, int32_t *dst, int32_t count);
 
+/* The upwind diffusion ball analysis of P:528-697 (host arithmetic, no context, no GPU).
+ * Inputs: f_min, f_max = min / max of |f(x,a)| over Omega x A (> 0), sigma_norm = ||sigma||_inf
+ * (the longest diffusion row; sqrt(2 eps) for sigma = sqrt(2 eps) I), dx.
+ *   omega     = f_min / sigma_norm^2                      (+inf when sigma = 0)
+ *   upsilon   = f_max / f_min
+ *   alpha_lo  = 1 / (omega dx)                            Eq. (lower-alpha)
+ *   alpha_hi  = 1/upsilon - (sqrt(1 + 4 omega dx upsilon) - 1) / (2 omega dx upsilon^2)
+ *                                                         Eq. (upper-alpha)
+ *   tau_dx    = dx / (1 + upsilon);  hyperbolic = 1/omega < tau_dx   Eq. (hyperbolicity)
+ *               (equality, up to 1e-12 relative, counts as not hyperbolic: reading R37)
+ *   alpha     = 1/(1 + upsilon) when hyperbolic, else 0.99 alpha_hi (the paper keeps
+ *               the upper bound and gives up the lower one; reading R36)
+ *   h         = alpha dx / f_min
+ *   eps_threshold = f_min dx / (2 (1 + upsilon)): the eps below which sigma = sqrt(2 eps) I is
+ *               hyperbolic (dx/4 for the eikonal equation, dx/120 for Zermelo
+ *               P:1240-1244). */
+typedef struct {
+    double omega, upsilon, alpha_lo, alpha_hi, alpha, h, tau_dx, eps_threshold;
+    int32_t hyperbolic;
+    int32_t reserved;
+} pdd_regime;
+pdd_status pdd_regime_analyse(double f_min, double f_max, double sigma_norm, double dx,
+                              pdd_regime *out);
+
 /* Number of kernels this context has enqueued since pdd_create (all calls). */
 long long pdd_kernel_launches(const pdd_ctx *ctx);
 

@@ -250,3 +250,16 @@ class Solver:
         self.build_patches(self.inst.n_patches)
         out["fine"] = self.solve("patchy", tol=tol, k_inner=k_inner, **kw)
         return out
+
+
+def regime_analyse(f_min: float, f_max: float, sigma_norm: float, dx: float) -> dict:
+    """The upwind diffusion ball analysis of P:528-697 through the C ABI (pdd_regime_analyse):
+    omega, upsilon, alpha bounds, the hyperbolicity flag, the paper's time step h = alpha dx /
+    f_min and the eps threshold of sigma = sqrt(2 eps) I."""
+    r = N.pdd_regime()
+    st = N.lib().pdd_regime_analyse(float(f_min), float(f_max), float(sigma_norm), float(dx),
+                                    C.byref(r))
+    _check(st, None)
+    d = r.as_dict()
+    d["hyperbolic"] = bool(d["hyperbolic"])
+    return d

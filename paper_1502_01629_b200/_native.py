@@ -22,7 +22,8 @@ EXPORTS = ["pdd_version", "pdd_workspace_bytes", "pdd_create", "pdd_coarse_solve
            "pdd_synthesize", "pdd_build_patches", "pdd_build_static", "pdd_solve",
            "pdd_apply_operator", "pdd_get_values", "pdd_set_values", "pdd_get_uhat",
            "pdd_get_coarse_values", "pdd_get_controls", "pdd_get_labels", "pdd_get_successors",
-           "pdd_get_patch_rounds", "pdd_kernel_launches", "pdd_last_error", "pdd_destroy"]
+           "pdd_get_patch_rounds", "pdd_kernel_launches", "pdd_last_error", "pdd_destroy",
+           "pdd_regime_analyse"]
 
 
 class pdd_coef(C.Structure):
@@ -56,6 +57,16 @@ class pdd_solve_stats(C.Structure):
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class pdd_regime(C.Structure):
+    _fields_ = [("omega", C.c_double), ("upsilon", C.c_double), ("alpha_lo", C.c_double),
+                ("alpha_hi", C.c_double), ("alpha", C.c_double), ("h", C.c_double),
+                ("tau_dx", C.c_double), ("eps_threshold", C.c_double), ("hyperbolic", C.c_int32),
+                ("reserved", C.c_int32)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
 
 
 class pdd_coarse_stats(C.Structure):
@@ -96,6 +107,8 @@ def lib():
               "pdd_get_successors"):
         getattr(L, f).argtypes = [ctx, vp, C.c_int32]
     L.pdd_get_patch_rounds.argtypes = [ctx, vp, C.c_int32]
+    L.pdd_regime_analyse.argtypes = [C.c_double, C.c_double, C.c_double, C.c_double,
+                                     C.POINTER(pdd_regime)]
     L.pdd_destroy.argtypes = [ctx]
     L.pdd_kernel_launches.argtypes = [ctx]
     L.pdd_kernel_launches.restype = C.c_longlong

@@ -1094,6 +1094,32 @@ pdd_status pdd_apply_operator(pdd_ctx *ctx, double *out, int32_t kernel, double 
     return PDD_OK;
 }
 
+pdd_status pdd_regime_analyse(double f_min, double f_max, double sigma_norm, double dx,
+                              pdd_regime *out)
+{
+    if (!out) return fail(nullptr, PDD_E_INVALID, "out is NULL");
+    if (!(f_min > 0.0) || !(f_max >= f_min) || !(sigma_norm >= 0.0) || !(dx > 0.0))
+        return fail(nullptr, PDD_E_INVALID, "regime: need 0 < f_min <= f_max, sigma_norm >= 0, dx > 0");
+    pdd_regime r{};
+    r.upsilon = f_max / f_min;
+    r.omega = sigma_norm > 0.0 ? f_min / (sigma_norm * sigma_norm) : INFINITY;
+    r.tau_dx = dx / (1.0 + r.upsilon);
+    const double inv_omega = sigma_norm > 0.0 ? (sigma_norm * sigma_norm) / f_min : 0.0;
+    r.alpha_lo = inv_omega / dx;
+    if (sigma_norm > 0.0) {
+        const double w = r.omega * dx * r.upsilon;
+        r.alpha_hi = 1.0 / r.upsilon - (std::sqrt(1.0 + 4.0 * w) - 1.0) / (2.0 * r.omega * dx * r.upsilon * r.upsilon);
+    } else {
+        r.alpha_hi = 1.0 / r.upsilon;
+    }
+    r.hyperbolic = inv_omega < r.tau_dx * (1.0 - 1e-12) ? 1 : 0;
+    r.alpha = r.hyperbolic ? 1.0 / (1.0 + r.upsilon) : 0.99 * r.alpha_hi;
+    r.h = r.alpha * dx / f_min;
+    r.eps_threshold = f_min * dx / (2.0 * (1.0 + r.upsilon));
+    *out = r;
+    return PDD_OK;
+}
+
 pdd_status pdd_get_patch_rounds(pdd_ctx *ctx, int32_t *dst, int32_t count)
 {
     if (!ctx || !dst) return fail(ctx, PDD_E_INVALID, "NULL argument");

@@ -340,6 +340,9 @@ __device__ __forceinline__ void row_table(const KP<real> &A, real *s_u, const re
     }
 }
 
+#ifndef PDD_GSG
+#define PDD_GSG 1    // path 1 (general stencil) uses the Gauss-Seidel tile sweeps of sweep_gs.cuh
+#endif
 #include "sweep_gs.cuh"
 
 constexpr bool kRawMinRef = PDD_RAWMIN != 0;   // fp32 path 3: V_ref = staged min (sweep_gs.cuh)
@@ -431,6 +434,12 @@ __device__ __forceinline__ void sweep_tile(const KP<real> &A, int t, unsigned ch
         done_sweeps = tile_gs4<CPL, WY, WX, CHECK>(A, s_u, s_ctrl, s_prog, s_red, pitch,
                                                    A.g.cstride, H, i0, j0, D, kin, res, Vref, ot & 3,
                                                    sbase);
+    } else if constexpr (PATH == 1 && PDD_GSG) {
+        const int ot = A.tile_orient ? A.tile_orient[t] : 0;
+        const int kin = (ot & 4) ? min(A.k_inner, A.k_coherent) : A.k_inner;
+        const int sbase = (A.tile_sweeps && !(ot & 4)) ? A.tile_sweeps[t] : 0;
+        done_sweeps = tile_gsg<real, CHECK>(A, s_u, s_ctrl, s_prog, s_red, pitch, H, i0, j0, D,
+                                            kin, res, Vref, ot & 3, sbase);
     } else {
         const int sweeps = CHECK ? 1 : A.k_inner;
         for (int sw = 0; sw < sweeps; ++sw) {

@@ -301,3 +301,95 @@ __device__ __forceinline__ int tile_gs4(const KP<float> &A, float *s_u, const fl
     }
     return sweeps;
 }
+
+
+// ------------------------------------------------------------------------------------------
+// General-stencil Gauss-Seidel sweeps (path 1: any coefficients, incl. fields such as C3's c(x)
+// and the general nonlinear terms; fp32 or fp64).  Same schedule as the row-table kernel: the
+// TH x 64 tile is swept k_inner times in the four fast-sweeping orientations (downstream first
+// for patchy tiles), a warp finishes its row one node at a time in the sweep's x order (each
+// node's gathers see the nodes finished before it: Gauss-Seidel along x), and rows follow the
+// sweep's y order through the same progress-counter pipeline over the 8 warps (a row starts a
+// 4-node group once the previous row is `lead` groups ahead): Gauss-Seidel along y.
+template <typename real, bool CHECK, bool XNEG>
+__device__ __forceinline__ void row_gsg(const KP<real> &A, real *s_u, const real *s_ctrl,
+                                        volatile int *s_prog, int pitch, int H, int i0, int ly,
+                                        int gj, int jj, int base, int lead, real D, real &res,
+                                        double Vref)
+{
+    constexpr int TW = 64;
+    constexpr int NG = TW / 4;
+    const int lane = threadIdx.x & 31;
+    const int n = A.P.n;
+    unsigned long long dmask, emask;
+    row_masks(A.P, TW, i0, gj, 0, dmask, emask);
+    real *rowp = s_u + (ly + H) * pitch + H;
+    const unsigned prog_prev =
+        (unsigned)__cvta_generic_to_shared((const void *)(s_prog + (jj > 0 ? jj - 1 : 0)));
+    for (int gs = 0; gs < NG; ++gs) {
+        if (!CHECK && jj > 0) {
+            const int need = base + min(gs + lead, NG);
+            while (prog_acquire_addr(prog_prev) < need) PDD_SPIN_PAUSE();
+        }
+#pragma unroll 1
+        for (int t = 0; t < 4; ++t) {
+            const int lx = XNEG ? TW - 1 - (4 * gs + t) : 4 * gs + t;
+            if ((dmask >> lx) & 1ull) continue;
+            const real best = general_node<real>(A.P, s_ctrl, rowp + lx, pitch, i0 + lx, gj, D, Vref);
+            commit_node<real, CHECK>(rowp + lx, best, true, res, A.out, (int64_t)gj * n + i0 + lx, Vref);
+            __syncwarp();      // lane 0's commit is seen by every lane's next gathers
+        }
+        if (!CHECK && lane == 0) prog_release(s_prog + jj, base + gs + 1);
+    }
+}
+
+template <typename real, bool CHECK>
+__device__ __forceinline__ int tile_gsg(const KP<real> &A, real *s_u, const real *s_ctrl,
+                                        volatile int *s_prog, double *s_red, int pitch, int H,
+                                        int i0, int j0, real D, int k_inner, real &res,
+                                        double Vref, int o0, int sbase)
+{
+    constexpr int NG = 16;
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int n = A.P.n;
+    const int lead = 1 + (3 + H) / 4;
+    const int sweeps = CHECK ? 1 : k_inner;
+    double first = 0.0;
+    for (int sw = 0; sw < sweeps; ++sw) {
+        res = (real)0;
+        const int orient = ((A.oxor >> (2 * ((sbase + sw) & 3))) & 3) ^ o0;
+        const bool xneg = orient & 1, yneg = orient & 2;
+        const int base = sw * NG;
+        for (int k = 0; k < TH / NW; ++k) {
+            const int jj = warp + NW * k;
+            const int ly = yneg ? TH - 1 - jj : jj;
+            const int gj = j0 + ly;
+            if (gj >= n) {
+                if (lane == 0) s_prog[jj] = base + NG;
+                continue;
+            }
+            if (xneg)
+                row_gsg<real, CHECK, true>(A, s_u, s_ctrl, s_prog, pitch, H, i0, ly, gj, jj, base,
+                                           lead, D, res, Vref);
+            else
+                row_gsg<real, CHECK, false>(A, s_u, s_ctrl, s_prog, pitch, H, i0, ly, gj, jj, base,
+                                            lead, D, res, Vref);
+        }
+        if (CHECK) break;
+        real r = res;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) r = rmax(r, __shfl_xor_sync(FULL, r, o));
+        if (lane == 0) s_red[warp] = (double)r;
+        __syncthreads();
+        if (A.early_tol > 0.0 && sw + 1 < sweeps) {
+            double m = 0.0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) m = fmax(m, s_red[w]);
+            __syncthreads();
+            if (sw == 0) first = m;
+            if (m < A.early_tol || m < A.early_rel * first) return sw + 1;
+        }
+    }
+    return sweeps;
+}

@@ -462,6 +462,78 @@ def general_instance(n: int, *, cost: int = 3, sigma: int = 3, eps: float = 0.1,
     return inst
 
 
+PAPER_FMINMAX = {"eikonal": (1.0, 1.0), "zermelo": (1.0 / 6.0, 1.5)}
+
+
+def paper_time_step(dx: float, eps: float, f_min: float, f_max: float) -> float:
+    """The paper's time step h = alpha dx / f_min: alpha = 1/(1 + Upsilon) when the upwind
+    diffusion ball condition 2 eps / f_min < dx / (1 + Upsilon) holds, otherwise
+    0.99 alpha_hi of Eq. (upper-alpha) so that h f_max + sqrt(2 eps h) < dx is kept (P:656-658;
+    DESIGN.md readings R36, R37).  Parameter choice only (problem data), no scheme arithmetic."""
+    ups = f_max / f_min
+    if eps <= 0.0 or (2.0 * eps / f_min) < (dx / (1.0 + ups)) * (1.0 - 1e-12):
+        alpha = 1.0 / (1.0 + ups)
+    else:
+        om = f_min / (2.0 * eps)
+        alpha = 0.99 * (1.0 / ups - (math.sqrt(1.0 + 4.0 * om * dx * ups) - 1.0) / (2.0 * om * dx * ups * ups))
+    return alpha * dx / f_min
+
+
+def paper_instance(problem: str, cells: int, eps: float, *, coarse_cells: Optional[int] = 50,
+                   eta: float = 1.0, theta: float = 0.25 * math.pi, n_a: int = 16,
+                   coarse_level: bool = False) -> Instance:
+    """The workloads of the paper's performance comparison (Tables 1 and 2):
+    Omega = [-1,1]^2 with ``cells`` cells per axis (the tables' "100^2 ... 800^2", dx = 2/cells,
+    reading Q26/R26), exit problem g = 0 on the boundary (lambda = 0), l = 1, 16 controls on the
+    unit circle, sigma = sqrt(2 eps) I with the paper's sqrt(h) scaling, h from
+    paper_time_step, boundary split into the four sides of the square, static
+    decomposition = four squares, coarse grid of 50^2 cells.
+      eikonal  (problem B, c = 1):  f(x,a) = a
+      zermelo  (problem C):         f(x,a) = (R_theta x/|x| + eta a / 2) / (1 + |x|^2)
+               theta = pi/4 and x/|x| := 0 at x = 0 (reading R35)."""
+    if problem not in PAPER_FMINMAX:
+        raise KeyError(problem)
+    lo, hi = -1.0, 1.0
+    n = cells + 1
+    dx = grid_params(n, lo, hi)
+    fmin, fmax = PAPER_FMINMAX[problem]
+    h = paper_time_step(dx, eps, fmin, fmax)
+    x = lo + np.arange(n) * dx
+    X1, X2 = np.meshgrid(x, x, indexing="xy")
+    kind = np.zeros((n, n), dtype=np.uint8)
+    kind[0, :] = kind[-1, :] = kind[:, 0] = kind[:, -1] = KIND_TARGET
+    z = Coef.const(0.0)
+    if problem == "eikonal":
+        speed, drift = Coef.const(1.0), (z, z)
+    else:
+        r2 = X1 * X1 + X2 * X2
+        r = np.sqrt(r2)
+        inv = np.where(r > 0.0, 1.0 / np.where(r > 0.0, r, 1.0), 0.0) / (1.0 + r2)
+        ct, st = math.cos(theta), math.sin(theta)
+        speed = Coef.field(0.5 * eta / (1.0 + r2))
+        drift = (Coef.field((ct * X1 - st * X2) * inv), Coef.field((st * X1 + ct * X2) * inv))
+    s = math.sqrt(2.0 * eps)
+    p = 2 if (eps > 0.0 and not coarse_level) else 0
+    sig = ((Coef.const(s), z), (z, Coef.const(s)))
+    mask = kind.reshape(-1) == KIND_TARGET
+    inst = make_instance(f"paper-{problem}-{cells}", n, lo, hi, n_a=n_a, lam=0.0, speed=speed,
+                         drift=drift, p=p, sigma=sig, kind=kind, h=h, diffusion_scale=1,
+                         sector=boundary_side_sectors(n, mask, 4), n_patches=4,
+                         static_blocks=(2, 2))
+    inst.meta.update(problem=problem, eps=eps, cells=cells, f_min=fmin, f_max=fmax)
+    if coarse_level:
+        inst.name += "-coarse"
+    elif coarse_cells is not None:
+        if cells % coarse_cells != 0:
+            raise ValueError("coarse grid must nest in the fine grid")
+        # same h/dx ratio on G_c (the coarse problem is the sigma = 0 problem there, P:824-825)
+        c = paper_instance(problem, coarse_cells, 0.0, coarse_cells=None, eta=eta, theta=theta,
+                           n_a=n_a, coarse_level=True)
+        c.h = h * (c.dx / dx)
+        inst.coarse = c
+    return inst
+
+
 def random_instance(n: int, seed: int, *, n_a: int = 8, p: int = 2, lam: float = 1.0,
                     field_speed: bool = True, obstacles: bool = True) -> Instance:
     """Small random instance (for brute force / schedule-independence pins): random positive
