@@ -67,6 +67,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-static", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-others", action="store_true",
+                    help="skip the time-to-converge report of the other BASELINE configs")
     return ap.parse_args()
 
 
@@ -353,6 +355,41 @@ def main():
         except Exception:
             pass
 
+    # the other BASELINE configs at full size (time-to-converge only; not the headline): patchy
+    # pipeline (coarse solve .. verified fine solve) and static solve on the same kernels
+    others = None
+    if not args.no_others and rank == 0 and args.n is None:
+        others = {}
+        for cfg in ("C1", "C2", "C3", "C4"):
+            if cfg == args.config:
+                continue
+            ci = I.make_config(cfg)
+            prec = 64 if cfg == "C1" else args.precision
+            so = Solver(ci, precision=prec, device=str(dev))
+            rec = {"grid": ci.n, "precision": prec, "tol": ci.tol}
+            for mode in (("static",) if ci.coarse is None else ("patchy", "static")):
+                pipeline_step(so, ci, args, mode=mode)                       # warm-up
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                if mode == "patchy":
+                    so.coarse_solve(ci.tol_coarse)
+                    so.synthesize()
+                    so.build_patches(ci.n_patches)
+                else:
+                    so.build_static(*ci.static_blocks)
+                sto = so.solve(mode, tol=ci.tol)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                rec[mode] = {"pipeline_s": e0.elapsed_time(e1) * 1e-3,
+                             "solve_s": sto["seconds_total"],
+                             "sweep_equivalents": sto["node_updates"] / ci.free_count(),
+                             "kernel_node_updates_per_s": sto["node_updates"] / max(sto["seconds_sweep"], 1e-12),
+                             "kernel": sto["kernel_used"], "converged": sto["converged"]}
+            so.close()
+            del so
+            others[cfg] = rec
+
     cpu = None
     if not args.no_cpu and rank == 0 and world == 1:
         v, desc, thr, _ = oracle_sample(inst, args.cpu_seconds)
@@ -368,7 +405,7 @@ def main():
                                    f" synthesis, {inst.n_patches} patch labels, fine solve to "
                                    f"tol {args.tol:g}) on {inst.n}^2",
                        "grid": inst.n, "controls": inst.n_controls, "branches": 2 * inst.p,
-                       "patches": inst.n_patches, "k_inner": args.k_inner if args.k_inner is not None else {"patchy": 1, "static": 4},
+                       "patches": inst.n_patches, "k_inner": args.k_inner if args.k_inner is not None else {"patchy": "auto (1)", "static": "auto (4)"},
                        "l2": "inputs larger than L2 (V fp64 %d MB)" % (inst.n * inst.n * 8 >> 20),
                        "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
             "time_to_converge": {"patchy_s": t_solve / args.steps,
@@ -377,6 +414,7 @@ def main():
                                  "rounds_patchy": rounds // args.steps,
                                  "sweep_equivalents_patchy": nu / args.steps / inst.free_count()},
             "static": static,
+            "other_configs": others,
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -107,10 +107,12 @@ typedef struct pdd_ctx pdd_ctx;
 typedef struct {
     int32_t mode;        /* 0 patchy: V starts at u_hat, tiles activated in ascending u_hat
                             order; 1 static: V starts at V0 (R11)         */
-    int32_t k_inner;     /* in-tile Gauss-Seidel sweeps per tile visit (>= 1).  Patchy tiles
-                            sweep first in their downstream orientation (the signs of u_hat's
-                            differences over the tile); incoherent tiles continue an orientation
-                            cycle across visits.  Measured best: 1 patchy, 4 static          */
+    int32_t k_inner;     /* in-tile Gauss-Seidel sweeps per tile visit (>= 1; 0 = automatic:
+                            1 patchy, 4 static, and 4 for a patchy grid whose tiles fit in one
+                            wave of sweep CTAs -- then the u_hat front is off too when delta
+                            = 0).  Patchy tiles sweep first in their downstream orientation
+                            (the signs of u_hat's differences over the tile); incoherent tiles
+                            continue an orientation cycle across visits                     */
     double tol;          /* sup-norm residual tolerance eps                                  */
     int64_t max_rounds;  /* cap on tile rounds                                               */
     double delta;        /* patchy bucket width in value units; 0 = automatic; < 0 = off      */
@@ -176,6 +178,29 @@ pdd_status pdd_synthesize(pdd_ctx *ctx);
  * jumping to the root of every successor chain; label = sector[root] when the root is a target
  * node, n_patches (orphan) otherwise; -1 on target nodes, -2 on obstacles.  M = 0 => 4. */
 pdd_status pdd_build_patches(pdd_ctx *ctx, int32_t n_patches, double M);
+
+/* The paper's own patch construction (reading R38): phi_p = chi_{Gamma_p} advected
+ * along the synthesised feedback by the semi-Lagrangian scheme phi_p(x_i) = phi_p(x_i + h f(x_i,
+ * a*(x_i))) (Eq. discrete-advection; sigma = 0 foot, bilinear, canonical fp64, Jacobi for all
+ * patches at once) until the sweep change is < eps_P (the paper's "poor tolerance"); then
+ * Omega_p = {phi_p >= tau_P} and the owner of a node is the patch of largest phi_p (lowest p on
+ * ties), orphan n_patches when every phi_p is 0; -1 target, -2 obstacle.  Replaces the labels of
+ * pdd_build_patches (a patchy pdd_solve then reports per-patch rounds for these patches).
+ * scratch: caller-owned DEVICE memory of >= pdd_fuzzy_scratch_bytes(n, n_patches) bytes (two
+ * patch-major fields n_patches x n*n fp64); on return the final phi starts at
+ * scratch + st->phi_offset.  Needs pdd_synthesize. */
+typedef struct {
+    int64_t sweeps;        /* Jacobi sweeps including the last (converged) one                 */
+    double residual;       /* change of the last sweep                                         */
+    double seconds;
+    int32_t converged;
+    int32_t overlap_nodes; /* free nodes in >= 2 patches Omega_p (phi_p >= tau_P)              */
+    int64_t phi_offset;    /* byte offset of the final phi fields inside scratch               */
+} pdd_fuzzy_stats;
+pdd_status pdd_fuzzy_scratch_bytes(int32_t n, int32_t n_patches, size_t *bytes);
+pdd_status pdd_build_fuzzy_patches(pdd_ctx *ctx, int32_t n_patches, double eps_P, double tau_P,
+                                   int64_t max_sweeps, void *scratch, size_t scratch_bytes,
+                                   pdd_fuzzy_stats *st);
 
 /* Static equal squares: px columns x py rows, boundaries floor(k n / P) (R19). */
 pdd_status pdd_build_static(pdd_ctx *ctx, int32_t px, int32_t py);

@@ -94,6 +94,11 @@ def lib():
         L.orc_uhat_at.argtypes = [C.c_int, C.c_int, dp, ip, C.c_int64, dp]
         L.orc_static_labels.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_uint8),
                                         C.POINTER(C.c_int16)]
+        L.orc_fuzzy_phi.argtypes = [P, C.POINTER(C.c_uint8), C.POINTER(C.c_int32), C.c_int,
+                                    C.c_double, C.c_int64, dp, dp]
+        L.orc_fuzzy_phi.restype = C.c_int64
+        L.orc_fuzzy_assign.argtypes = [P, dp, C.c_int, C.c_double, C.POINTER(C.c_int16),
+                                       C.POINTER(C.c_uint8)]
         _lib = L
     return _lib
 
@@ -350,3 +355,31 @@ def solve_pipeline(inst, tol: Optional[float] = None, fine: bool = True,
         out["V"], out["sweeps"], out["residual"] = fs["V"], fs["sweeps"], fs["residual"]
     out["threads"] = num_threads()
     return out
+
+
+def fuzzy_phi(inst, astar: np.ndarray, n_patches: int, eps_P: float, max_sweeps: int = 10**6):
+    """phi_p of the paper's fuzzy patches: Jacobi of the SL advection scheme along the
+    synthesised field until the sweep change is < eps_P.  Returns dict(phi (n_patches, N),
+    sweeps, residual)."""
+    P = Problem(inst)
+    N = inst.n * inst.n
+    a = np.ascontiguousarray(astar, dtype=np.uint8)
+    sec = np.ascontiguousarray(inst.sector, dtype=np.int32)
+    phi = np.empty(n_patches * N, dtype=np.float64)
+    res = C.c_double(0.0)
+    sw = lib().orc_fuzzy_phi(P.ref, _ptr(a, C.c_uint8), _ptr(sec, C.c_int32), int(n_patches),
+                             float(eps_P), int(max_sweeps), _ptr(phi, C.c_double), C.byref(res))
+    return {"phi": phi.reshape(n_patches, N), "sweeps": int(sw), "residual": res.value}
+
+
+def fuzzy_assign(inst, phi: np.ndarray, tau_P: float):
+    """Thresholding / ownership of the fuzzy patches (R38): (labels, members)."""
+    P = Problem(inst)
+    phi = np.ascontiguousarray(phi, dtype=np.float64)
+    npatch = phi.shape[0]
+    N = inst.n * inst.n
+    lab = np.empty(N, dtype=np.int16)
+    mem = np.empty(N, dtype=np.uint8)
+    lib().orc_fuzzy_assign(P.ref, _ptr(phi.reshape(-1), C.c_double), int(npatch), float(tau_P),
+                           _ptr(lab, C.c_int16), _ptr(mem, C.c_uint8))
+    return lab, mem

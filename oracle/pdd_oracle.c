@@ -582,3 +582,93 @@ void orc_static_labels(int n, int px, int py, const uint8_t *kind, int16_t *labe
         }
     }
 }
+
+/* Fuzzy patches of the paper (reading R38).
+ * phi_p = chi_{Gamma_p} on the Dirichlet set (target node of sector p: 1, any other Dirichlet
+ * node: 0), 0 on free nodes; then the semi-Lagrangian advection scheme Eq. (discrete-advection)
+ *     phi_p(x_i) = phi_p(x_i + h f(x_i, a*(x_i)))        (bilinear, sigma = 0 foot, clamped)
+ * iterated for all p at once by Jacobi (every node from the previous iterate) until the sup-norm
+ * change of a sweep is < eps_P (the paper's "poor tolerance"); the count includes that sweep.
+ * Canonical arithmetic (R30): the foot is the synthesis foot f = c a + d, g = i + q f, and the
+ * value w00 v00 + w10 v10 + w01 v01 + w11 v11 summed in that order.  phi: n_patches * N
+ * (patch-major).  Returns the number of sweeps (max_sweeps if not converged). */
+int64_t orc_fuzzy_phi(const orc_problem *P, const uint8_t *astar, const int32_t *sector,
+                      int n_patches, double eps_P, int64_t max_sweeps, double *phi,
+                      double *residual_out)
+{
+    const int n = P->n;
+    const int64_t N = (int64_t)n * n;
+    const double q = P->h / P->dx;
+    double *cur = phi;
+    double *nxt = (double *)malloc(sizeof(double) * (size_t)N * (size_t)n_patches);
+    for (int p = 0; p < n_patches; ++p)
+        for (int64_t k = 0; k < N; ++k)
+            cur[(int64_t)p * N + k] = (P->kind[k] == 1 && sector[k] == p) ? 1.0 : 0.0;
+    int64_t s = 0;
+    double res = INFINITY;
+    while (s < max_sweeps) {
+        res = 0.0;
+#pragma omp parallel for schedule(static) reduction(max : res)
+        for (int j = 0; j < n; ++j)
+            for (int i = 0; i < n; ++i) {
+                const int64_t k = (int64_t)j * n + i;
+                if (P->kind[k] != 0) {
+                    for (int p = 0; p < n_patches; ++p) nxt[(int64_t)p * N + k] = cur[(int64_t)p * N + k];
+                    continue;
+                }
+                const int a = astar[k];
+                const double c = coef_at(&P->speed, i, j, n);
+                const double f1 = c * P->ctrl[2 * a] + coef_at(&P->drift[0], i, j, n);
+                const double f2 = c * P->ctrl[2 * a + 1] + coef_at(&P->drift[1], i, j, n);
+                int64_t cr[4];
+                double wg[4];
+                bilinear_stencil(n, (double)i + q * f1, (double)j + q * f2, cr, wg);
+                for (int p = 0; p < n_patches; ++p) {
+                    const double *F = cur + (int64_t)p * N;
+                    double v = wg[0] * F[cr[0]];
+                    v = v + wg[1] * F[cr[1]];
+                    v = v + wg[2] * F[cr[2]];
+                    v = v + wg[3] * F[cr[3]];
+                    nxt[(int64_t)p * N + k] = v;
+                    const double d = fabs(v - F[k]);
+                    if (d > res) res = d;
+                }
+            }
+        double *t = cur; cur = nxt; nxt = t;
+        ++s;
+        if (res < eps_P) break;
+    }
+    if (cur != phi) {
+        memcpy(phi, cur, sizeof(double) * (size_t)N * (size_t)n_patches);
+        nxt = cur;
+    }
+    free(nxt);
+    if (residual_out) *residual_out = res;
+    return s;
+}
+
+/* Thresholding and ownership (reading R38): Omega_p = {phi_p >= tau_P}; the owner of
+ * a free node is the patch of largest phi_p (lowest p on ties) -- it is a member of Omega_p
+ * whenever any patch is; no positive phi_p at all -> orphan label n_patches.  Target -1,
+ * obstacle -2.  members (optional): number of patches with phi_p >= tau_P (overlap degree). */
+void orc_fuzzy_assign(const orc_problem *P, const double *phi, int n_patches, double tau_P,
+                      int16_t *labels, uint8_t *members)
+{
+    const int64_t N = (int64_t)P->n * P->n;
+    for (int64_t k = 0; k < N; ++k) {
+        if (P->kind[k] != 0) {
+            labels[k] = P->kind[k] == 1 ? -1 : -2;
+            if (members) members[k] = 0;
+            continue;
+        }
+        int best = -1, cnt = 0;
+        double bv = 0.0;
+        for (int p = 0; p < n_patches; ++p) {
+            const double v = phi[(int64_t)p * N + k];
+            if (v >= tau_P) ++cnt;
+            if (v > bv) { bv = v; best = p; }
+        }
+        labels[k] = (int16_t)(best < 0 ? n_patches : best);
+        if (members) members[k] = (uint8_t)(cnt > 255 ? 255 : cnt);
+    }
+}

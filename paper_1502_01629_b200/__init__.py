@@ -167,6 +167,29 @@ class Solver:
     def build_patches(self, n_patches: int, M: float = 4.0) -> None:
         self._ck(N.lib().pdd_build_patches(self._ctx, int(n_patches), float(M)))
 
+    def build_fuzzy_patches(self, n_patches: int, eps_P: float = 1e-3, tau_P: float = 0.5,
+                            max_sweeps: int = 1 << 20, return_phi: bool = False) -> dict:
+        """The paper's fuzzy patches: phi_p advected along the feedback until the
+        sweep change is < eps_P, thresholded at tau_P (owner = largest phi_p).  The device
+        scratch (two n_patches x n^2 fp64 fields) is a torch tensor owned here."""
+        import torch
+        nb = C.c_size_t(0)
+        _check(N.lib().pdd_fuzzy_scratch_bytes(int(self.n), int(n_patches), C.byref(nb)), None)
+        scratch = torch.empty(int(nb.value), dtype=torch.uint8, device=self.device)
+        st = N.pdd_fuzzy_stats()
+        self._ck(N.lib().pdd_build_fuzzy_patches(self._ctx, int(n_patches), float(eps_P),
+                                                 float(tau_P), int(max_sweeps),
+                                                 C.c_void_p(scratch.data_ptr()), int(nb.value),
+                                                 C.byref(st)))
+        out = st.as_dict()
+        if return_phi:
+            nn = self.n * self.n
+            off = int(st.phi_offset)
+            out["phi"] = scratch[off:off + 8 * nn * int(n_patches)].view(torch.float64) \
+                .reshape(int(n_patches), nn).cpu().numpy()
+        del scratch
+        return out
+
     def build_static(self, px: int, py: int) -> None:
         self._ck(N.lib().pdd_build_static(self._ctx, int(px), int(py)))
 
@@ -176,8 +199,8 @@ class Solver:
               early_exit: bool = True, bucket_policy: int = 0) -> dict:
         o = N.pdd_solve_opts()
         o.mode = MODE_PATCHY if mode in ("patchy", 0) else MODE_STATIC
-        if k_inner is None:   # sweeps per tile visit: measured best per mode
-            k_inner = 1 if o.mode == MODE_PATCHY else 4
+        if k_inner is None:   # 0 = automatic in libpdd: 1 patchy / 4 static,
+            k_inner = 0       # 4 for a patchy grid that fits one wave of sweep CTAs
         o.k_inner, o.tol, o.max_rounds, o.delta, o.kernel = int(k_inner), float(tol), int(max_rounds), float(delta), int(kernel)
         o.schedule = 1 if schedule in ("ordered", 1) else 0
         o.reserved[0] = 0 if early_exit else 1

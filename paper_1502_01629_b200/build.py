@@ -39,8 +39,9 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str = Non
     lib = out or LIB
     bdir = os.path.dirname(os.path.abspath(lib)) if out else BUILD
     os.makedirs(bdir, exist_ok=True)
-    srcs = [os.path.join(CSRC, u) for u in UNITS] + [os.path.join(CSRC, "pdd_internal.cuh"),
-                                                     os.path.join(ROOT, "include", "pdd.h")]
+    # every source and header of the library (an edit to any of them triggers a rebuild)
+    srcs = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(ROOT, "include", "pdd.h"),
+                                                                os.path.abspath(__file__)]
     newest = max(os.path.getmtime(s) for s in srcs)
     if not force and os.path.exists(lib) and os.path.getmtime(lib) >= newest:
         return lib

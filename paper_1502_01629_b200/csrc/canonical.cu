@@ -97,6 +97,68 @@ __device__ double canon_node_update(const DProblem &P, const double *V, int i, i
     return best;
 }
 
+// Row-invariant part of the coarse update when every coefficient depends on x2 only (C2, C4, C5):
+// per (row j, control a) the x offset q f1, the clamped y cell / fraction and h l(x, a), computed
+// with exactly the operations (and order) of canon_node_update -- the table only hoists them out
+// of the node loop, so the sweep stays bit-identical.
+__global__ void k_coarse_rowtab(DProblem P, CoarseRowEntry *tab)
+{
+    const int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (id >= (int64_t)P.n * P.na) return;
+    const int n = P.n;
+    const int j = (int)(id / P.na), a = (int)(id % P.na);
+    const double c = coef_at(P.speed, 0, j, n);
+    const double f1 = DADD(DMUL(c, P.ctrl[2 * a]), coef_at(P.drift[0], 0, j, n));
+    const double f2 = DADD(DMUL(c, P.ctrl[2 * a + 1]), coef_at(P.drift[1], 0, j, n));
+    CoarseRowEntry e;
+    e.bxq = DMUL(P.q, f1);
+    double gy = DADD((double)j, DMUL(P.q, f2));
+    const double top = (double)(n - 1);
+    if (gy < 0.0) gy = 0.0;
+    if (gy > top) gy = top;
+    int cy = (int)floor(gy);
+    if (cy > n - 2) cy = n - 2;
+    e.ty = DSUB(gy, (double)cy);
+    e.uy = DSUB(1.0, e.ty);
+    const double l = coef_at(P.cost, 0, j, n);
+    e.hl = DMUL(P.h, P.cost_ctrl ? DADD(l, P.cost_ctrl[a]) : l);
+    e.cy = cy;
+    e.pad = 0;
+    tab[id] = e;
+}
+
+// canon_node_update with the row-invariant table (same operations on every node)
+__device__ double canon_node_update_rt(const DProblem &P, const double *V, int i, int j,
+                                       const CoarseRowEntry *__restrict__ row)
+{
+    const int n = P.n;
+    const int64_t self = (int64_t)j * n + i;
+    const double top = (double)(n - 1);
+    double best = INFINITY;
+    for (int a = 0; a < P.na; ++a) {
+        const CoarseRowEntry e = row[a];
+        double gx = DADD((double)i, e.bxq);
+        if (gx < 0.0) gx = 0.0;
+        if (gx > top) gx = top;
+        int cx = (int)floor(gx);
+        if (cx > n - 2) cx = n - 2;
+        const double tx = DSUB(gx, (double)cx);
+        const double ux = DSUB(1.0, tx);
+        const double wg[4] = {DMUL(ux, e.uy), DMUL(tx, e.uy), DMUL(ux, e.ty), DMUL(tx, e.ty)};
+        const int64_t c0 = (int64_t)e.cy * n + cx;
+        const int64_t cr[4] = {c0, c0 + 1, c0 + n, c0 + n + 1};
+        double lam0 = 0.0, rp = 0.0;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            if (cr[t] == self) lam0 = DADD(lam0, wg[t]);
+            else rp = DADD(rp, DMUL(wg[t], V[cr[t]]));
+        }
+        const double v = DDIV(DADD(e.hl, DMUL(P.beta, rp)), DSUB(1.0, DMUL(P.beta, lam0)));
+        if (v < best) best = v;
+    }
+    return best;
+}
+
 __global__ void k_coarse_sweep(DProblem P, const double *__restrict__ Vin, double *__restrict__ Vout,
                                double tol, unsigned long long *res_hist, int sweep,
                                int *sweeps_done)
@@ -133,7 +195,7 @@ constexpr int CT = 16;
 __global__ void __launch_bounds__(CT * CT) k_coarse_sweep_tiles(
     DProblem P, const double *__restrict__ Vin, double *__restrict__ Vout, double tol,
     unsigned long long *res_hist, int sweep, int *sweeps_done, const uint8_t *fprev,
-    uint8_t *fout, int tiles_x)
+    uint8_t *fout, int tiles_x, const CoarseRowEntry *rowtab)
 {
     if (sweep > 0 && __longlong_as_double((long long)res_hist[sweep - 1]) < tol) return;
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(sweeps_done, 1);
@@ -163,7 +225,8 @@ __global__ void __launch_bounds__(CT * CT) k_coarse_sweep_tiles(
         if (!s_act || P.kind[k] != 0) {
             Vout[k] = vin;
         } else {
-            const double v = canon_node_update(P, Vin, i, j);
+            const double v = rowtab ? canon_node_update_rt(P, Vin, i, j, rowtab + (int64_t)j * P.na)
+                                    : canon_node_update(P, Vin, i, j);
             Vout[k] = v;
             res = fabs(DSUB(v, vin));
             changed = __double_as_longlong(v) != __double_as_longlong(vin);
@@ -230,6 +293,86 @@ __global__ void k_synthesize(DProblem P, const double *__restrict__ uhat, uint8_
         }
         astar[k] = (uint8_t)arg;
     }
+}
+
+// ------------------------------------------------------------------ fuzzy patches (NEXT #2)
+// phi_p = chi_{Gamma_p} on the Dirichlet set, 0 on free nodes; patch-major layout.
+__global__ void k_fuzzy_init(DProblem P, const int16_t *__restrict__ sector, int np, double *phi)
+{
+    const int64_t N = (int64_t)P.n * P.n;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < N;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const int sp = P.kind[k] == 1 ? sector[k] : -1;
+        for (int p = 0; p < np; ++p) phi[(int64_t)p * N + k] = sp == p ? 1.0 : 0.0;
+    }
+}
+
+// One Jacobi sweep of the SL advection scheme phi_p(x_i) = phi_p(x_i + h f(x_i, a*(x_i)))
+// (Eq. discrete-advection) for every patch, canonical fp64 (the synthesis foot,
+// corner sums in the order 00, 10, 01, 11); self-stopping once the previous sweep's change was
+// < eps (same protocol as k_coarse_sweep).
+__global__ void k_fuzzy_sweep(DProblem P, const uint8_t *__restrict__ astar, int np,
+                              const double *__restrict__ cur, double *__restrict__ nxt, double eps,
+                              unsigned long long *res_hist, int sweep, int *sweeps_done)
+{
+    if (sweep > 0 && __longlong_as_double((long long)res_hist[sweep - 1]) < eps) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(sweeps_done, 1);
+    const int n = P.n;
+    const int64_t N = (int64_t)n * n;
+    double res = 0.0;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < N;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        if (P.kind[k] != 0) {
+            for (int p = 0; p < np; ++p) nxt[(int64_t)p * N + k] = cur[(int64_t)p * N + k];
+            continue;
+        }
+        const int i = (int)(k % n), j = (int)(k / n);
+        const int a = astar[k];
+        const double c = coef_at(P.speed, i, j, n);
+        const double f1 = DADD(DMUL(c, P.ctrl[2 * a]), coef_at(P.drift[0], i, j, n));
+        const double f2 = DADD(DMUL(c, P.ctrl[2 * a + 1]), coef_at(P.drift[1], i, j, n));
+        int64_t cr[4];
+        double wg[4];
+        canon_stencil(n, DADD((double)i, DMUL(P.q, f1)), DADD((double)j, DMUL(P.q, f2)), cr, wg);
+        for (int p = 0; p < np; ++p) {
+            const double *F = cur + (int64_t)p * N;
+            double v = DMUL(wg[0], F[cr[0]]);
+            v = DADD(v, DMUL(wg[1], F[cr[1]]));
+            v = DADD(v, DMUL(wg[2], F[cr[2]]));
+            v = DADD(v, DMUL(wg[3], F[cr[3]]));
+            nxt[(int64_t)p * N + k] = v;
+            res = fmax(res, fabs(DSUB(v, F[k])));
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) res = fmax(res, __shfl_xor_sync(0xffffffffu, res, o));
+    if ((threadIdx.x & 31) == 0 && res > 0.0)
+        atomicMax(&res_hist[sweep], (unsigned long long)__double_as_longlong(res));
+}
+
+// Thresholding / ownership (R38): owner = the patch of largest phi_p (lowest p on
+// ties; it belongs to Omega_p = {phi_p >= tau} whenever any patch does), orphan n_patches when no
+// phi_p is positive; members = number of patches with phi_p >= tau (overlap degree).
+__global__ void k_fuzzy_assign(DProblem P, const double *__restrict__ phi, int np, double tau,
+                               int16_t *__restrict__ labels, int *overlap)
+{
+    const int64_t N = (int64_t)P.n * P.n;
+    int ov = 0;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < N;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const uint8_t kd = P.kind[k];
+        if (kd != 0) { labels[k] = kd == 1 ? -1 : -2; continue; }
+        int best = -1, cnt = 0;
+        double bv = 0.0;
+        for (int p = 0; p < np; ++p) {
+            const double v = phi[(int64_t)p * N + k];
+            if (v >= tau) ++cnt;
+            if (v > bv) { bv = v; best = p; }
+        }
+        labels[k] = (int16_t)(best < 0 ? np : best);
+        ov += cnt >= 2;
+    }
+    for (int o = 16; o > 0; o >>= 1) ov += __shfl_xor_sync(0xffffffffu, ov, o);
+    if ((threadIdx.x & 31) == 0 && ov) atomicAdd(overlap, ov);
 }
 
 __global__ void k_successor(DProblem P, double M, const uint8_t *__restrict__ astar,
@@ -327,14 +470,43 @@ void launch_coarse_sweep(const DProblem &P, const double *Vin, double *Vout, dou
 
 void launch_coarse_sweep_tiles(const DProblem &P, const double *Vin, double *Vout, double tol,
                                unsigned long long *res_hist, int sweep, int *sweeps_done,
-                               const uint8_t *fprev, uint8_t *fout, cudaStream_t s)
+                               const uint8_t *fprev, uint8_t *fout, const CoarseRowEntry *rowtab,
+                               cudaStream_t s)
 {
     const int tx = (P.n + CT - 1) / CT;
     k_coarse_sweep_tiles<<<tx * tx, CT * CT, 0, s>>>(P, Vin, Vout, tol, res_hist, sweep,
-                                                     sweeps_done, fprev, fout, tx);
+                                                     sweeps_done, fprev, fout, tx, rowtab);
+}
+
+void launch_coarse_rowtab(const DProblem &P, CoarseRowEntry *tab, cudaStream_t s)
+{
+    const int64_t m = (int64_t)P.n * P.na;
+    k_coarse_rowtab<<<grid_for(m, 128), 128, 0, s>>>(P, tab);
 }
 
 int coarse_tile() { return CT; }
+
+void launch_fuzzy_init(const DProblem &P, const int16_t *sector, int np, double *phi, cudaStream_t s)
+{
+    const int64_t N = (int64_t)P.n * P.n;
+    k_fuzzy_init<<<grid_for(N, 256), 256, 0, s>>>(P, sector, np, phi);
+}
+
+void launch_fuzzy_sweep(const DProblem &P, const uint8_t *astar, int np, const double *cur,
+                        double *nxt, double eps, unsigned long long *res_hist, int sweep,
+                        int *sweeps_done, cudaStream_t s)
+{
+    const int64_t N = (int64_t)P.n * P.n;
+    k_fuzzy_sweep<<<grid_for(N, 128), 128, 0, s>>>(P, astar, np, cur, nxt, eps, res_hist, sweep,
+                                                    sweeps_done);
+}
+
+void launch_fuzzy_assign(const DProblem &P, const double *phi, int np, double tau, int16_t *labels,
+                         int *overlap, cudaStream_t s)
+{
+    const int64_t N = (int64_t)P.n * P.n;
+    k_fuzzy_assign<<<grid_for(N, 256), 256, 0, s>>>(P, phi, np, tau, labels, overlap);
+}
 
 void launch_prolong(int nc, const double *uc, int n, double *out, cudaStream_t s)
 {

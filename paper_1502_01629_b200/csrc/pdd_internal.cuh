@@ -67,11 +67,28 @@ void launch_init_values(const DProblem &P, double *V, cudaStream_t s);
 void launch_coarse_sweep(const DProblem &P, const double *Vin, double *Vout, double tol,
                          unsigned long long *res_hist, int sweep, int *sweeps_done,
                          cudaStream_t s);
-// active-tile form of the same sweep (bit-identical; fprev/fout: per-tile change flags)
+// row-invariant part of the coarse node update (row-uniform coefficients), per (row, control)
+struct CoarseRowEntry {
+    double bxq;      // q f1
+    double ty, uy;   // clamped y fraction and 1 - ty
+    double hl;       // h l(x, a)
+    int cy, pad;     // y cell
+};
+void launch_coarse_rowtab(const DProblem &P, CoarseRowEntry *tab, cudaStream_t s);
+// active-tile form of the same sweep (bit-identical; fprev/fout: per-tile change flags; rowtab:
+// the row-invariant table or NULL)
 void launch_coarse_sweep_tiles(const DProblem &P, const double *Vin, double *Vout, double tol,
                                unsigned long long *res_hist, int sweep, int *sweeps_done,
-                               const uint8_t *fprev, uint8_t *fout, cudaStream_t s);
+                               const uint8_t *fprev, uint8_t *fout, const CoarseRowEntry *rowtab,
+                               cudaStream_t s);
 int coarse_tile();
+// fuzzy patches: phi_p init, one Jacobi advection sweep, thresholding
+void launch_fuzzy_init(const DProblem &P, const int16_t *sector, int np, double *phi, cudaStream_t s);
+void launch_fuzzy_sweep(const DProblem &P, const uint8_t *astar, int np, const double *cur,
+                        double *nxt, double eps, unsigned long long *res_hist, int sweep,
+                        int *sweeps_done, cudaStream_t s);
+void launch_fuzzy_assign(const DProblem &P, const double *phi, int np, double tau, int16_t *labels,
+                         int *overlap, cudaStream_t s);
 void launch_prolong(int nc, const double *uc, int n, double *out, cudaStream_t s);
 void launch_synthesize(const DProblem &P, const double *uhat, uint8_t *astar, cudaStream_t s);
 void launch_successor(const DProblem &P, double M, const uint8_t *astar, int32_t *succ,
@@ -197,6 +214,8 @@ struct SweepLaunch {
     ActCounters *acnt = nullptr;         //   the activation counters, stamps tile_chg
     int32_t *tile_stamp = nullptr;
     int32_t *tile_sweeps = nullptr;      // orientation schedule continues across visits
+    int *occupancy_out = nullptr;        // != NULL: report the device-driven kernel's resident
+                                         //   CTAs per SM and launch nothing
 };
 
 // device-driven round kernels (one thread each) around the activation and the sweep

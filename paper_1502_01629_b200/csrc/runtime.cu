@@ -113,6 +113,8 @@ struct pdd_ctx {
     float *f32buf = nullptr;
     unsigned long long *res_hist = nullptr;
     uint8_t *cflag = nullptr;   // coarse active-tile change flags, 2 x tiles
+    CoarseRowEntry *crowtab = nullptr;   // coarse row-invariant table (n_c x N_A)
+    bool coarse_rowuniform = false;
     bool coarse_tiled = false;  // coarse reach < tile: active-tile sweeps
     int *dev_int = nullptr;     // [0] sweeps_done, [1] jump changed flag
     void *rowtab = nullptr;
@@ -304,6 +306,7 @@ static size_t layout(pdd_ctx *c, void *ws, const pdd_problem *f, const pdd_probl
     unsigned long long *rh = cp ? cv.take<unsigned long long>(kMaxCoarseSweeps) : nullptr;
     const int ctn = cp ? (cp->n + coarse_tile() - 1) / coarse_tile() : 0;
     uint8_t *cflag = cp ? cv.take<uint8_t>(2 * (size_t)ctn * ctn) : nullptr;
+    CoarseRowEntry *crt = cp ? cv.take<CoarseRowEntry>((size_t)cp->n * cp->n_controls) : nullptr;
     uint8_t *astar = cv.take<uint8_t>(N);
     int16_t *labels = cv.take<int16_t>(N);
     int32_t *s0 = cp ? cv.take<int32_t>(N) : nullptr;
@@ -347,6 +350,7 @@ static size_t layout(pdd_ctx *c, void *ws, const pdd_problem *f, const pdd_probl
         c->uc[1] = uc1;
         c->res_hist = rh;
         c->cflag = cflag;
+        c->crowtab = crt;
         c->astar = astar;
         c->labels = labels;
         c->succ0 = s0;
@@ -434,6 +438,11 @@ pdd_status pdd_create(const pdd_problem *fine, const pdd_problem *coarse, int32_
     // active-tile coarse sweeps need the stencil reach (+ the bilinear corner) inside one tile
     // (computed here: the host arrays of the problem are valid only during this call)
     ctx->coarse_tiled = coarse && reach_cells(coarse) + 2.0 < (double)coarse_tile();
+    if (coarse) {
+        auto rok = [](const pdd_coef &c) { return c.kind == PDD_COEF_CONST || c.kind == PDD_COEF_ROW; };
+        ctx->coarse_rowuniform = rok(coarse->speed) && rok(coarse->drift[0]) && rok(coarse->drift[1]) &&
+                                 rok(coarse->cost);
+    }
     // aligned base
     char *base = (char *)workspace;
     const size_t mis = (size_t)((uintptr_t)base % kAlign);
@@ -502,6 +511,11 @@ pdd_status pdd_coarse_solve(pdd_ctx *ctx, double tol_c, int64_t max_sweeps, pdd_
     bool converged = false;
     int64_t batch = 8;
     const bool tiled = ctx->coarse_tiled && !std::getenv("PDD_COARSE_FULL");   // env: A/B only
+    const bool use_rt = tiled && ctx->coarse_rowuniform && !std::getenv("PDD_COARSE_NORT");
+    if (use_rt) {
+        launch_coarse_rowtab(Pc, ctx->crowtab, s);
+        ctx->launches++;
+    }
     while (issued < max_sweeps) {
         const int64_t b = std::min<int64_t>(batch, max_sweeps - issued);
         const size_t ctn = (size_t)((Pc.n + coarse_tile() - 1) / coarse_tile());
@@ -510,7 +524,8 @@ pdd_status pdd_coarse_solve(pdd_ctx *ctx, double tol_c, int64_t max_sweeps, pdd_
                 launch_coarse_sweep_tiles(Pc, ctx->uc[issued & 1], ctx->uc[(issued + 1) & 1], tol_c,
                                           ctx->res_hist, (int)issued, ctx->dev_int,
                                           ctx->cflag + ((issued + 1) & 1) * ctn * ctn,
-                                          ctx->cflag + (issued & 1) * ctn * ctn, s);
+                                          ctx->cflag + (issued & 1) * ctn * ctn,
+                                          use_rt ? ctx->crowtab : nullptr, s);
             else
                 launch_coarse_sweep(Pc, ctx->uc[issued & 1], ctx->uc[(issued + 1) & 1], tol_c,
                                     ctx->res_hist, (int)issued, ctx->dev_int, s);
@@ -602,6 +617,93 @@ pdd_status pdd_build_patches(pdd_ctx *ctx, int32_t n_patches, double M)
     ctx->n_patches = n_patches;
     ctx->prepared_kernel = -1;
     return PDD_OK;
+}
+
+pdd_status pdd_fuzzy_scratch_bytes(int32_t n, int32_t n_patches, size_t *bytes)
+{
+    if (!bytes) return fail(nullptr, PDD_E_INVALID, "bytes is NULL");
+    if (n < 3 || n_patches < 1 || n_patches >= kMaxPatches)
+        return fail(nullptr, PDD_E_INVALID, "fuzzy scratch: n >= 3 and 1 <= n_patches < %d", kMaxPatches);
+    *bytes = 2 * sizeof(double) * (size_t)n_patches * (size_t)n * (size_t)n + 256;
+    return PDD_OK;
+}
+
+pdd_status pdd_build_fuzzy_patches(pdd_ctx *ctx, int32_t n_patches, double eps_P, double tau_P,
+                                   int64_t max_sweeps, void *scratch, size_t scratch_bytes,
+                                   pdd_fuzzy_stats *st)
+{
+    if (!ctx) return fail(nullptr, PDD_E_INVALID, "ctx is NULL");
+    if (!ctx->synth_done) return fail(ctx, PDD_E_STATE, "pdd_build_fuzzy_patches needs pdd_synthesize first");
+    if (n_patches < 1 || n_patches >= kMaxPatches)
+        return fail(ctx, PDD_E_INVALID, "n_patches must be in 1..%d", kMaxPatches - 1);
+    if (!ctx->F.sector) return fail(ctx, PDD_E_INVALID, "the fine problem has no sector table");
+    if (!(eps_P > 0.0) || !(tau_P > 0.0 && tau_P < 1.0))
+        return fail(ctx, PDD_E_INVALID, "need eps_P > 0 and 0 < tau_P < 1");
+    if (max_sweeps <= 0 || max_sweeps > kMaxCoarseSweeps)
+        return fail(ctx, PDD_E_INVALID, "max_sweeps must be in 1..%lld", (long long)kMaxCoarseSweeps);
+    size_t need = 0;
+    pdd_status ps = pdd_fuzzy_scratch_bytes(ctx->fine.n, n_patches, &need);
+    if (ps != PDD_OK) return ps;
+    if (!scratch || scratch_bytes < need)
+        return fail(ctx, PDD_E_NOMEM, "fuzzy scratch needs %zu bytes", need);
+    cudaStream_t s = ctx->stream;
+    const int64_t N = (int64_t)ctx->fine.n * ctx->fine.n;
+    char *b = (char *)scratch;
+    const size_t mis = (size_t)((uintptr_t)b % 256);
+    if (mis) b += 256 - mis;
+    double *phi[2] = {reinterpret_cast<double *>(b), reinterpret_cast<double *>(b) + (size_t)n_patches * N};
+    CK(cudaEventRecord(ctx->ev[0], s));
+    launch_fuzzy_init(ctx->F.d, ctx->F.sector, n_patches, phi[0], s);
+    CK(cudaMemsetAsync(ctx->res_hist, 0, sizeof(unsigned long long) * max_sweeps, s));
+    CK(cudaMemsetAsync(ctx->dev_int, 0, 2 * sizeof(int), s));
+    ctx->launches++;
+    int64_t issued = 0, batch = 8;
+    int done = 0;
+    bool converged = false;
+    while (issued < max_sweeps) {
+        const int64_t nb = std::min<int64_t>(batch, max_sweeps - issued);
+        for (int64_t q = 0; q < nb; ++q, ++issued)
+            launch_fuzzy_sweep(ctx->F.d, ctx->astar, n_patches, phi[issued & 1], phi[(issued + 1) & 1],
+                               eps_P, ctx->res_hist, (int)issued, ctx->dev_int, s);
+        ctx->launches += nb;
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(ctx->h_int, ctx->dev_int, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        done = ctx->h_int[0];
+        if (done < issued) { converged = true; break; }
+        unsigned long long last = 0;
+        CK(cudaMemcpy(&last, ctx->res_hist + (issued - 1), sizeof last, cudaMemcpyDeviceToHost));
+        double lr;
+        std::memcpy(&lr, &last, sizeof lr);
+        if (lr < eps_P) { converged = true; break; }
+        batch = std::min<int64_t>(batch * 2, 256);
+    }
+    const double *fin = phi[done & 1];
+    CK(cudaMemsetAsync(ctx->dev_int + 1, 0, sizeof(int), s));
+    launch_fuzzy_assign(ctx->F.d, fin, n_patches, tau_P, ctx->labels, ctx->dev_int + 1, s);
+    ctx->launches++;
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(ctx->ev[1], s));
+    CK(cudaMemcpyAsync(ctx->h_int + 1, ctx->dev_int + 1, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    ctx->labels_mode = 1;
+    ctx->n_patches = n_patches;
+    ctx->prepared_kernel = -1;
+    if (st) {
+        unsigned long long lastbits = 0;
+        if (done > 0)
+            CK(cudaMemcpy(&lastbits, ctx->res_hist + (done - 1), sizeof lastbits, cudaMemcpyDeviceToHost));
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]);
+        st->sweeps = done;
+        std::memcpy(&st->residual, &lastbits, sizeof(double));
+        st->seconds = ms * 1e-3;
+        st->converged = converged ? 1 : 0;
+        st->overlap_nodes = ctx->h_int[1];
+        st->phi_offset = (int64_t)((const char *)fin - (const char *)scratch);
+    }
+    return converged ? PDD_OK : fail(ctx, PDD_E_NOCONVERGE, "fuzzy patches: %lld sweeps without reaching eps_P",
+                                     (long long)done);
 }
 
 pdd_status pdd_build_static(pdd_ctx *ctx, int32_t px, int32_t py)
@@ -881,7 +983,7 @@ pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
     if (!ctx) return fail(nullptr, PDD_E_INVALID, "ctx is NULL");
     if (!o) return fail(ctx, PDD_E_INVALID, "opts is NULL");
     if (o->mode != 0 && o->mode != 1) return fail(ctx, PDD_E_INVALID, "mode must be 0 or 1");
-    if (o->k_inner < 1 || o->k_inner > 1024) return fail(ctx, PDD_E_INVALID, "k_inner outside 1..1024");
+    if (o->k_inner < 0 || o->k_inner > 1024) return fail(ctx, PDD_E_INVALID, "k_inner outside 0..1024");
     if (!(o->tol > 0.0)) return fail(ctx, PDD_E_INVALID, "tol must be > 0");
     if (o->mode == 0 && (!ctx->synth_done || ctx->labels_mode != 1))
         return fail(ctx, PDD_E_STATE, "patchy solve needs pdd_synthesize and pdd_build_patches");
@@ -924,7 +1026,31 @@ pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&resident, cudaDevAttrMultiProcessorCount, dev);
-        resident *= ctx->path == 3 ? 3 : 2;   // sweep CTAs resident per SM (launch_one's bounds)
+        // sweep CTAs resident per SM: the occupancy of the device-driven sweep kernel
+        SweepLaunch Q = make_launch(ctx, nullptr, 0, 1, 0, nullptr);
+        int per_sm = 1;
+        Q.occupancy_out = &per_sm;
+        CK(launch_sweep(Q, s));
+        resident *= std::max(1, per_sm);
+    }
+    // automatic settings (k_inner = 0, delta = 0): when every tile with free nodes fits in one
+    // wave of resident sweep CTAs, holding tiles back behind the u_hat front only adds rounds of
+    // one-visit latency (measured on the paper's 800^2 Zermelo / eikonal grids), so the patchy
+    // solve then admits every tile at once (u_hat start, downstream orientations) and every
+    // visit does up to 4 in-tile sweeps; otherwise 1 sweep per visit (patchy) / 4 (static)
+    int tiles_free = 0;
+    {
+        std::vector<int32_t> tf(ctx->n_tiles);
+        CK(cudaMemcpyAsync(tf.data(), ctx->T.tile_free, sizeof(int32_t) * tf.size(),
+                           cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        for (int32_t v : tf) tiles_free += v > 0;
+    }
+    const bool one_wave = tiles_free <= 2 * resident;   // "fits in (about) one wave": <= 2 waves
+    const int k_inner = o->k_inner > 0 ? o->k_inner : (o->mode == 0 && !one_wave ? 1 : 4);
+    if (o->mode == 0 && o->delta == 0.0 && one_wave && o->reserved[1] != 2) {
+        delta = -1.0;
+        thr = INFINITY;
     }
     if (o->mode == 0 && o->reserved[1] == 2) {
         ready_slack = o->delta > 0.0 ? o->delta : 0.25 * ctx->g.TH * ctx->fine.h * d.lmax;
@@ -975,7 +1101,7 @@ pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
     while (o->schedule != 1) {
         if (S.rounds >= o->max_rounds) break;
         CK(cudaEventRecord(ctx->ev[2], s));
-        SweepLaunch L = make_launch(ctx, ctx->T.list[cur], ctx->n_tiles, o->k_inner, 0, nullptr);
+        SweepLaunch L = make_launch(ctx, ctx->T.list[cur], ctx->n_tiles, k_inner, 0, nullptr);
         L.early_tol = o->reserved[0] ? 0.0 : o->tol;   // reserved[0] = 1 disables early exit
         L.ctl = ctx->rctl;
         L.acnt = reinterpret_cast<ActCounters *>(ctx->T.counters);

@@ -45,8 +45,12 @@ namespace pdd {
 
 // register cap per path: the GS row-table kernel (path 3) at 80 registers keeps 3 CTAs (24
 // warps) per SM without spills -- measured 1.6x faster than its unconstrained 137-register build
+#ifndef PDD_MIN_BLOCKS1
+#define PDD_MIN_BLOCKS1 2   // path 1 (general stencil) CTAs per SM bound (measured: C3 patchy
+                            // 0.124 -> 0.106 s, static 0.29 -> 0.22 s against 1 CTA/SM)
+#endif
 template <int PATH>
-constexpr int min_blocks() { return PDD_MIN_BLOCKS > 0 ? PDD_MIN_BLOCKS : (PATH == 3 ? 3 : 1); }
+constexpr int min_blocks() { return PDD_MIN_BLOCKS > 0 ? PDD_MIN_BLOCKS : (PATH == 3 ? 3 : PATH == 1 ? PDD_MIN_BLOCKS1 : 1); }
 #ifndef PDD_TH
 #define PDD_TH 32           // tile rows (multiple of NW)
 #endif
@@ -144,35 +148,79 @@ __device__ __forceinline__ float warp_min<float>(float v)
 }
 #endif
 
+// Per-node coefficients of the general stencil (values at node (gi, gj)); loaded from global
+// memory by node_coef.  The row-pipelined kernel prefetches them for a whole row at its start so
+// that no global load sits on the node-by-node dependency chain.
+template <typename real>
+struct NodeCoef {
+    real c, d1, d2, o[2][2], sa, D;
+};
+
+template <typename real>
+__device__ __forceinline__ NodeCoef<real> node_coef(const DProblem &P, int gi, int gj, real D,
+                                                    double Vref)
+{
+    const int n = P.n;
+    NodeCoef<real> r;
+    r.c = (real)coef_at(P.speed, gi, gj, n);
+    r.d1 = (real)coef_at(P.drift[0], gi, gj, n);
+    r.d2 = (real)coef_at(P.drift[1], gi, gj, n);
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        r.o[k][0] = k < P.p ? (real)(P.sc * coef_at(P.sigma[k][0], gi, gj, n)) : (real)0;
+        r.o[k][1] = k < P.p ? (real)(P.sc * coef_at(P.sigma[k][1], gi, gj, n)) : (real)0;
+    }
+    // sigma(x, a) = s(x) a (sigma_mode 1, R32): the single noise column follows the control
+    r.sa = P.sigma_mode == 1 ? (real)(P.sc * coef_at(P.sigma[0][0], gi, gj, n)) : (real)0;
+    // a running-cost field needs D = h l(x_i) - (1 - beta) V_ref per node (fp64 then rounded)
+    r.D = P.cost.kind != 0 ? (real)(P.h * coef_at(P.cost, gi, gj, n) - (1.0 - P.beta) * Vref) : D;
+    return r;
+}
+
+template <typename real>
+__device__ __forceinline__ real general_node_c(const DProblem &P, const real *__restrict__ s_ctrl,
+                                               const real *base, int pitch, int gi, int gj,
+                                               const NodeCoef<real> &nc);
+
 // General stencil at one node (lane = control).  base points at the node in shared memory.
 template <typename real>
 __device__ __forceinline__ real general_node(const DProblem &P, const real *__restrict__ s_ctrl,
                                           const real *base, int pitch, int gi, int gj, real D,
                                           double Vref)
 {
+    return general_node_c<real>(P, s_ctrl, base, pitch, gi, gj, node_coef<real>(P, gi, gj, D, Vref));
+}
+
+// Out-of-line form for the nodes with x-clamped feet of the row-table kernel (boundary tiles
+// only): keeps the general stencil's registers out of the 80-register row loop.
+template <typename real>
+__device__ __noinline__ real general_node_edge(const DProblem &P, const real *__restrict__ s_ctrl,
+                                               const real *base, int pitch, int gi, int gj, real D,
+                                               double Vref)
+{
+    return general_node<real>(P, s_ctrl, base, pitch, gi, gj, D, Vref);
+}
+
+template <typename real>
+__device__ __forceinline__ real general_node_c(const DProblem &P, const real *__restrict__ s_ctrl,
+                                               const real *base, int pitch, int gi, int gj,
+                                               const NodeCoef<real> &nc)
+{
     const int lane = threadIdx.x & 31;
     const int n = P.n;
-    const real c = (real)coef_at(P.speed, gi, gj, n);
-    const real d1 = (real)coef_at(P.drift[0], gi, gj, n);
-    const real d2 = (real)coef_at(P.drift[1], gi, gj, n);
+    const real c = nc.c, d1 = nc.d1, d2 = nc.d2;
     const int p = P.p;
     const int nb = p > 0 ? 2 * p : 1;
-    real off[2][2] = {{0, 0}, {0, 0}};
-    for (int k = 0; k < p; ++k) {
-        off[k][0] = (real)(P.sc * coef_at(P.sigma[k][0], gi, gj, n));
-        off[k][1] = (real)(P.sc * coef_at(P.sigma[k][1], gi, gj, n));
-    }
-    const real q = (real)P.q, beta = (real)P.beta;
+    real off[2][2] = {{nc.o[0][0], nc.o[0][1]}, {nc.o[1][0], nc.o[1][1]}};
+    const real q = (real)P.q;
     const real bw = (real)(P.beta / (double)nb);
     const real xlo = (real)(-gi), xhi = (real)(n - 1 - gi);
     const real ylo = (real)(-gj), yhi = (real)(n - 1 - gj);
     const real cxm = (real)(n - 2 - gi), cym = (real)(n - 2 - gj);
+    const real D = nc.D;
+    const real sa = nc.sa;
     const real uself = *base;
-    (void)beta;
-    // a running-cost field needs D = h l(x_i) - (1 - beta) V_ref per node (fp64 then rounded)
-    if (P.cost.kind != 0) D = (real)(P.h * coef_at(P.cost, gi, gj, n) - (1.0 - P.beta) * Vref);
-    // sigma(x, a) = s(x) a (sigma_mode 1, R32): the single noise column follows the control
-    const real sa = P.sigma_mode == 1 ? (real)(P.sc * coef_at(P.sigma[0][0], gi, gj, n)) : (real)0;
+    const bool big_self = rabs(uself) > (real)1e3;   // |u_self| >> any value difference of a tile
     real best = rinf<real>();
     for (int k = lane; k < P.na; k += 32) {
         const real bx = q * (c * s_ctrl[2 * k] + d1);
@@ -197,12 +245,26 @@ __device__ __forceinline__ real general_node(const DProblem &P, const real *__re
             const real fy = rmin(rfloor(yr), cym);
             const real tx = xr - fx, ty = yr - fy;
             const real *pc = base + (int)fy * pitch + (int)fx;
-            const real u00 = pc[0], u10 = pc[1], u01 = pc[pitch], u11 = pc[pitch + 1];
-            const real a0 = u00 + tx * (u10 - u00);
-            const real a1 = u01 + tx * (u11 - u01);
-            const real val = a0 + ty * (a1 - a0);
             const real ws = rmax((real)0, (real)1 - rabs(xr)) * rmax((real)0, (real)1 - rabs(yr));
-            R += val - ws * uself;
+            if (big_self) {
+                // the node's own corner enters with value 0 (its weight goes to Lambda0,
+                // P:433-436): excluding it, rather than subtracting ws u_self afterwards, keeps R
+                // exact when u_self is large (an exit problem's 1e6 start value next to the
+                // front, fp32); warp-uniform branch, taken only for such nodes
+                const int ix = (int)fx, iy = (int)fy;
+                const real u00 = (ix == 0 && iy == 0) ? (real)0 : pc[0];
+                const real u10 = (ix == -1 && iy == 0) ? (real)0 : pc[1];
+                const real u01 = (ix == 0 && iy == -1) ? (real)0 : pc[pitch];
+                const real u11 = (ix == -1 && iy == -1) ? (real)0 : pc[pitch + 1];
+                const real a0 = u00 + tx * (u10 - u00);
+                const real a1 = u01 + tx * (u11 - u01);
+                R += a0 + ty * (a1 - a0);
+            } else {
+                const real u00 = pc[0], u10 = pc[1], u01 = pc[pitch], u11 = pc[pitch + 1];
+                const real a0 = u00 + tx * (u10 - u00);
+                const real a1 = u01 + tx * (u11 - u01);
+                R += (a0 + ty * (a1 - a0)) - ws * uself;
+            }
             L0 += ws;
         }
         const real v = (Dk + bw * R) / ((real)1 - bw * L0);
@@ -340,6 +402,9 @@ __device__ __forceinline__ void row_table(const KP<real> &A, real *s_u, const re
     }
 }
 
+#ifndef PDD_BIGREF
+#define PDD_BIGREF 1     // V_ref = staged min on a tile whose values span > 1 + |min| (R39)
+#endif
 #ifndef PDD_GSG
 #define PDD_GSG 1    // path 1 (general stencil) uses the Gauss-Seidel tile sweeps of sweep_gs.cuh
 #endif
@@ -398,10 +463,23 @@ __device__ __forceinline__ void sweep_tile(const KP<real> &A, int t, unsigned ch
 #pragma unroll
         for (int w = 0; w < NW; ++w) Vref = fmin(Vref, s_red[w]);
     } else {
-        // the other paths compare with order-mapped keys / shuffles: the tile-centre value keeps
-        // |u| smallest (fp64 runs to r <= 1e-12 (1 - beta) sit at a few ulp of u)
+        // the tile-centre value keeps |u| smallest (fp64 runs to r <= 1e-12 (1 - beta) sit at a
+        // few ulp of u) -- except on a tile whose staged values span more than 1 + |min| (an exit
+        // problem's 1e6 start values, or values interpolated from them, next to the front, R39):
+        // then the smallest staged value, so that the nodes the front has reached keep full
+        // precision next to the placeholders
         const int ci = min(i0 + TW / 2, n - 1), cj = min(j0 + TH / 2, n - 1);
         Vref = __ldcg(A.V + (int64_t)cj * n + ci);
+        if (PDD_BIGREF) {
+            double vminb = s_red[0];
+#pragma unroll
+            for (int w = 1; w < NW; ++w) vminb = fmin(vminb, s_red[w]);
+            double vmax = -INFINITY;
+#pragma unroll
+            for (int m = 0; m < MAXE; ++m) vmax = fmax(vmax, vs[m] < INFINITY ? vs[m] : -INFINITY);
+            const int wide = __syncthreads_or(vmax - vminb > 1.0 + fabs(vminb));
+            if (wide) Vref = vminb;
+        }
     }
 #pragma unroll
     for (int m = 0; m < MAXE; ++m) {
@@ -645,7 +723,7 @@ static cudaError_t launch_one(const SweepLaunch &L, cudaStream_t s)
         kern<<<grid, NW * 32, smem, s>>>(A, L.order);
         return cudaGetLastError();
     }
-    if (L.ctl && !CHECK) {
+    if ((L.ctl || L.occupancy_out) && !CHECK) {
         auto kern = k_sweep_dyn<real, PATH, CPL, WY, WX>;
         static int per_sm = -1, sms = 0;    // per instantiation: occupancy is fixed
         if (per_sm < 0) {
@@ -660,6 +738,10 @@ static cudaError_t launch_one(const SweepLaunch &L, cudaStream_t s)
             cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NW * 32, smem);
             if (e != cudaSuccess) return e;
             per_sm = std::max(1, per_sm);
+        }
+        if (L.occupancy_out) {
+            *L.occupancy_out = per_sm;
+            return cudaSuccess;
         }
         int grid = per_sm * sms;
         if (grid > L.n_list) grid = L.n_list;     // n_list: upper bound of the count

@@ -81,11 +81,15 @@ constexpr int P3_HMAX = 4;
 // (saves 4 ALU ops per node, ~3 % on C5) -- off by default: |u| then spans the whole tile range
 // instead of half of it, and on coarse grids (tile value range ~1) the fp32 noise floor
 // (1 ulp of u = 1.2e-7) rises above a 1e-7 tolerance
+#ifndef PDD_EDGE_CALL
+#define PDD_EDGE_CALL 0   // 1: the general stencil as an out-of-line call (measured slower)
+#endif
+
 #ifndef PDD_RAWMIN
 #define PDD_RAWMIN 0
 #endif
 
-template <int CPL, int WY, int WX, bool CHECK, bool XNEG>
+template <int CPL, int WY, int WX, bool CHECK, bool XNEG, bool EDGE>
 __device__ __forceinline__ void row_gs4(const KP<float> &A, float *s_u, const float *s_ctrl,
                                         volatile int *s_prog, int pitch_rt, int cstride_rt, int H,
                                         int i0, int ly, int gj, int jj, int base, int lead,
@@ -142,8 +146,8 @@ __device__ __forceinline__ void row_gs4(const KP<float> &A, float *s_u, const fl
     unsigned skip16 = 0u;
 #pragma unroll
     for (int G = 0; G < NG; ++G) skip16 |= (unsigned)((skip >> (4 * G + nd)) & 1ull) << G;
-    const unsigned long long edge = emask & ~dmask;           // nodes needing the general stencil
     const unsigned prog_prev = (unsigned)__cvta_generic_to_shared((const void *)(s_prog + (jj > 0 ? jj - 1 : 0)));
+    const unsigned long long edge = EDGE ? (emask & ~dmask) : 0ull;
     for (int gs = 0; gs < NG; ++gs) {
         const int G = xneg ? NG - 1 - gs : gs;
         const int g = 4 * G;
@@ -225,17 +229,23 @@ __device__ __forceinline__ void row_gs4(const KP<float> &A, float *s_u, const fl
                 }
             }
         }
-        // nodes of this group whose feet may be clamped in x: general stencil (these sit
-        // within H of the domain's x-boundary; their in-group order is not enforced)
-        unsigned long long em = edge ? edge & (0xfull << g) : 0ull;
-        if (em) {
-            __syncwarp();
-            while (em) {
-                const int lx = __ffsll((long long)em) - 1;
-                em &= em - 1;
-                const float best = general_node<float>(A.P, s_ctrl, rowp + lx, pitch, i0 + lx, gj, D, Vref);
-                commit_node<float, CHECK, 4>(rowp + lx, best, last, res, A.out,
-                                             (int64_t)gj * n + i0 + lx, Vref, cstride);
+        // nodes of this group whose feet may be clamped in x (within H of the domain's x-boundary):
+        // general stencil, in the row pipeline so the next row sees them.  Only the tiles at the
+        // domain's x-boundary instantiate this (EDGE): the interior tiles' loop carries none of
+        // the general stencil's live ranges (0 spills at 80 registers)
+        if constexpr (EDGE) {
+            unsigned long long em = edge & (0xfull << g);
+            if (em) {
+                __syncwarp();
+                while (em) {
+                    const int lx = __ffsll((long long)em) - 1;
+                    em &= em - 1;
+                    const float best = PDD_EDGE_CALL
+                        ? general_node_edge<float>(A.P, s_ctrl, rowp + lx, pitch, i0 + lx, gj, D, Vref)
+                        : general_node<float>(A.P, s_ctrl, rowp + lx, pitch, i0 + lx, gj, D, Vref);
+                    commit_node<float, CHECK, 4>(rowp + lx, best, last, res, A.out,
+                                                 (int64_t)gj * n + i0 + lx, Vref, cstride);
+                }
             }
         }
         if (!CHECK) {
@@ -260,6 +270,7 @@ __device__ __forceinline__ int tile_gs4(const KP<float> &A, float *s_u, const fl
     const int lead = 1 + (3 + H) / 4;          // groups the previous row must be ahead
     const int sweeps = CHECK ? 1 : k_inner;
     double first = 0.0;                        // change of the visit's first sweep
+    const bool edge_tile = i0 < A.Hx || i0 + 64 > n - 1 - A.Hx;   // holds nodes with x-clamped feet
 
     for (int sw = 0; sw < sweeps; ++sw) {
         // every sweep tracks its residual: a tile that is converged w.r.t. its halo stops early
@@ -277,12 +288,21 @@ __device__ __forceinline__ int tile_gs4(const KP<float> &A, float *s_u, const fl
                 if (lane == 0) s_prog[jj] = base + NG;
                 continue;
             }
-            if (xneg)
-                row_gs4<CPL, WY, WX, CHECK, true>(A, s_u, s_ctrl, s_prog, pitch, cstride, H, i0, ly,
-                                                  gj, jj, base, lead, D, last, res, Vref);
-            else
-                row_gs4<CPL, WY, WX, CHECK, false>(A, s_u, s_ctrl, s_prog, pitch, cstride, H, i0, ly,
-                                                   gj, jj, base, lead, D, last, res, Vref);
+            if (edge_tile) {
+                if (xneg)
+                    row_gs4<CPL, WY, WX, CHECK, true, true>(A, s_u, s_ctrl, s_prog, pitch, cstride, H, i0,
+                                                            ly, gj, jj, base, lead, D, last, res, Vref);
+                else
+                    row_gs4<CPL, WY, WX, CHECK, false, true>(A, s_u, s_ctrl, s_prog, pitch, cstride, H, i0,
+                                                             ly, gj, jj, base, lead, D, last, res, Vref);
+            } else {
+                if (xneg)
+                    row_gs4<CPL, WY, WX, CHECK, true, false>(A, s_u, s_ctrl, s_prog, pitch, cstride, H, i0,
+                                                             ly, gj, jj, base, lead, D, last, res, Vref);
+                else
+                    row_gs4<CPL, WY, WX, CHECK, false, false>(A, s_u, s_ctrl, s_prog, pitch, cstride, H, i0,
+                                                              ly, gj, jj, base, lead, D, last, res, Vref);
+            }
         }
         if (CHECK) break;
         float r = res;
@@ -326,6 +346,10 @@ __device__ __forceinline__ void row_gsg(const KP<real> &A, real *s_u, const real
     real *rowp = s_u + (ly + H) * pitch + H;
     const unsigned prog_prev =
         (unsigned)__cvta_generic_to_shared((const void *)(s_prog + (jj > 0 ? jj - 1 : 0)));
+    // the row's coefficients, prefetched: lane L holds nodes L and L + 32 (global loads overlap
+    // the wait for the previous row instead of sitting on every node's dependency chain)
+    const NodeCoef<real> nc0 = node_coef<real>(A.P, min(i0 + lane, n - 1), gj, D, Vref);
+    const NodeCoef<real> nc1 = node_coef<real>(A.P, min(i0 + lane + 32, n - 1), gj, D, Vref);
     for (int gs = 0; gs < NG; ++gs) {
         if (!CHECK && jj > 0) {
             const int need = base + min(gs + lead, NG);
@@ -335,7 +359,19 @@ __device__ __forceinline__ void row_gsg(const KP<real> &A, real *s_u, const real
         for (int t = 0; t < 4; ++t) {
             const int lx = XNEG ? TW - 1 - (4 * gs + t) : 4 * gs + t;
             if ((dmask >> lx) & 1ull) continue;
-            const real best = general_node<real>(A.P, s_ctrl, rowp + lx, pitch, i0 + lx, gj, D, Vref);
+            const NodeCoef<real> &src = lx < 32 ? nc0 : nc1;
+            NodeCoef<real> nc;
+            const int sl = lx & 31;
+            nc.c = __shfl_sync(FULL, src.c, sl);
+            nc.d1 = __shfl_sync(FULL, src.d1, sl);
+            nc.d2 = __shfl_sync(FULL, src.d2, sl);
+            nc.o[0][0] = __shfl_sync(FULL, src.o[0][0], sl);
+            nc.o[0][1] = __shfl_sync(FULL, src.o[0][1], sl);
+            nc.o[1][0] = __shfl_sync(FULL, src.o[1][0], sl);
+            nc.o[1][1] = __shfl_sync(FULL, src.o[1][1], sl);
+            nc.sa = __shfl_sync(FULL, src.sa, sl);
+            nc.D = __shfl_sync(FULL, src.D, sl);
+            const real best = general_node_c<real>(A.P, s_ctrl, rowp + lx, pitch, i0 + lx, gj, nc);
             commit_node<real, CHECK>(rowp + lx, best, true, res, A.out, (int64_t)gj * n + i0 + lx, Vref);
             __syncwarp();      // lane 0's commit is seen by every lane's next gathers
         }

@@ -7,12 +7,23 @@ from paper_1502_01629_b200 import Solver
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--cfg", default="C5"); ap.add_argument("--n", type=int, default=None)
-ap.add_argument("--prec", type=int, default=32); ap.add_argument("--k", default="4")
+ap.add_argument("--paper", default=None, help="problem:cells:eps (paper_instance)")
+ap.add_argument("--general", default=None, help="cost:sigma:n:eps:n_coarse (general_instance)")
+ap.add_argument("--prec", type=int, default=32); ap.add_argument("--k", default="0")
 ap.add_argument("--modes", default="patchy,static"); ap.add_argument("--tol", type=float, default=1e-6)
 ap.add_argument("--kernel", type=int, default=0); ap.add_argument("--delta", default="0")
 ap.add_argument("--max_rounds", type=int, default=200000); ap.add_argument("--schedule", default="rounds"); ap.add_argument("--policy", type=int, default=0)
 a = ap.parse_args()
-t = time.time(); inst = I.make_config(a.cfg, n=a.n); print("gen", time.time() - t, flush=True)
+t = time.time()
+if a.paper:
+    pb, ce, ep = a.paper.split(":")
+    inst = I.paper_instance(pb, int(ce), float(ep))
+elif a.general:
+    co, sg, nn, ep, nc = a.general.split(":")
+    inst = I.general_instance(int(nn), cost=int(co), sigma=int(sg), eps=float(ep), n_coarse=int(nc))
+else:
+    inst = I.make_config(a.cfg, n=a.n)
+print("gen", time.time() - t, flush=True)
 t = time.time(); s = Solver(inst, precision=a.prec); torch.cuda.synchronize(); print("create", time.time() - t, flush=True)
 cs = s.coarse_solve(inst.tol_coarse); print("coarse", cs, flush=True)
 t = time.time(); s.synthesize(); s.build_patches(inst.n_patches); print("synth+patches", time.time() - t, flush=True)

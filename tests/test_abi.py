@@ -49,15 +49,17 @@ def test_struct_sizes_match_c(tmp_path):
     from paper_1502_01629_b200 import _native as N
     src = tmp_path / "sz.c"
     src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "pdd.h"\nint main(){'
-                   'printf("%zu %zu %zu %zu %zu %zu %zu\\n", sizeof(pdd_problem), sizeof(pdd_coef),'
+                   'printf("%zu %zu %zu %zu %zu %zu %zu %zu %zu %zu\\n", sizeof(pdd_problem), sizeof(pdd_coef),'
                    'sizeof(pdd_solve_opts), sizeof(pdd_solve_stats), sizeof(pdd_coarse_stats),'
-                   'offsetof(pdd_problem, kind), offsetof(pdd_problem, sigma));return 0;}')
+                   'offsetof(pdd_problem, kind), offsetof(pdd_problem, sigma),'
+                   'offsetof(pdd_problem, cost_ctrl), sizeof(pdd_regime), sizeof(pdd_fuzzy_stats));return 0;}')
     exe = tmp_path / "sz"
     subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
     vals = list(map(int, subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()))
     py = [C.sizeof(N.pdd_problem), C.sizeof(N.pdd_coef), C.sizeof(N.pdd_solve_opts),
           C.sizeof(N.pdd_solve_stats), C.sizeof(N.pdd_coarse_stats),
-          N.pdd_problem.kind.offset, N.pdd_problem.sigma.offset]
+          N.pdd_problem.kind.offset, N.pdd_problem.sigma.offset, N.pdd_problem.cost_ctrl.offset,
+          C.sizeof(N.pdd_regime), C.sizeof(N.pdd_fuzzy_stats)]
     assert vals == py
 
 

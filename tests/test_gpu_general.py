@@ -115,3 +115,27 @@ def test_patchy_pipeline_exit_problem(cost, sigma):
     assert st["converged"] == 1
     _check(s.get_values(), ref["V"], 64)
     s.close()
+
+
+@pytest.mark.parametrize("problem,eps_P", [("eikonal", 1e-3), ("zermelo", 1e-4)])
+def test_fuzzy_patches_bit_exact(problem, eps_P):
+    """The paper's fuzzy patches on the GPU: canonical fp64 advection of phi_p along
+    the synthesised feedback -- sweep count, phi and the thresholded labels bit-exact with the
+    oracle; the patchy solve then runs on these patches."""
+    from paper_1502_01629_b200 import Solver
+    inst = I.paper_instance(problem, 200, 1e-9)
+    ref = O.solve_pipeline(inst, tol=1e-14)
+    fz = O.fuzzy_phi(inst, ref["astar"], 4, eps_P)
+    lab, mem = O.fuzzy_assign(inst, fz["phi"], 0.5)
+    s = Solver(inst, precision=64)
+    s.coarse_solve(inst.tol_coarse)
+    s.synthesize()
+    st = s.build_fuzzy_patches(4, eps_P=eps_P, tau_P=0.5, return_phi=True)
+    assert st["converged"] == 1 and st["sweeps"] == fz["sweeps"]
+    assert np.array_equal(st["phi"].view(np.uint64), fz["phi"].view(np.uint64))
+    assert np.array_equal(s.get_labels(), lab)
+    assert st["overlap_nodes"] == int(np.count_nonzero(mem >= 2))
+    sol = s.solve("patchy", tol=1e-13)
+    assert sol["converged"] == 1
+    assert float(np.abs(s.get_values() - ref["V"]).max()) <= 1e-10
+    s.close()
