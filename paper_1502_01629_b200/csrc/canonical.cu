@@ -375,6 +375,42 @@ __global__ void k_fuzzy_assign(DProblem P, const double *__restrict__ phi, int n
     if ((threadIdx.x & 31) == 0 && ov) atomicAdd(overlap, ov);
 }
 
+// k_synthesize with the row-invariant table of k_coarse_rowtab built on the fine grid (row-uniform
+// coefficients): the same operations per (node, control), the row-dependent ones hoisted
+__global__ void k_synthesize_rt(DProblem P, const double *__restrict__ uhat,
+                                const CoarseRowEntry *__restrict__ tab, uint8_t *__restrict__ astar)
+{
+    const int n = P.n;
+    const int64_t N = (int64_t)n * n;
+    const double top = (double)(n - 1);
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < N;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        if (P.kind[k] != 0) { astar[k] = 255; continue; }
+        const int i = (int)(k % n), j = (int)(k / n);
+        const CoarseRowEntry *row = tab + (int64_t)j * P.na;
+        double best = INFINITY;
+        int arg = -1;
+        for (int a = 0; a < P.na; ++a) {
+            const CoarseRowEntry e = row[a];
+            double gx = DADD((double)i, e.bxq);
+            if (gx < 0.0) gx = 0.0;
+            if (gx > top) gx = top;
+            int cx = (int)floor(gx);
+            if (cx > n - 2) cx = n - 2;
+            const double tx = DSUB(gx, (double)cx);
+            const double ux = DSUB(1.0, tx);
+            const int64_t c0 = (int64_t)e.cy * n + cx;
+            double s = DMUL(DMUL(ux, e.uy), uhat[c0]);
+            s = DADD(s, DMUL(DMUL(tx, e.uy), uhat[c0 + 1]));
+            s = DADD(s, DMUL(DMUL(ux, e.ty), uhat[c0 + n]));
+            s = DADD(s, DMUL(DMUL(tx, e.ty), uhat[c0 + n + 1]));
+            const double v = DADD(e.hl, DMUL(P.beta, s));
+            if (v < best) { best = v; arg = a; }
+        }
+        astar[k] = (uint8_t)arg;
+    }
+}
+
 __global__ void k_successor(DProblem P, double M, const uint8_t *__restrict__ astar,
                             int32_t *__restrict__ succ)
 {
@@ -512,6 +548,13 @@ void launch_prolong(int nc, const double *uc, int n, double *out, cudaStream_t s
 {
     const int64_t N = (int64_t)n * n;
     k_prolong<<<grid_for(N, 256), 256, 0, s>>>(nc, uc, n, (n - 1) / (nc - 1), out);
+}
+
+void launch_synthesize_rt(const DProblem &P, const double *uhat, const CoarseRowEntry *tab,
+                          uint8_t *astar, cudaStream_t s)
+{
+    const int64_t N = (int64_t)P.n * P.n;
+    k_synthesize_rt<<<grid_for(N, 128), 128, 0, s>>>(P, uhat, tab, astar);
 }
 
 void launch_synthesize(const DProblem &P, const double *uhat, uint8_t *astar, cudaStream_t s)

@@ -114,7 +114,8 @@ struct pdd_ctx {
     unsigned long long *res_hist = nullptr;
     uint8_t *cflag = nullptr;   // coarse active-tile change flags, 2 x tiles
     CoarseRowEntry *crowtab = nullptr;   // coarse row-invariant table (n_c x N_A)
-    bool coarse_rowuniform = false;
+    CoarseRowEntry *frowtab = nullptr;   // the same for the fine-grid synthesis (n x N_A)
+    bool coarse_rowuniform = false, fine_rowuniform = false;
     bool coarse_tiled = false;  // coarse reach < tile: active-tile sweeps
     int *dev_int = nullptr;     // [0] sweeps_done, [1] jump changed flag
     void *rowtab = nullptr;
@@ -307,6 +308,7 @@ static size_t layout(pdd_ctx *c, void *ws, const pdd_problem *f, const pdd_probl
     const int ctn = cp ? (cp->n + coarse_tile() - 1) / coarse_tile() : 0;
     uint8_t *cflag = cp ? cv.take<uint8_t>(2 * (size_t)ctn * ctn) : nullptr;
     CoarseRowEntry *crt = cp ? cv.take<CoarseRowEntry>((size_t)cp->n * cp->n_controls) : nullptr;
+    CoarseRowEntry *frt = cp ? cv.take<CoarseRowEntry>((size_t)n * f->n_controls) : nullptr;
     uint8_t *astar = cv.take<uint8_t>(N);
     int16_t *labels = cv.take<int16_t>(N);
     int32_t *s0 = cp ? cv.take<int32_t>(N) : nullptr;
@@ -351,6 +353,7 @@ static size_t layout(pdd_ctx *c, void *ws, const pdd_problem *f, const pdd_probl
         c->res_hist = rh;
         c->cflag = cflag;
         c->crowtab = crt;
+        c->frowtab = frt;
         c->astar = astar;
         c->labels = labels;
         c->succ0 = s0;
@@ -438,10 +441,13 @@ pdd_status pdd_create(const pdd_problem *fine, const pdd_problem *coarse, int32_
     // active-tile coarse sweeps need the stencil reach (+ the bilinear corner) inside one tile
     // (computed here: the host arrays of the problem are valid only during this call)
     ctx->coarse_tiled = coarse && reach_cells(coarse) + 2.0 < (double)coarse_tile();
-    if (coarse) {
+    {
         auto rok = [](const pdd_coef &c) { return c.kind == PDD_COEF_CONST || c.kind == PDD_COEF_ROW; };
-        ctx->coarse_rowuniform = rok(coarse->speed) && rok(coarse->drift[0]) && rok(coarse->drift[1]) &&
-                                 rok(coarse->cost);
+        if (coarse)
+            ctx->coarse_rowuniform = rok(coarse->speed) && rok(coarse->drift[0]) &&
+                                     rok(coarse->drift[1]) && rok(coarse->cost);
+        ctx->fine_rowuniform = rok(fine->speed) && rok(fine->drift[0]) && rok(fine->drift[1]) &&
+                               rok(fine->cost);
     }
     // aligned base
     char *base = (char *)workspace;
@@ -569,8 +575,15 @@ pdd_status pdd_synthesize(pdd_ctx *ctx)
     if (!ctx->coarse_done) return fail(ctx, PDD_E_STATE, "pdd_synthesize needs pdd_coarse_solve first");
     cudaStream_t s = ctx->stream;
     launch_prolong(ctx->coarse.n, ctx->uc_final, ctx->fine.n, ctx->uhat, s);
-    launch_synthesize(ctx->F.d, ctx->uhat, ctx->astar, s);
-    ctx->launches += 2;
+    if (ctx->fine_rowuniform && !std::getenv("PDD_SYNTH_NORT")) {   // env: A/B only
+        // row-invariant part of the synthesis hoisted into a (row, control) table: bit-identical
+        launch_coarse_rowtab(ctx->F.d, ctx->frowtab, s);
+        launch_synthesize_rt(ctx->F.d, ctx->uhat, ctx->frowtab, ctx->astar, s);
+        ctx->launches += 3;
+    } else {
+        launch_synthesize(ctx->F.d, ctx->uhat, ctx->astar, s);
+        ctx->launches += 2;
+    }
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(s));
     ctx->synth_done = true;
