@@ -108,9 +108,9 @@ typedef struct {
     int32_t mode;        /* 0 patchy: V starts at u_hat, tiles activated in ascending u_hat
                             order; 1 static: V starts at V0 (R11)         */
     int32_t k_inner;     /* in-tile Gauss-Seidel sweeps per tile visit (>= 1; 0 = automatic:
-                            1 patchy, 4 static, and 4 for a patchy grid whose tiles fit in one
-                            wave of sweep CTAs -- then the u_hat front is off too when delta
-                            = 0).  Patchy tiles sweep first in their downstream orientation
+                            1 patchy, 4 static, and 4 for a patchy general-stencil grid whose
+                            tiles fit in about one wave of sweep CTAs -- on such grids the
+                            u_hat front is off when delta = 0).  Patchy tiles sweep first in their downstream orientation
                             (the signs of u_hat's differences over the tile); incoherent tiles
                             continue an orientation cycle across visits                     */
     double tol;          /* sup-norm residual tolerance eps                                  */

@@ -1060,7 +1060,11 @@ pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
         for (int32_t v : tf) tiles_free += v > 0;
     }
     const bool one_wave = tiles_free <= 2 * resident;   // "fits in (about) one wave": <= 2 waves
-    const int k_inner = o->k_inner > 0 ? o->k_inner : (o->mode == 0 && !one_wave ? 1 : 4);
+    // (measured: on one-wave grids the general stencil wants 4 sweeps per visit -- paper Zermelo
+    // 800^2: 49.7 vs 117 sweep-equivalents -- the row-table kernels 1: C2 10 ms vs 16 ms,
+    // eikonal 800^2 16 ms vs 34 ms)
+    const int k_inner = o->k_inner > 0 ? o->k_inner
+                        : (o->mode == 1 ? 4 : (one_wave && ctx->path == 1 ? 4 : 1));
     if (o->mode == 0 && o->delta == 0.0 && one_wave && o->reserved[1] != 2) {
         delta = -1.0;
         thr = INFINITY;

@@ -49,13 +49,19 @@ namespace pdd {
 #define PDD_MIN_BLOCKS1 2   // path 1 (general stencil) CTAs per SM bound (measured: C3 patchy
                             // 0.124 -> 0.106 s, static 0.29 -> 0.22 s against 1 CTA/SM)
 #endif
+#ifndef PDD_MIN_BLOCKS3
+#define PDD_MIN_BLOCKS3 3   // path 3 (row-table GS) CTAs per SM bound: 80 registers at 8 warps
+#endif
 template <int PATH>
-constexpr int min_blocks() { return PDD_MIN_BLOCKS > 0 ? PDD_MIN_BLOCKS : (PATH == 3 ? 3 : PATH == 1 ? PDD_MIN_BLOCKS1 : 1); }
+constexpr int min_blocks() { return PDD_MIN_BLOCKS > 0 ? PDD_MIN_BLOCKS : (PATH == 3 ? PDD_MIN_BLOCKS3 : PATH == 1 ? PDD_MIN_BLOCKS1 : 1); }
 #ifndef PDD_TH
 #define PDD_TH 32           // tile rows (multiple of NW)
 #endif
 constexpr int TH = PDD_TH;      // tile rows
-constexpr int NW = 8;           // warps per CTA
+#ifndef PDD_NW
+#define PDD_NW 8
+#endif
+constexpr int NW = PDD_NW;      // warps per CTA
 constexpr int RPW = TH / NW;    // rows per warp
 constexpr int TW_GENERAL = 64;
 constexpr unsigned FULL = 0xffffffffu;
@@ -405,6 +411,9 @@ __device__ __forceinline__ void row_table(const KP<real> &A, real *s_u, const re
 #ifndef PDD_BIGREF
 #define PDD_BIGREF 1     // V_ref = staged min on a tile whose values span > 1 + |min| (R39)
 #endif
+#ifndef PDD_FASTWB
+#define PDD_FASTWB 1     // single-sweep visits: write-back without reading the old V
+#endif
 #ifndef PDD_GSG
 #define PDD_GSG 1    // path 1 (general stencil) uses the Gauss-Seidel tile sweeps of sweep_gs.cuh
 #endif
@@ -435,7 +444,7 @@ __device__ __forceinline__ void sweep_tile(const KP<real> &A, int t, unsigned ch
     // min(V0, minimum of the staged values): every u >= 0 and D >= 0, so every candidate
     // c0 + sum W u is >= 0 and the fp32 min over controls can compare raw float bits
     const int W2 = TW + 2 * H, H2 = TH + 2 * H;
-    constexpr int MAXE = 16;                       // (TH + 2H)(TW + 2H) <= 16 x 256 (H <= 4)
+    constexpr int MAXE = ((TH + 16) * 80 + NW * 32 - 1) / (NW * 32);   // (TH + 2H)(TW + 2H), H <= 8
     double vs[MAXE];
     double vmin = INFINITY;
 #pragma unroll
@@ -554,6 +563,29 @@ __device__ __forceinline__ void sweep_tile(const KP<real> &A, int t, unsigned ch
 
     // write back changed interior nodes, net change of the visit
     double chg = 0.0;
+    if (PDD_FASTWB && done_sweeps == 1) {
+        // one sweep: the visit's net change of a node IS that sweep's change, so the tile's net
+        // change is the sweep residual (rmaxv) and the write-back needs no read of the old V
+        // (a dependent global load per node on the visit's critical path); every free node is
+        // written (an unchanged node is rewritten within the arithmetic's rounding of V - V_ref)
+        constexpr int PER = (TH * TW + NW * 32 - 1) / (NW * 32);
+        uint8_t kd[PER];
+#pragma unroll
+        for (int m = 0; m < PER; ++m) {
+            const int e = threadIdx.x + m * NW * 32;
+            const int ly = e / TW, lx = e - ly * TW;
+            const int gi = i0 + lx, gj = j0 + ly;
+            kd[m] = (e < TH * TW && gi < n && gj < n) ? A.P.kind[(int64_t)gj * n + gi] : (uint8_t)1;
+        }
+#pragma unroll
+        for (int m = 0; m < PER; ++m) {
+            const int e = threadIdx.x + m * NW * 32;
+            if (kd[m] != 0) continue;
+            const int ly = e / TW, lx = e - ly * TW;
+            A.V[(int64_t)(j0 + ly) * n + i0 + lx] = Vref + (double)s_u[(ly + H) * pitch + lx + H];
+        }
+        chg = rmaxv;
+    } else
     for (int e = threadIdx.x; e < TH * TW; e += blockDim.x) {
         const int ly = e / TW, lx = e - ly * TW;
         const int gi = i0 + lx, gj = j0 + ly;
