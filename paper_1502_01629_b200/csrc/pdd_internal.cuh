@@ -225,6 +225,9 @@ struct SweepLaunch {
 void launch_round_begin(RoundCtl *ctl, ActCounters *c, cudaStream_t s);
 void launch_round_end(RoundCtl *ctl, const ActCounters *c, cudaStream_t s);
 void launch_round_reset(RoundCtl *ctl, double thr, cudaStream_t s);
+// order the round's active list by key (patchy: min u_hat) before the sweep
+void launch_sort_round(const RoundCtl *ctl, const ActCounters *c, const double *key, int32_t *list,
+                       cudaStream_t s);
 
 void launch_tile_init(const DProblem &P, const TileGeom &g, const double *uhat,
                       const int16_t *labels, TileState &T, cudaStream_t s, double coh_thr = 2.0);

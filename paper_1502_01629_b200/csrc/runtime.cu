@@ -1112,6 +1112,9 @@ pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
         CK(cudaMemsetAsync(ctx->T.tile_sweeps, 0, sizeof(int32_t) * ctx->n_tiles, s));
     }
     int batch = trace ? 1 : 4;
+    // patchy: visit each round's tiles in increasing min u_hat (A/B switch PDD_SORT)
+    const char *se = std::getenv("PDD_SORT");
+    const bool sort_rounds = o->mode == 0 && se && std::atoi(se) != 0;
     const char *te = std::getenv("PDD_TACT");   // A/B: neighbour-change activation threshold / tol
     const double tact = te ? std::atof(te) : 1.0;
     long long rounds_prev = 0;
@@ -1133,6 +1136,10 @@ pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
             launch_round_begin(ctx->rctl, L.acnt, s);
             launch_activate(ctx->g, ctx->T, cur, o->tol, o->tol * tact, 0.0, 0, ctx->n_tiles, s,
                             ready_slack, ctx->rctl, true);
+            if (sort_rounds) {
+                launch_sort_round(ctx->rctl, L.acnt, ctx->T.tile_minu, ctx->T.list[cur], s);
+                ctx->launches++;
+            }
             CK(cudaEventRecord(ctx->evp[0][b], s));
             CK(launch_sweep(L, s));
             CK(cudaEventRecord(ctx->evp[1][b], s));

@@ -411,6 +411,9 @@ __device__ __forceinline__ void row_table(const KP<real> &A, real *s_u, const re
 #ifndef PDD_BIGREF
 #define PDD_BIGREF 1     // V_ref = staged min on a tile whose values span > 1 + |min| (R39)
 #endif
+#ifndef PDD_PREFETCH
+#define PDD_PREFETCH 0   // 1: L2 prefetch of the next tile while sweeping (measured slower: spills)
+#endif
 #ifndef PDD_FASTWB
 #define PDD_FASTWB 1     // single-sweep visits: write-back without reading the old V
 #endif
@@ -634,6 +637,42 @@ __global__ void __launch_bounds__(NW * 32, min_blocks<PATH>()) k_sweep_dyn(KP<re
     __shared__ int s_t;
     if (A.ctl->stop) return;
     const int count = A.acnt->count;
+#if PDD_PREFETCH
+    // fetch one tile ahead and pull its tile + halo rows of V into L2 while the current tile is
+    // swept, so that the next visit's staging loads hit L2 instead of HBM
+    __shared__ int s_next;
+    if (threadIdx.x == 0) {
+        const int i = atomicAdd(&A.acnt->fetch, 1);
+        s_next = i < count ? A.list[i] : -1;
+    }
+    for (;;) {
+        __syncthreads();
+        const int t = s_next;
+        __syncthreads();
+        if (t < 0) return;
+        if (threadIdx.x == 0) {
+            const int i = atomicAdd(&A.acnt->fetch, 1);
+            s_next = i < count ? A.list[i] : -1;
+        }
+        __syncthreads();
+        const int tn = s_next;
+        if (tn >= 0) {
+            const int TWt = PATH == 2 ? TWOf<WY, WX>::value : TW_GENERAL;
+            const int n = A.P.n, H = A.g.H;
+            const int i0 = (tn % A.g.tiles_x) * TWt - H, j0 = (tn / A.g.tiles_x) * TH - H;
+            const int rows = TH + 2 * H, cols = TWt + 2 * H;
+            // one 128-byte line per thread-step: 16 doubles
+            const int lines_per_row = (cols + 15) / 16 + 1;
+            for (int e = threadIdx.x; e < rows * lines_per_row; e += blockDim.x) {
+                const int r = e / lines_per_row, c = (e - r * lines_per_row) * 16;
+                const int gj = j0 + r, gi = min(max(i0 + c, 0), n - 1);
+                if (gj >= 0 && gj < n)
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(A.V + (int64_t)gj * n + gi));
+            }
+        }
+        sweep_tile<real, PATH, CPL, WY, WX, false>(A, t, smem_raw, nullptr, nullptr);
+    }
+#else
     for (;;) {
         if (threadIdx.x == 0) {
             const int i = atomicAdd(&A.acnt->fetch, 1);
@@ -645,6 +684,7 @@ __global__ void __launch_bounds__(NW * 32, min_blocks<PATH>()) k_sweep_dyn(KP<re
         if (t < 0) return;
         sweep_tile<real, PATH, CPL, WY, WX, false>(A, t, smem_raw, nullptr, nullptr);
     }
+#endif
 }
 
 // Ordered schedule (one pass): persistent CTAs take tiles in ascending key order (P:744-749,
@@ -1052,6 +1092,55 @@ void launch_activate(const TileGeom &g, TileState &T, int out_list, double tol, 
 {
     k_activate<<<(n_tiles + 255) / 256, 256, 0, s>>>(g, T, out_list, tol, tol_act, thr, round,
                                                      n_tiles, slack, ctl, from_ctl);
+}
+
+// Order a round's active list by the tiles' min u_hat (the paper's processing order)
+// so that the dynamic fetch of k_sweep_dyn visits upstream tiles first: one CTA, bitonic sort of
+// (key, tile) pairs in shared memory; lists longer than SORT_MAX keep their activation order.
+constexpr int SORT_MAX = 4096;
+__global__ void __launch_bounds__(1024) k_sort_round(const RoundCtl *ctl, const ActCounters *c,
+                                                      const double *key, int32_t *list)
+{
+    __shared__ float sk[SORT_MAX];
+    __shared__ int32_t sv[SORT_MAX];
+    if (ctl->stop) return;
+    const int cnt = c->count;
+    if (cnt <= 1 || cnt > SORT_MAX) return;
+    int m = 1;
+    while (m < cnt) m <<= 1;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        if (i < cnt) {
+            const int t = list[i];
+            sk[i] = (float)key[t];
+            sv[i] = t;
+        } else {
+            sk[i] = __int_as_float(0x7f800000);
+            sv[i] = -1;
+        }
+    }
+    __syncthreads();
+    for (int k = 2; k <= m; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < m; i += blockDim.x) {
+                const int l = i ^ j;
+                if (l > i) {
+                    const bool up = (i & k) == 0;
+                    const float a = sk[i], b = sk[l];
+                    if ((a > b) == up) {
+                        sk[i] = b; sk[l] = a;
+                        const int32_t tv = sv[i]; sv[i] = sv[l]; sv[l] = tv;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) list[i] = sv[i];
+}
+
+void launch_sort_round(const RoundCtl *ctl, const ActCounters *c, const double *key, int32_t *list,
+                       cudaStream_t s)
+{
+    k_sort_round<<<1, 1024, 0, s>>>(ctl, c, key, list);
 }
 
 // ------------------------------------------------------------------ device-driven rounds
