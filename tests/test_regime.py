@@ -96,3 +96,15 @@ def test_invalid_arguments(ra):
         ra(0.0, 1.0, 0.1, 0.01)
     with pytest.raises(PddError):
         ra(2.0, 1.0, 0.1, 0.01)
+
+
+def test_generator_time_step_matches_analyser(ra):
+    """pdd_inputs.paper_time_step (problem data, written independently) and the library's
+    pdd_regime_analyse give the same h = alpha dx / f_min on both sides of the threshold."""
+    import pdd_inputs as I
+    for problem, (fmin, fmax) in I.PAPER_FMINMAX.items():
+        for dx in (0.02, 0.005):
+            for eps in (0.0, 1e-6, 1e-4, 2.5e-3, 1e-2):
+                h = I.paper_time_step(dx, eps, fmin, fmax)
+                r = ra(fmin, fmax, math.sqrt(2.0 * eps), dx)
+                assert h == pytest.approx(r["h"], rel=1e-12), (problem, dx, eps)
