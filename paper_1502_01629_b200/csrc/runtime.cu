@@ -782,8 +782,10 @@ static pdd_status prepare(pdd_ctx *ctx, int kernel_req)
     ctx->WX = WX;
     ctx->Hx = H;
     TileGeom g{};
-    g.TW = (path == 2 && !g4) ? rowtab_tw(WY, WX) : 64;
-    g.TH = sweep_tile_rows();
+    int tw3 = 64, th3 = 32;
+    p3_tile(tw3, th3);
+    g.TW = (path == 2 && !g4) ? rowtab_tw(WY, WX) : (g4 ? tw3 : 64);
+    g.TH = g4 ? th3 : sweep_tile_rows();
     g.H = H;
     g.tiles_x = (p->n + g.TW - 1) / g.TW;
     g.tiles_y = (p->n + g.TH - 1) / g.TH;
@@ -1022,11 +1024,11 @@ pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
 
     double delta = o->delta;
     if (o->mode == 1) delta = -1.0;
-    // automatic bucket width: the value change across 1/8 of a tile width at unit speed
-    // (measured on C5: ~8 cells of front travel per round minimises time-to-converge)
+    // automatic bucket width: the value change across 6 cells at unit speed (measured on C5 / C4
+    // / C3: 6 cells of front travel per round beat 4.8 and 8)
     if (delta == 0.0) {
         const char *e = std::getenv("PDD_DSCALE");      // A/B only
-        delta = ctx->g.TW * ctx->fine.h * d.lmax / 8.0 * (e ? std::atof(e) : 1.0);
+        delta = 6.0 * ctx->fine.h * d.lmax * (e ? std::atof(e) : 1.0);
     }
     double thr = delta > 0.0 ? -1.0 : INFINITY;
     // bucket policy 2 (patchy): no moving threshold; a tile is admitted once its upstream

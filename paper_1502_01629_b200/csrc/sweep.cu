@@ -431,7 +431,8 @@ template <typename real, int PATH, int CPL, int WY, int WX, bool CHECK>
 __device__ __forceinline__ void sweep_tile(const KP<real> &A, int t, unsigned char *smem_raw,
                                            double *res_out, double *chg_out)
 {
-    constexpr int TW = PATH == 2 ? TWOf<WY, WX>::value : TW_GENERAL;
+    constexpr int TW = PATH == 2 ? TWOf<WY, WX>::value : PATH == 3 ? TW3 : TW_GENERAL;
+    constexpr int THt = PATH == 3 ? TH3 : TH;      // tile rows of this path
     constexpr int NCOPY = PATH == 3 ? 4 : 1;
     double *s_red = reinterpret_cast<double *>(smem_raw);            // NW
     volatile int *s_prog = reinterpret_cast<volatile int *>(s_red + NW);   // TH progress counters
@@ -440,14 +441,14 @@ __device__ __forceinline__ void sweep_tile(const KP<real> &A, int t, unsigned ch
     const int H = A.g.H, pitch = A.g.pitch;
     const int n = A.P.n;
     const int i0 = (t % A.g.tiles_x) * TW;
-    const int j0 = (t / A.g.tiles_x) * TH;
+    const int j0 = (t / A.g.tiles_x) * THt;
     // stage tile + halo (coalesced fp64 row reads, held in registers: one consistent snapshot
     // even while neighbouring CTAs of the same round write their tiles), converted relative to
     // V_ref = the tile-centre value (|u| at most half the tile's value range), or with PDD_RAWMIN
     // min(V0, minimum of the staged values): every u >= 0 and D >= 0, so every candidate
     // c0 + sum W u is >= 0 and the fp32 min over controls can compare raw float bits
-    const int W2 = TW + 2 * H, H2 = TH + 2 * H;
-    constexpr int MAXE = ((TH + 16) * 80 + NW * 32 - 1) / (NW * 32);   // (TH + 2H)(TW + 2H), H <= 8
+    const int W2 = TW + 2 * H, H2 = THt + 2 * H;
+    constexpr int MAXE = ((THt + 16) * (TW + 16) + NW * 32 - 1) / (NW * 32);   // (TH + 2H)(TW + 2H), H <= 8
     double vs[MAXE];
     double vmin = INFINITY;
 #pragma unroll
@@ -480,7 +481,7 @@ __device__ __forceinline__ void sweep_tile(const KP<real> &A, int t, unsigned ch
         // problem's 1e6 start values, or values interpolated from them, next to the front, R39):
         // then the smallest staged value, so that the nodes the front has reached keep full
         // precision next to the placeholders
-        const int ci = min(i0 + TW / 2, n - 1), cj = min(j0 + TH / 2, n - 1);
+        const int ci = min(i0 + TW / 2, n - 1), cj = min(j0 + THt / 2, n - 1);
         Vref = __ldcg(A.V + (int64_t)cj * n + ci);
         if (PDD_BIGREF) {
             double vminb = s_red[0];
@@ -504,7 +505,7 @@ __device__ __forceinline__ void sweep_tile(const KP<real> &A, int t, unsigned ch
         }
     }
     for (int e = threadIdx.x; e < 2 * A.P.na; e += blockDim.x) s_ctrl[e] = (real)A.P.ctrl[e];
-    if (threadIdx.x < TH) s_prog[threadIdx.x] = 0;
+    if (threadIdx.x < THt) s_prog[threadIdx.x] = 0;
     __syncthreads();
 
     // D = h l - (1 - beta) V_ref >= 0 (V_ref <= V0 = h l / (1 - beta); the clamp removes fp64
@@ -571,14 +572,14 @@ __device__ __forceinline__ void sweep_tile(const KP<real> &A, int t, unsigned ch
         // change is the sweep residual (rmaxv) and the write-back needs no read of the old V
         // (a dependent global load per node on the visit's critical path); every free node is
         // written (an unchanged node is rewritten within the arithmetic's rounding of V - V_ref)
-        constexpr int PER = (TH * TW + NW * 32 - 1) / (NW * 32);
+        constexpr int PER = (THt * TW + NW * 32 - 1) / (NW * 32);
         uint8_t kd[PER];
 #pragma unroll
         for (int m = 0; m < PER; ++m) {
             const int e = threadIdx.x + m * NW * 32;
             const int ly = e / TW, lx = e - ly * TW;
             const int gi = i0 + lx, gj = j0 + ly;
-            kd[m] = (e < TH * TW && gi < n && gj < n) ? A.P.kind[(int64_t)gj * n + gi] : (uint8_t)1;
+            kd[m] = (e < THt * TW && gi < n && gj < n) ? A.P.kind[(int64_t)gj * n + gi] : (uint8_t)1;
         }
 #pragma unroll
         for (int m = 0; m < PER; ++m) {
@@ -589,7 +590,7 @@ __device__ __forceinline__ void sweep_tile(const KP<real> &A, int t, unsigned ch
         }
         chg = rmaxv;
     } else
-    for (int e = threadIdx.x; e < TH * TW; e += blockDim.x) {
+    for (int e = threadIdx.x; e < THt * TW; e += blockDim.x) {
         const int ly = e / TW, lx = e - ly * TW;
         const int gi = i0 + lx, gj = j0 + ly;
         if (gi >= n || gj >= n) continue;
@@ -657,10 +658,11 @@ __global__ void __launch_bounds__(NW * 32, min_blocks<PATH>()) k_sweep_dyn(KP<re
         __syncthreads();
         const int tn = s_next;
         if (tn >= 0) {
-            const int TWt = PATH == 2 ? TWOf<WY, WX>::value : TW_GENERAL;
+            const int TWt = PATH == 2 ? TWOf<WY, WX>::value : PATH == 3 ? TW3 : TW_GENERAL;
+            const int THq = PATH == 3 ? TH3 : TH;
             const int n = A.P.n, H = A.g.H;
-            const int i0 = (tn % A.g.tiles_x) * TWt - H, j0 = (tn / A.g.tiles_x) * TH - H;
-            const int rows = TH + 2 * H, cols = TWt + 2 * H;
+            const int i0 = (tn % A.g.tiles_x) * TWt - H, j0 = (tn / A.g.tiles_x) * THq - H;
+            const int rows = THq + 2 * H, cols = TWt + 2 * H;
             // one 128-byte line per thread-step: 16 doubles
             const int lines_per_row = (cols + 15) / 16 + 1;
             for (int e = threadIdx.x; e < rows * lines_per_row; e += blockDim.x) {
@@ -868,6 +870,12 @@ void p3_geometry(int &pitch, int &cstride, int &hmax)
     pitch = P3_PITCH;
     cstride = P3_CSTRIDE;
     hmax = P3_HMAX;
+}
+
+void p3_tile(int &tw, int &th)
+{
+    tw = TW3;
+    th = TH3;
 }
 
 cudaError_t launch_sweep(const SweepLaunch &L, cudaStream_t s)

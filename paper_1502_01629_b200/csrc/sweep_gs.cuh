@@ -73,9 +73,59 @@ __device__ __forceinline__ int prog_acquire(volatile int *p)
 // path-3 shared-memory geometry for H <= 4 (runtime.cu prepare() uses the same numbers): rows of
 // 76 floats (16-byte aligned, odd number of 16-byte groups), 4 shifted copies 3048 floats apart
 // ((TH + 8) x 76 + 4 rounded so the copies start in different bank groups)
-constexpr int P3_PITCH = 76;
-constexpr int P3_CSTRIDE = 3048;
+// PDD_P3_WIDE: tiles of 16 rows x 128 columns instead of 32 x 64 (same 2048 nodes): 32 groups per
+// row against the 8-warp row pipeline's 2 x 8 = 16 groups of lead, so the ring of warps has slack
+// and a single-sweep visit fills / drains the pipeline in 62 instead of 78 group steps.
+#ifndef PDD_P3_WIDE
+#define PDD_P3_WIDE 1
+#endif
+#ifndef PDD_P3_TW
+#define PDD_P3_TW (PDD_P3_WIDE ? 128 : 64)
+#endif
+#ifndef PDD_P3_TH
+#define PDD_P3_TH (PDD_P3_WIDE ? 16 : 32)
+#endif
 constexpr int P3_HMAX = 4;
+constexpr int TW3 = PDD_P3_TW;   // path-3 tile columns (64 or 128)
+constexpr int TH3 = PDD_P3_TH;   // path-3 tile rows (multiple of 8)
+// rows of TW3 + 2 H_max floats rounded up to 16 bytes with an odd number of float4 (consecutive
+// window rows in different 16-byte bank groups); the 4 shifted copies (TH3 + 8) rows + 4 apart,
+// rounded so that they start in different bank groups
+constexpr int p3_pitch_of(int tw)
+{
+    int p = tw + 2 * P3_HMAX;
+    while (p % 4 != 0 || ((p / 4) & 1) == 0) ++p;
+    return p;
+}
+constexpr int p3_cstride_of(int th, int pitch)
+{
+    int c = (th + 2 * P3_HMAX) * pitch + 4;
+    while (c % 4 != 0 || ((c / 4) % 8) != 2) ++c;
+    return c;
+}
+constexpr int P3_PITCH = p3_pitch_of(TW3);
+constexpr int P3_CSTRIDE = p3_cstride_of(TH3, P3_PITCH);
+static_assert(TW3 == 64 || TW3 == 128, "path-3 tile width");
+
+// per-row masks for up to 128 columns: bit lx of word lx >> 6
+__device__ __forceinline__ void row_masks128(const DProblem &P, int TW, int i0, int gj, int Hx,
+                                             unsigned long long dm[2], unsigned long long em[2])
+{
+    const int lane = threadIdx.x & 31;
+    const int n = P.n;
+    dm[0] = dm[1] = em[0] = em[1] = 0ull;
+#pragma unroll
+    for (int part = 0; part < 4; ++part) {
+        if (part * 32 >= TW) break;
+        const int lx = part * 32 + lane;
+        const int gi = i0 + lx;
+        const bool oob = lx >= TW || gi >= n;
+        const bool dir = oob || P.kind[(int64_t)gj * n + gi] != 0;
+        const bool edge = !dir && (gi < Hx || gi > n - 1 - Hx);
+        dm[part >> 1] |= (unsigned long long)__ballot_sync(FULL, dir) << (32 * (part & 1));
+        em[part >> 1] |= (unsigned long long)__ballot_sync(FULL, edge) << (32 * (part & 1));
+    }
+}
 
 // PDD_RAWMIN 1: V_ref = min of the staged tile, all candidates >= 0, REDUX on the raw float bits
 // (saves 4 ALU ops per node, ~3 % on C5) -- off by default: |u| then spans the whole tile range
@@ -100,16 +150,16 @@ __device__ __forceinline__ void row_gs4(const KP<float> &A, float *s_u, const fl
     (void)pitch_rt;
     (void)cstride_rt;
     constexpr int pitch = P3_PITCH, cstride = P3_CSTRIDE;
-    constexpr int TW = 64;
-    constexpr int NG = TW / 4;                 // groups per row
+    constexpr int TW = TW3;
+    constexpr int NG = TW / 4;                 // groups per row (<= 32)
     constexpr int NWC = WX + 3;                // window columns used per group
     constexpr bool xneg = XNEG;
     const int lane = threadIdx.x & 31;
     const int n = A.P.n;
     // ---- row setup (independent of other rows: overlaps the wait for jj - 1)
-    unsigned long long dmask, emask;
-    row_masks(A.P, TW, i0, gj, A.Hx, dmask, emask);
-    const unsigned long long skip = dmask | emask;
+    unsigned long long dm[2], em2[2];
+    row_masks128(A.P, TW, i0, gj, A.Hx, dm, em2);
+    const unsigned long long skip[2] = {dm[0] | em2[0], dm[1] | em2[1]};
     const RowEntry<float, WY, WX> *tab =
         reinterpret_cast<const RowEntry<float, WY, WX> *>(A.rowtab) + (int64_t)gj * A.na_pad;
     float Wt[CPL][WY * WX];
@@ -145,9 +195,12 @@ __device__ __forceinline__ void row_gs4(const KP<float> &A, float *s_u, const fl
     // per-lane skip bits of its node in every group (bit G = node 4G + nd is special)
     unsigned skip16 = 0u;
 #pragma unroll
-    for (int G = 0; G < NG; ++G) skip16 |= (unsigned)((skip >> (4 * G + nd)) & 1ull) << G;
+    for (int G = 0; G < NG; ++G) {
+        const int b = 4 * G + nd;
+        skip16 |= (unsigned)((skip[b >> 6] >> (b & 63)) & 1ull) << G;
+    }
     const unsigned prog_prev = (unsigned)__cvta_generic_to_shared((const void *)(s_prog + (jj > 0 ? jj - 1 : 0)));
-    const unsigned long long edge = EDGE ? (emask & ~dmask) : 0ull;
+    const unsigned long long edge[2] = {EDGE ? (em2[0] & ~dm[0]) : 0ull, EDGE ? (em2[1] & ~dm[1]) : 0ull};
     for (int gs = 0; gs < NG; ++gs) {
         const int G = xneg ? NG - 1 - gs : gs;
         const int g = 4 * G;
@@ -185,7 +238,7 @@ __device__ __forceinline__ void row_gs4(const KP<float> &A, float *s_u, const fl
                 acc[c][gg] = a;
             }
         }
-        const unsigned sk4 = (unsigned)(skip >> g) & 0xfu;     // special nodes of this group
+        const unsigned sk4 = (unsigned)(skip[g >> 6] >> (g & 63)) & 0xfu;   // special nodes of this group
         const float4 o4 = *reinterpret_cast<const float4 *>(oldp + g);
         const float old[4] = {o4.x, o4.y, o4.z, o4.w};
         float nv[4], dlt[4], rd[4];
@@ -234,11 +287,11 @@ __device__ __forceinline__ void row_gs4(const KP<float> &A, float *s_u, const fl
         // domain's x-boundary instantiate this (EDGE): the interior tiles' loop carries none of
         // the general stencil's live ranges (0 spills at 80 registers)
         if constexpr (EDGE) {
-            unsigned long long em = edge & (0xfull << g);
+            unsigned em = (unsigned)(edge[g >> 6] >> (g & 63)) & 0xfu;
             if (em) {
                 __syncwarp();
                 while (em) {
-                    const int lx = __ffsll((long long)em) - 1;
+                    const int lx = g + __ffs(em) - 1;
                     em &= em - 1;
                     const float best = PDD_EDGE_CALL
                         ? general_node_edge<float>(A.P, s_ctrl, rowp + lx, pitch, i0 + lx, gj, D, Vref)
@@ -263,14 +316,14 @@ __device__ __forceinline__ int tile_gs4(const KP<float> &A, float *s_u, const fl
                                          int cstride, int H, int i0, int j0, float D, int k_inner,
                                          float &res, double Vref, int o0, int sbase)
 {
-    constexpr int NG = 16;
+    constexpr int NG = TW3 / 4;
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int n = A.P.n;
     const int lead = 1 + (3 + H) / 4;          // groups the previous row must be ahead
     const int sweeps = CHECK ? 1 : k_inner;
     double first = 0.0;                        // change of the visit's first sweep
-    const bool edge_tile = i0 < A.Hx || i0 + 64 > n - 1 - A.Hx;   // holds nodes with x-clamped feet
+    const bool edge_tile = i0 < A.Hx || i0 + TW3 > n - 1 - A.Hx;   // holds nodes with x-clamped feet
 
     for (int sw = 0; sw < sweeps; ++sw) {
         // every sweep tracks its residual: a tile that is converged w.r.t. its halo stops early
@@ -280,9 +333,9 @@ __device__ __forceinline__ int tile_gs4(const KP<float> &A, float *s_u, const fl
         const int orient = ((A.oxor >> (2 * ((sbase + sw) & 3))) & 3) ^ o0;   // o0: downstream first
         const bool xneg = orient & 1, yneg = orient & 2;
         const int base = sw * NG;              // progress counters are monotone across sweeps
-        for (int k = 0; k < TH / NW; ++k) {
+        for (int k = 0; k < TH3 / NW; ++k) {
             const int jj = warp + NW * k;      // position in this sweep's row order
-            const int ly = yneg ? TH - 1 - jj : jj;
+            const int ly = yneg ? TH3 - 1 - jj : jj;
             const int gj = j0 + ly;
             if (gj >= n) {
                 if (lane == 0) s_prog[jj] = base + NG;
