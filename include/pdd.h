@@ -187,8 +187,9 @@ pdd_status pdd_build_patches(pdd_ctx *ctx, int32_t n_patches, double M);
  * ties), orphan n_patches when every phi_p is 0; -1 target, -2 obstacle.  Replaces the labels of
  * pdd_build_patches (a patchy pdd_solve then reports per-patch rounds for these patches).
  * scratch: caller-owned DEVICE memory of >= pdd_fuzzy_scratch_bytes(n, n_patches) bytes (two
- * patch-major fields n_patches x n*n fp64); on return the final phi starts at
- * scratch + st->phi_offset.  Needs pdd_synthesize. */
+ * patch-major fields n_patches x n*n fp64, i.e. 16 n_patches n^2 bytes: the paper's few-patch
+ * decompositions; the successor labels of pdd_build_patches scale to hundreds of patches); on
+ * return the final phi starts at scratch + st->phi_offset.  Needs pdd_synthesize. */
 typedef struct {
     int64_t sweeps;        /* Jacobi sweeps including the last (converged) one                 */
     double residual;       /* change of the last sweep                                         */

@@ -414,6 +414,9 @@ __device__ __forceinline__ void row_table(const KP<real> &A, real *s_u, const re
 #ifndef PDD_PREFETCH
 #define PDD_PREFETCH 0   // 1: L2 prefetch of the next tile while sweeping (measured slower: spills)
 #endif
+#ifndef PDD_TILE_KEY
+#define PDD_TILE_KEY 0
+#endif
 #ifndef PDD_FASTWB
 #define PDD_FASTWB 1     // single-sweep visits: write-back without reading the old V
 #endif
@@ -889,7 +892,8 @@ __global__ void k_tile_init(DProblem P, TileGeom g, const double *uhat, const in
                             TileState T, double coh_thr)
 {
     __shared__ int s_free;
-    __shared__ unsigned long long s_min;
+    __shared__ unsigned long long s_min, s_max;
+    __shared__ double s_sum;
     __shared__ int s_lab[4];
     __shared__ double s_dx, s_dy;
     __shared__ int s_sx[2], s_sy[2];     // u_hat differences by sign (x pairs, y pairs)
@@ -899,6 +903,8 @@ __global__ void k_tile_init(DProblem P, TileGeom g, const double *uhat, const in
     if (threadIdx.x == 0) {
         s_free = 0;
         s_min = 0xffffffffffffffffull;
+        s_max = 0ull;
+        s_sum = 0.0;
         for (int k = 0; k < 4; ++k) s_lab[k] = -1;
         s_dx = 0.0;
         s_dy = 0.0;
@@ -906,7 +912,7 @@ __global__ void k_tile_init(DProblem P, TileGeom g, const double *uhat, const in
     }
     __syncthreads();
     int cnt = 0;
-    double mn = INFINITY, dx = 0.0, dy = 0.0;
+    double mn = INFINITY, mx = 0.0, sm = 0.0, dx = 0.0, dy = 0.0;
     int sx[2] = {0, 0}, sy[2] = {0, 0};
     for (int e = threadIdx.x; e < g.TW * g.TH; e += blockDim.x) {
         const int ly = e / g.TW, lx = e - ly * g.TW;
@@ -917,6 +923,8 @@ __global__ void k_tile_init(DProblem P, TileGeom g, const double *uhat, const in
         ++cnt;
         if (uhat) {
             mn = fmin(mn, uhat[k]);
+            mx = fmax(mx, uhat[k]);
+            sm += uhat[k];
             // direction in which u_hat grows = direction information travels (values depend on
             // smaller neighbouring values): the first in-tile sweep follows it
             if (lx + 1 < g.TW && gi + 1 < n && P.kind[k + 1] == 0) {
@@ -950,10 +958,17 @@ __global__ void k_tile_init(DProblem P, TileGeom g, const double *uhat, const in
         atomicAdd(&s_sy[1], sy[1]);
     }
     if (mn < INFINITY) atomicMin(&s_min, (unsigned long long)__double_as_longlong(fmax(mn, 0.0)));
+    if (mx > 0.0) atomicMax(&s_max, (unsigned long long)__double_as_longlong(mx));
+    if (sm != 0.0) atomicAdd(&s_sum, sm);
     __syncthreads();
     if (threadIdx.x == 0) {
         T.tile_free[t] = s_free;
-        T.tile_minu[t] = uhat ? (s_free > 0 ? __longlong_as_double((long long)s_min) : INFINITY) : 0.0;
+        // admission key of the patchy front: the tile's smallest u_hat (PDD_TILE_KEY 0), or a
+        // point between its smallest and its mean (1: mean, 2: midpoint of min and mean)
+        double key = __longlong_as_double((long long)s_min);
+        if (PDD_TILE_KEY == 1 && s_free > 0) key = s_sum / s_free;
+        if (PDD_TILE_KEY == 2 && s_free > 0) key = 0.5 * (key + s_sum / s_free);
+        T.tile_minu[t] = uhat ? (s_free > 0 ? key : INFINITY) : 0.0;
         T.tile_res[t] = s_free > 0 ? INFINITY : 0.0;
         T.tile_chg[t] = 0.0;
         for (int k = 0; k < 4; ++k) T.tile_lab[4 * t + k] = (int16_t)s_lab[k];
