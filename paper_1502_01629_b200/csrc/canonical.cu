@@ -66,6 +66,49 @@ __global__ void k_init_values(DProblem P, double *V)
     }
 }
 
+// Exact minimum over controls of the IEEE quotients num_a / den_a (num > 0, den > 0) with few
+// fp64 divisions: an fp32 estimate (relative error < 1e-6) of each quotient selects the controls
+// whose quotient can still be the minimum (within a 1e-5 window of the running estimate); only
+// those get the IEEE division.  Rounding is monotone, so min_a rn(num_a / den_a) = rn(q*) for the
+// exact minimiser a*, which is always among the candidates: the result is bit-identical to
+// dividing for every control.  Up to EXK candidates are kept; beyond that they are divided at once.
+#ifndef PDD_EXACT_MIN
+#define PDD_EXACT_MIN 0   // measured slower on sm_100a (C5 coarse 31 vs 24 ms): kept as an option
+#endif
+constexpr int EXK = 4;
+struct ExactMin {
+    float mt = INFINITY;                     // running estimate of the minimum
+    double cn[EXK], cd[EXK];
+    int cnt = 0;
+    double vex = INFINITY;                   // exact min of the candidates beyond EXK
+    __device__ __forceinline__ void add(double num, double den)
+    {
+        const float q = __fdividef((float)num, (float)den);
+        if (q < mt * (1.0f - 1e-5f)) {            // clearly below every candidate so far
+            cnt = 0;
+            vex = INFINITY;
+        } else if (q > mt * (1.0f + 1e-5f)) {
+            return;                               // cannot be the minimum
+        }
+        mt = fminf(mt, q);
+        if (cnt < EXK) {
+            cn[cnt] = num;
+            cd[cnt] = den;
+            ++cnt;
+        } else {
+            vex = fmin(vex, DDIV(num, den));
+        }
+    }
+    __device__ __forceinline__ double result() const
+    {
+        double b = vex;
+#pragma unroll
+        for (int k = 0; k < EXK; ++k)
+            if (k < cnt) b = fmin(b, DDIV(cn[k], cd[k]));
+        return b;
+    }
+};
+
 // sigma = 0 node update of the modified scheme (one foot point, w = 1)
 __device__ double canon_node_update(const DProblem &P, const double *V, int i, int j)
 {
@@ -135,6 +178,7 @@ __device__ double canon_node_update_rt(const DProblem &P, const double *V, int i
     const int64_t self = (int64_t)j * n + i;
     const double top = (double)(n - 1);
     double best = INFINITY;
+    ExactMin em;
     for (int a = 0; a < P.na; ++a) {
         const CoarseRowEntry e = row[a];
         double gx = DADD((double)i, e.bxq);
@@ -153,10 +197,14 @@ __device__ double canon_node_update_rt(const DProblem &P, const double *V, int i
             if (cr[t] == self) lam0 = DADD(lam0, wg[t]);
             else rp = DADD(rp, DMUL(wg[t], V[cr[t]]));
         }
-        const double v = DDIV(DADD(e.hl, DMUL(P.beta, rp)), DSUB(1.0, DMUL(P.beta, lam0)));
-        if (v < best) best = v;
+        if (PDD_EXACT_MIN) {
+            em.add(DADD(e.hl, DMUL(P.beta, rp)), DSUB(1.0, DMUL(P.beta, lam0)));
+        } else {
+            const double v = DDIV(DADD(e.hl, DMUL(P.beta, rp)), DSUB(1.0, DMUL(P.beta, lam0)));
+            if (v < best) best = v;
+        }
     }
-    return best;
+    return PDD_EXACT_MIN ? em.result() : best;
 }
 
 __global__ void k_coarse_sweep(DProblem P, const double *__restrict__ Vin, double *__restrict__ Vout,
