@@ -115,3 +115,29 @@ def test_workspace_scales_with_grid(lib):
     # the per-node arrays dominate the growth: doubling n quadruples the increment
     r = (sizes[2] - sizes[1]) / (sizes[1] - sizes[0])
     assert 3.5 < r < 4.5
+
+
+def test_fuzzy_scratch_bytes_and_validation(lib):
+    from paper_1502_01629_b200 import _native as N
+    nb = C.c_size_t(0)
+    assert lib.pdd_fuzzy_scratch_bytes(101, 4, C.byref(nb)) == N.PDD_OK
+    assert nb.value == 2 * 8 * 4 * 101 * 101 + 256            # two patch-major fp64 fields
+    assert lib.pdd_fuzzy_scratch_bytes(2, 4, C.byref(nb)) == N.PDD_E_INVALID
+    assert lib.pdd_fuzzy_scratch_bytes(101, 0, C.byref(nb)) == N.PDD_E_INVALID
+
+
+def test_boundary_side_sectors_split_the_ring_evenly():
+    """SPEC's example for the paper's four sides: N = 101, N_P = 4 -> four subsets
+    of 100 boundary nodes, corners assigned counter-clockwise; N_P = 1 -> the whole boundary."""
+    import pdd_inputs as I
+    n = 101
+    inst = I.paper_instance("eikonal", n - 1, 0.0, coarse_cells=None)
+    sec = inst.sector
+    ring = inst.kind == I.KIND_TARGET
+    assert ring.sum() == 4 * (n - 1)
+    assert sorted(np.bincount(sec[ring], minlength=4).tolist()) == [100, 100, 100, 100]
+    grid = sec.reshape(n, n)
+    assert set(grid[0, 1:-1]) == {3} and set(grid[-1, 1:-1]) == {1}      # bottom / top sides
+    assert set(grid[1:-1, 0]) == {2} and set(grid[1:-1, -1]) == {0}      # left / right sides
+    one = I.boundary_side_sectors(n, ring, 1)
+    assert set(one[ring]) == {0} and np.all(one[~ring] == -1)
