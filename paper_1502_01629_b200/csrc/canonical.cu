@@ -72,6 +72,9 @@ __global__ void k_init_values(DProblem P, double *V)
 // those get the IEEE division.  Rounding is monotone, so min_a rn(num_a / den_a) = rn(q*) for the
 // exact minimiser a*, which is always among the candidates: the result is bit-identical to
 // dividing for every control.  Up to EXK candidates are kept; beyond that they are divided at once.
+#ifndef PDD_COARSE_SMEM
+#define PDD_COARSE_SMEM 1   // tiled coarse sweep: V tile + halo staged in shared memory
+#endif
 #ifndef PDD_EXACT_MIN
 #define PDD_EXACT_MIN 0   // measured slower on sm_100a (C5 coarse 31 vs 24 ms): kept as an option
 #endif
@@ -207,6 +210,43 @@ __device__ double canon_node_update_rt(const DProblem &P, const double *V, int i
     return PDD_EXACT_MIN ? em.result() : best;
 }
 
+// The same update reading V from a shared-memory copy of the tile + halo (CH cells): the 4 x N_A
+// corner gathers per node hit shared memory instead of L1/L2 (the coarse sweep stalled on them:
+// long scoreboard 3.4 per issue).  Same values, same operations: bit-identical.
+constexpr int CH = 4;
+constexpr int CSW = 16 + 2 * CH;   // staged row width (CT + 2 CH)
+__device__ double canon_node_update_rt_s(const DProblem &P, const double *__restrict__ sV, int i,
+                                         int j, int ib, int jb, const CoarseRowEntry *__restrict__ row)
+{
+    const int n = P.n;
+    const double top = (double)(n - 1);
+    double best = INFINITY;
+    for (int a = 0; a < P.na; ++a) {
+        const CoarseRowEntry e = row[a];
+        double gx = DADD((double)i, e.bxq);
+        if (gx < 0.0) gx = 0.0;
+        if (gx > top) gx = top;
+        int cx = (int)floor(gx);
+        if (cx > n - 2) cx = n - 2;
+        const double tx = DSUB(gx, (double)cx);
+        const double ux = DSUB(1.0, tx);
+        const double wg[4] = {DMUL(ux, e.uy), DMUL(tx, e.uy), DMUL(ux, e.ty), DMUL(tx, e.ty)};
+        const int s0 = (e.cy - jb) * CSW + (cx - ib);
+        const int sr[4] = {s0, s0 + 1, s0 + CSW, s0 + CSW + 1};
+        const bool self[4] = {cx == i && e.cy == j, cx + 1 == i && e.cy == j,
+                              cx == i && e.cy + 1 == j, cx + 1 == i && e.cy + 1 == j};
+        double lam0 = 0.0, rp = 0.0;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            if (self[t]) lam0 = DADD(lam0, wg[t]);
+            else rp = DADD(rp, DMUL(wg[t], sV[sr[t]]));
+        }
+        const double v = DDIV(DADD(e.hl, DMUL(P.beta, rp)), DSUB(1.0, DMUL(P.beta, lam0)));
+        if (v < best) best = v;
+    }
+    return best;
+}
+
 __global__ void k_coarse_sweep(DProblem P, const double *__restrict__ Vin, double *__restrict__ Vout,
                                double tol, unsigned long long *res_hist, int sweep,
                                int *sweeps_done)
@@ -243,7 +283,7 @@ constexpr int CT = 16;
 __global__ void __launch_bounds__(CT * CT) k_coarse_sweep_tiles(
     DProblem P, const double *__restrict__ Vin, double *__restrict__ Vout, double tol,
     unsigned long long *res_hist, int sweep, int *sweeps_done, const uint8_t *fprev,
-    uint8_t *fout, int tiles_x, const CoarseRowEntry *rowtab)
+    uint8_t *fout, int tiles_x, const CoarseRowEntry *rowtab, int stage_ok)
 {
     if (sweep > 0 && __longlong_as_double((long long)res_hist[sweep - 1]) < tol) return;
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(sweeps_done, 1);
@@ -265,6 +305,16 @@ __global__ void __launch_bounds__(CT * CT) k_coarse_sweep_tiles(
     }
     __syncthreads();
     const int i = tx * CT + (int)(threadIdx.x % CT), j = ty * CT + (int)(threadIdx.x / CT);
+    const int ib = tx * CT - CH, jb = ty * CT - CH;
+    __shared__ double sV[CSW * CSW];
+    const bool staged = rowtab && PDD_COARSE_SMEM && s_act && stage_ok;
+    if (staged) {
+        for (int e = threadIdx.x; e < CSW * CSW; e += CT * CT) {
+            const int gi = ib + e % CSW, gj = jb + e / CSW;
+            sV[e] = (gi >= 0 && gj >= 0 && gi < n && gj < n) ? Vin[(int64_t)gj * n + gi] : 0.0;
+        }
+        __syncthreads();
+    }
     double res = 0.0;
     int changed = 0;
     if (i < n && j < n) {
@@ -273,7 +323,8 @@ __global__ void __launch_bounds__(CT * CT) k_coarse_sweep_tiles(
         if (!s_act || P.kind[k] != 0) {
             Vout[k] = vin;
         } else {
-            const double v = rowtab ? canon_node_update_rt(P, Vin, i, j, rowtab + (int64_t)j * P.na)
+            const double v = staged ? canon_node_update_rt_s(P, sV, i, j, ib, jb, rowtab + (int64_t)j * P.na)
+                           : rowtab ? canon_node_update_rt(P, Vin, i, j, rowtab + (int64_t)j * P.na)
                                     : canon_node_update(P, Vin, i, j);
             Vout[k] = v;
             res = fabs(DSUB(v, vin));
@@ -555,12 +606,14 @@ void launch_coarse_sweep(const DProblem &P, const double *Vin, double *Vout, dou
 void launch_coarse_sweep_tiles(const DProblem &P, const double *Vin, double *Vout, double tol,
                                unsigned long long *res_hist, int sweep, int *sweeps_done,
                                const uint8_t *fprev, uint8_t *fout, const CoarseRowEntry *rowtab,
-                               cudaStream_t s)
+                               int stage_ok, cudaStream_t s)
 {
     const int tx = (P.n + CT - 1) / CT;
     k_coarse_sweep_tiles<<<tx * tx, CT * CT, 0, s>>>(P, Vin, Vout, tol, res_hist, sweep,
-                                                     sweeps_done, fprev, fout, tx, rowtab);
+                                                     sweeps_done, fprev, fout, tx, rowtab, stage_ok);
 }
+
+int coarse_halo() { return CH; }
 
 void launch_coarse_rowtab(const DProblem &P, CoarseRowEntry *tab, cudaStream_t s)
 {

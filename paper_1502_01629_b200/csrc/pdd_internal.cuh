@@ -83,7 +83,8 @@ void launch_synthesize_rt(const DProblem &P, const double *uhat, const CoarseRow
 void launch_coarse_sweep_tiles(const DProblem &P, const double *Vin, double *Vout, double tol,
                                unsigned long long *res_hist, int sweep, int *sweeps_done,
                                const uint8_t *fprev, uint8_t *fout, const CoarseRowEntry *rowtab,
-                               cudaStream_t s);
+                               int stage_ok, cudaStream_t s);
+int coarse_halo();   // halo of the shared-memory staged coarse sweep (needs reach + 1 <= halo)
 int coarse_tile();
 // fuzzy patches: phi_p init, one Jacobi advection sweep, thresholding
 void launch_fuzzy_init(const DProblem &P, const int16_t *sector, int np, double *phi, cudaStream_t s);

@@ -116,6 +116,7 @@ struct pdd_ctx {
     CoarseRowEntry *crowtab = nullptr;   // coarse row-invariant table (n_c x N_A)
     CoarseRowEntry *frowtab = nullptr;   // the same for the fine-grid synthesis (n x N_A)
     bool coarse_rowuniform = false, fine_rowuniform = false;
+    bool coarse_stage = false;   // coarse reach + 1 <= staged halo
     bool coarse_tiled = false;  // coarse reach < tile: active-tile sweeps
     int *dev_int = nullptr;     // [0] sweeps_done, [1] jump changed flag
     void *rowtab = nullptr;
@@ -441,6 +442,7 @@ pdd_status pdd_create(const pdd_problem *fine, const pdd_problem *coarse, int32_
     // active-tile coarse sweeps need the stencil reach (+ the bilinear corner) inside one tile
     // (computed here: the host arrays of the problem are valid only during this call)
     ctx->coarse_tiled = coarse && reach_cells(coarse) + 2.0 < (double)coarse_tile();
+    ctx->coarse_stage = coarse && reach_cells(coarse) + 1.0 <= (double)coarse_halo();
     {
         auto rok = [](const pdd_coef &c) { return c.kind == PDD_COEF_CONST || c.kind == PDD_COEF_ROW; };
         if (coarse)
@@ -531,7 +533,8 @@ pdd_status pdd_coarse_solve(pdd_ctx *ctx, double tol_c, int64_t max_sweeps, pdd_
                                           ctx->res_hist, (int)issued, ctx->dev_int,
                                           ctx->cflag + ((issued + 1) & 1) * ctn * ctn,
                                           ctx->cflag + (issued & 1) * ctn * ctn,
-                                          use_rt ? ctx->crowtab : nullptr, s);
+                                          use_rt ? ctx->crowtab : nullptr,
+                                          ctx->coarse_stage ? 1 : 0, s);
             else
                 launch_coarse_sweep(Pc, ctx->uc[issued & 1], ctx->uc[(issued + 1) & 1], tol_c,
                                     ctx->res_hist, (int)issued, ctx->dev_int, s);
