@@ -510,6 +510,49 @@ __global__ void k_synthesize_rt(DProblem P, const double *__restrict__ uhat,
     }
 }
 
+// k_synthesize_rt on 16 x 16 node tiles with u_hat's tile + halo (CH cells) staged in shared
+// memory: the 4 N_A gathers per node hit shared memory.  Same operations: bit-identical.
+__global__ void __launch_bounds__(256) k_synthesize_rt_s(DProblem P, const double *__restrict__ uhat,
+                                                         const CoarseRowEntry *__restrict__ tab,
+                                                         uint8_t *__restrict__ astar, int tiles_x)
+{
+    __shared__ double sU[CSW * CSW];
+    const int n = P.n;
+    const int tx = blockIdx.x % tiles_x, ty = blockIdx.x / tiles_x;
+    const int ib = tx * 16 - CH, jb = ty * 16 - CH;
+    for (int e = threadIdx.x; e < CSW * CSW; e += 256) {
+        const int gi = ib + e % CSW, gj = jb + e / CSW;
+        sU[e] = (gi >= 0 && gj >= 0 && gi < n && gj < n) ? uhat[(int64_t)gj * n + gi] : 0.0;
+    }
+    __syncthreads();
+    const int i = tx * 16 + (int)(threadIdx.x & 15), j = ty * 16 + (int)(threadIdx.x >> 4);
+    if (i >= n || j >= n) return;
+    const int64_t k = (int64_t)j * n + i;
+    if (P.kind[k] != 0) { astar[k] = 255; return; }
+    const double top = (double)(n - 1);
+    const CoarseRowEntry *row = tab + (int64_t)j * P.na;
+    double best = INFINITY;
+    int arg = -1;
+    for (int a = 0; a < P.na; ++a) {
+        const CoarseRowEntry e = row[a];
+        double gx = DADD((double)i, e.bxq);
+        if (gx < 0.0) gx = 0.0;
+        if (gx > top) gx = top;
+        int cx = (int)floor(gx);
+        if (cx > n - 2) cx = n - 2;
+        const double tx2 = DSUB(gx, (double)cx);
+        const double ux = DSUB(1.0, tx2);
+        const int s0 = (e.cy - jb) * CSW + (cx - ib);
+        double sm = DMUL(DMUL(ux, e.uy), sU[s0]);
+        sm = DADD(sm, DMUL(DMUL(tx2, e.uy), sU[s0 + 1]));
+        sm = DADD(sm, DMUL(DMUL(ux, e.ty), sU[s0 + CSW]));
+        sm = DADD(sm, DMUL(DMUL(tx2, e.ty), sU[s0 + CSW + 1]));
+        const double v = DADD(e.hl, DMUL(P.beta, sm));
+        if (v < best) { best = v; arg = a; }
+    }
+    astar[k] = (uint8_t)arg;
+}
+
 __global__ void k_successor(DProblem P, double M, const uint8_t *__restrict__ astar,
                             int32_t *__restrict__ succ)
 {
@@ -652,8 +695,13 @@ void launch_prolong(int nc, const double *uc, int n, double *out, cudaStream_t s
 }
 
 void launch_synthesize_rt(const DProblem &P, const double *uhat, const CoarseRowEntry *tab,
-                          uint8_t *astar, cudaStream_t s)
+                          uint8_t *astar, int stage_ok, cudaStream_t s)
 {
+    if (stage_ok && PDD_COARSE_SMEM) {
+        const int tx = (P.n + 15) / 16;
+        k_synthesize_rt_s<<<tx * tx, 256, 0, s>>>(P, uhat, tab, astar, tx);
+        return;
+    }
     const int64_t N = (int64_t)P.n * P.n;
     k_synthesize_rt<<<grid_for(N, 128), 128, 0, s>>>(P, uhat, tab, astar);
 }

@@ -77,7 +77,7 @@ struct CoarseRowEntry {
 void launch_coarse_rowtab(const DProblem &P, CoarseRowEntry *tab, cudaStream_t s);
 // synthesis with the same row-invariant table built on the fine grid (bit-identical)
 void launch_synthesize_rt(const DProblem &P, const double *uhat, const CoarseRowEntry *tab,
-                          uint8_t *astar, cudaStream_t s);
+                          uint8_t *astar, int stage_ok, cudaStream_t s);
 // active-tile form of the same sweep (bit-identical; fprev/fout: per-tile change flags; rowtab:
 // the row-invariant table or NULL)
 void launch_coarse_sweep_tiles(const DProblem &P, const double *Vin, double *Vout, double tol,

@@ -117,6 +117,7 @@ struct pdd_ctx {
     CoarseRowEntry *frowtab = nullptr;   // the same for the fine-grid synthesis (n x N_A)
     bool coarse_rowuniform = false, fine_rowuniform = false;
     bool coarse_stage = false;   // coarse reach + 1 <= staged halo
+    bool synth_stage = false;    // fine sigma = 0 reach + 1 <= staged halo (synthesis)
     bool coarse_tiled = false;  // coarse reach < tile: active-tile sweeps
     int *dev_int = nullptr;     // [0] sweeps_done, [1] jump changed flag
     void *rowtab = nullptr;
@@ -444,6 +445,12 @@ pdd_status pdd_create(const pdd_problem *fine, const pdd_problem *coarse, int32_
     ctx->coarse_tiled = coarse && reach_cells(coarse) + 2.0 < (double)coarse_tile();
     ctx->coarse_stage = coarse && reach_cells(coarse) + 1.0 <= (double)coarse_halo();
     {
+        // the synthesis foot has no diffusion branch: its reach is h max|f| / dx
+        pdd_problem f0 = *fine;
+        f0.p = 0;
+        ctx->synth_stage = reach_cells(&f0) + 1.0 <= (double)coarse_halo();
+    }
+    {
         auto rok = [](const pdd_coef &c) { return c.kind == PDD_COEF_CONST || c.kind == PDD_COEF_ROW; };
         if (coarse)
             ctx->coarse_rowuniform = rok(coarse->speed) && rok(coarse->drift[0]) &&
@@ -581,7 +588,7 @@ pdd_status pdd_synthesize(pdd_ctx *ctx)
     if (ctx->fine_rowuniform && !std::getenv("PDD_SYNTH_NORT")) {   // env: A/B only
         // row-invariant part of the synthesis hoisted into a (row, control) table: bit-identical
         launch_coarse_rowtab(ctx->F.d, ctx->frowtab, s);
-        launch_synthesize_rt(ctx->F.d, ctx->uhat, ctx->frowtab, ctx->astar, s);
+        launch_synthesize_rt(ctx->F.d, ctx->uhat, ctx->frowtab, ctx->astar, ctx->synth_stage ? 1 : 0, s);
         ctx->launches += 3;
     } else {
         launch_synthesize(ctx->F.d, ctx->uhat, ctx->astar, s);
