@@ -114,6 +114,8 @@ struct TileState {
     double *tile_minu;       // min u_hat over free nodes (patchy bucket key)
     double *tile_res;        // last in-tile residual (or verification residual)
     double *tile_chg;        // net change of the last visit (0 if not visited this round)
+    float *tile_edge;        // 4 per tile: bound on the last visit's change within H of the tile's
+                             // west / east / south / north side (what a neighbour's stencil reads)
     int16_t *tile_lab;       // up to 4 distinct patch labels per tile (-1 unused)
     uint8_t *tile_orient;    // first in-tile sweep orientation (bit 0: -x, bit 1: -y)
     int32_t *tile_stamp;     // sweep id that wrote tile_chg (valid iff == RoundCtl::sweep_id)
@@ -196,6 +198,7 @@ struct SweepLaunch {
     const int32_t *list;
     int n_list;
     double *tile_res, *tile_chg;
+    float *tile_edge;
     int k_inner;
     double *out;             // check mode with output (apply operator)
     const void *rowtab;      // RowEntry array [n][na_pad]

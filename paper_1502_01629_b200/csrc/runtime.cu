@@ -327,6 +327,7 @@ static size_t layout(pdd_ctx *c, void *ws, const pdd_problem *f, const pdd_probl
     T.tile_minu = cv.take<double>(tmax);
     T.tile_res = cv.take<double>(tmax);
     T.tile_chg = cv.take<double>(tmax);
+    T.tile_edge = cv.take<float>(4 * (size_t)tmax);
     T.tile_lab = cv.take<int16_t>(4 * (size_t)tmax);
     T.tile_orient = cv.take<uint8_t>(tmax);
     T.tile_stamp = cv.take<int32_t>(tmax);
@@ -836,6 +837,7 @@ static SweepLaunch make_launch(pdd_ctx *ctx, const int32_t *list, int n_list, in
     L.n_list = n_list;
     L.tile_res = ctx->T.tile_res;
     L.tile_chg = ctx->T.tile_chg;
+    L.tile_edge = ctx->T.tile_edge;
     L.k_inner = k_inner;
     L.out = out;
     L.rowtab = ctx->rowtab;

@@ -98,6 +98,7 @@ struct KP {
     TileGeom g;
     const int32_t *list;
     double *tile_res, *tile_chg;
+    float *tile_edge;
     int k_inner;
     double *out;
     const void *rowtab;
@@ -420,6 +421,9 @@ __device__ __forceinline__ void row_table(const KP<real> &A, real *s_u, const re
 #ifndef PDD_FASTWB
 #define PDD_FASTWB 1     // single-sweep visits: write-back without reading the old V
 #endif
+#ifndef PDD_EDGE_ACT
+#define PDD_EDGE_ACT 0   // 1: re-activate a tile only for changes in the neighbour's facing strip
+#endif
 #ifndef PDD_GSG
 #define PDD_GSG 1    // path 1 (general stencil) uses the Gauss-Seidel tile sweeps of sweep_gs.cuh
 #endif
@@ -519,6 +523,7 @@ __device__ __forceinline__ void sweep_tile(const KP<real> &A, int t, unsigned ch
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     real res = 0;
     int done_sweeps = CHECK ? 1 : A.k_inner;
+    float edge4[4] = {-1.f, -1.f, -1.f, -1.f};   // path 3: per-side change bounds (else: chg)
     if constexpr (PATH == 3 && sizeof(real) == 4) {
         const int ot = A.tile_orient ? A.tile_orient[t] : 0;
         const int kin = (ot & 4) ? min(A.k_inner, A.k_coherent) : A.k_inner;
@@ -527,7 +532,7 @@ __device__ __forceinline__ void sweep_tile(const KP<real> &A, int t, unsigned ch
         const int sbase = (A.tile_sweeps && !(ot & 4)) ? A.tile_sweeps[t] : 0;
         done_sweeps = tile_gs4<CPL, WY, WX, CHECK>(A, s_u, s_ctrl, s_prog, s_red, pitch,
                                                    A.g.cstride, H, i0, j0, D, kin, res, Vref, ot & 3,
-                                                   sbase);
+                                                   sbase, edge4);
     } else if constexpr (PATH == 1 && PDD_GSG) {
         const int ot = A.tile_orient ? A.tile_orient[t] : 0;
         const int kin = (ot & 4) ? min(A.k_inner, A.k_coherent) : A.k_inner;
@@ -615,6 +620,9 @@ __device__ __forceinline__ void sweep_tile(const KP<real> &A, int t, unsigned ch
     for (int w = 0; w < NW; ++w) cm = fmax(cm, s_red[w]);
     if (threadIdx.x == 0) {
         A.tile_chg[t] = cm;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            A.tile_edge[4 * t + q] = edge4[q] >= 0.f ? fminf(edge4[q], (float)cm) : (float)cm;
         if (A.tile_stamp) A.tile_stamp[t] = A.ctl->sweep_id + 1;
         if (A.tile_sweeps) A.tile_sweeps[t] += done_sweeps;
         if (A.nu_counter)   // node-updates actually performed (early exit aware)
@@ -762,6 +770,7 @@ static cudaError_t launch_one(const SweepLaunch &L, cudaStream_t s)
     A.list = L.list;
     A.tile_res = L.tile_res;
     A.tile_chg = L.tile_chg;
+    A.tile_edge = L.tile_edge;
     A.k_inner = L.k_inner;
     A.out = L.out;
     A.rowtab = L.rowtab;
@@ -971,6 +980,7 @@ __global__ void k_tile_init(DProblem P, TileGeom g, const double *uhat, const in
         T.tile_minu[t] = uhat ? (s_free > 0 ? key : INFINITY) : 0.0;
         T.tile_res[t] = s_free > 0 ? INFINITY : 0.0;
         T.tile_chg[t] = 0.0;
+        for (int q = 0; q < 4; ++q) T.tile_edge[4 * t + q] = 0.f;
         for (int k = 0; k < 4; ++k) T.tile_lab[4 * t + k] = (int16_t)s_lab[k];
         // coherent tile: (nearly) every u_hat difference has the tile's sign in x and in y, so
         // one sweep in that orientation carries information across the whole tile
@@ -1037,7 +1047,16 @@ __global__ void k_activate(TileGeom g, TileState T, int out_list, double tol, do
                         if ((dx | dy) == 0 || ax < 0 || ay < 0 || ax >= g.tiles_x || ay >= g.tiles_y)
                             continue;
                         const int nb = ay * g.tiles_x + ax;
-                        if (T.tile_chg[nb] >= tol_act && (!ctl || T.tile_stamp[nb] == sid) &&
+                        // the change of the neighbour's side strip facing this tile (a diagonal
+                        // neighbour's corner: the smaller of its two strips bounds it)
+                        double cf = T.tile_chg[nb];
+                        if (PDD_EDGE_ACT) {
+                            const float *ed = T.tile_edge + 4 * (size_t)nb;   // W, E, S, N
+                            const float ex = dx < 0 ? ed[1] : dx > 0 ? ed[0] : INFINITY;
+                            const float ey = dy < 0 ? ed[3] : dy > 0 ? ed[2] : INFINITY;
+                            cf = fmin(cf, (double)fminf(ex, ey));
+                        }
+                        if (cf >= tol_act && (!ctl || T.tile_stamp[nb] == sid) &&
                             (upw < 0.0 || T.tile_minu[nb] <= T.tile_minu[t] + upw)) {
                             need = true;
                             break;

@@ -143,7 +143,8 @@ template <int CPL, int WY, int WX, bool CHECK, bool XNEG, bool EDGE>
 __device__ __forceinline__ void row_gs4(const KP<float> &A, float *s_u, const float *s_ctrl,
                                         volatile int *s_prog, int pitch_rt, int cstride_rt, int H,
                                         int i0, int ly, int gj, int jj, int base, int lead,
-                                        float D, bool last, float &res, double Vref)
+                                        float D, bool last, float &res, double Vref, float &eW,
+                                        float &eE, float &rowmax)
 {
     // compile-time smem geometry (P3_PITCH / P3_CSTRIDE, checked against the host's TileGeom):
     // every window row / shifted-copy offset becomes an immediate of the LDS / STS
@@ -266,8 +267,15 @@ __device__ __forceinline__ void row_gs4(const KP<float> &A, float *s_u, const fl
             rd[gg] = sk ? 0.f : m - old[gg];
             dlt[gg] = CHECK ? 0.f : rd[gg];
         }
-        if (last)
-            res = fmaxf(res, fmaxf(fmaxf(fabsf(rd[0]), fabsf(rd[1])), fmaxf(fabsf(rd[2]), fabsf(rd[3]))));
+        {
+            const float gm = fmaxf(fmaxf(fabsf(rd[0]), fabsf(rd[1])), fmaxf(fabsf(rd[2]), fabsf(rd[3])));
+            if (last) res = fmaxf(res, gm);
+            if constexpr (PDD_EDGE_ACT != 0) {
+                rowmax = fmaxf(rowmax, gm);
+                if (G == 0) eW = fmaxf(eW, gm);        // columns 0..3 cover the west strip (H <= 4)
+                if (G == NG - 1) eE = fmaxf(eE, gm);   // and TW-4..TW-1 the east strip
+            }
+        }
         {
             // lane L < 16 writes node L & 3 of the group into shifted copy L >> 2 (one STS)
             float x = nv[0];
@@ -310,13 +318,40 @@ __device__ __forceinline__ void row_gs4(const KP<float> &A, float *s_u, const fl
     }
 }
 
+// CTA-wide maxima of the per-warp side bounds (all threads get them)
+__device__ __forceinline__ void tile_edges_out(float eW, float eE, float eS, float eN,
+                                               float (*s_edge)[NW], float edge4[4])
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    float v[4] = {eW, eE, eS, eN};
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[q] = fmaxf(v[q], __shfl_xor_sync(FULL, v[q], o));
+    __syncthreads();
+    if (lane == 0)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) s_edge[q][warp] = v[q];
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        float m = 0.f;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) m = fmaxf(m, s_edge[q][w]);
+        edge4[q] = m;
+    }
+}
+
 template <int CPL, int WY, int WX, bool CHECK>
 __device__ __forceinline__ int tile_gs4(const KP<float> &A, float *s_u, const float *s_ctrl,
                                          volatile int *s_prog, double *s_red, int pitch,
                                          int cstride, int H, int i0, int j0, float D, int k_inner,
-                                         float &res, double Vref, int o0, int sbase)
+                                         float &res, double Vref, int o0, int sbase,
+                                         float edge4[4])
 {
     constexpr int NG = TW3 / 4;
+    __shared__ float s_edge[4][NW];
+    float eW = 0.f, eE = 0.f, eS = 0.f, eN = 0.f;   // per-side change bounds, summed over sweeps
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int n = A.P.n;
@@ -333,6 +368,7 @@ __device__ __forceinline__ int tile_gs4(const KP<float> &A, float *s_u, const fl
         const int orient = ((A.oxor >> (2 * ((sbase + sw) & 3))) & 3) ^ o0;   // o0: downstream first
         const bool xneg = orient & 1, yneg = orient & 2;
         const int base = sw * NG;              // progress counters are monotone across sweeps
+        float sW = 0.f, sE = 0.f, sS = 0.f, sN = 0.f;   // this sweep's side maxima (this warp)
         for (int k = 0; k < TH3 / NW; ++k) {
             const int jj = warp + NW * k;      // position in this sweep's row order
             const int ly = yneg ? TH3 - 1 - jj : jj;
@@ -341,21 +377,30 @@ __device__ __forceinline__ int tile_gs4(const KP<float> &A, float *s_u, const fl
                 if (lane == 0) s_prog[jj] = base + NG;
                 continue;
             }
+            float rowmax = 0.f;
             if (edge_tile) {
                 if (xneg)
                     row_gs4<CPL, WY, WX, CHECK, true, true>(A, s_u, s_ctrl, s_prog, pitch, cstride, H, i0,
-                                                            ly, gj, jj, base, lead, D, last, res, Vref);
+                                                            ly, gj, jj, base, lead, D, last, res, Vref, sW, sE, rowmax);
                 else
                     row_gs4<CPL, WY, WX, CHECK, false, true>(A, s_u, s_ctrl, s_prog, pitch, cstride, H, i0,
-                                                             ly, gj, jj, base, lead, D, last, res, Vref);
+                                                             ly, gj, jj, base, lead, D, last, res, Vref, sW, sE, rowmax);
             } else {
                 if (xneg)
                     row_gs4<CPL, WY, WX, CHECK, true, false>(A, s_u, s_ctrl, s_prog, pitch, cstride, H, i0,
-                                                             ly, gj, jj, base, lead, D, last, res, Vref);
+                                                             ly, gj, jj, base, lead, D, last, res, Vref, sW, sE, rowmax);
                 else
                     row_gs4<CPL, WY, WX, CHECK, false, false>(A, s_u, s_ctrl, s_prog, pitch, cstride, H, i0,
-                                                              ly, gj, jj, base, lead, D, last, res, Vref);
+                                                              ly, gj, jj, base, lead, D, last, res, Vref, sW, sE, rowmax);
             }
+            if constexpr (PDD_EDGE_ACT != 0) {
+                if (ly < P3_HMAX) sS = fmaxf(sS, rowmax);            // rows of the south strip
+                if (ly >= TH3 - P3_HMAX) sN = fmaxf(sN, rowmax);     // and of the north strip
+            }
+        }
+        if constexpr (PDD_EDGE_ACT != 0) {
+            if (edge_tile) sW = sE = sS = sN = fmaxf(fmaxf(sW, sE), fmaxf(fmaxf(sS, sN), res));
+            eW += sW; eE += sE; eS += sS; eN += sN;
         }
         if (CHECK) break;
         float r = res;
@@ -369,9 +414,13 @@ __device__ __forceinline__ int tile_gs4(const KP<float> &A, float *s_u, const fl
             for (int w = 0; w < NW; ++w) m = fmax(m, s_red[w]);
             __syncthreads();                   // s_red is reused by the next sweep
             if (sw == 0) first = m;
-            if (m < A.early_tol || m < A.early_rel * first) return sw + 1;   // sweeps done
+            if (m < A.early_tol || m < A.early_rel * first) {
+                if constexpr (PDD_EDGE_ACT != 0) tile_edges_out(eW, eE, eS, eN, s_edge, edge4);
+                return sw + 1;   // sweeps done
+            }
         }
     }
+    if constexpr (!CHECK && PDD_EDGE_ACT != 0) tile_edges_out(eW, eE, eS, eN, s_edge, edge4);
     return sweeps;
 }
 
