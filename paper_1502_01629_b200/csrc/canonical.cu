@@ -75,6 +75,9 @@ __global__ void k_init_values(DProblem P, double *V)
 #ifndef PDD_COARSE_SMEM
 #define PDD_COARSE_SMEM 1   // tiled coarse sweep: V tile + halo staged in shared memory
 #endif
+#ifndef PDD_COARSE_RTSMEM
+#define PDD_COARSE_RTSMEM 1   // ... and the tile's rows of the row-invariant table
+#endif
 #ifndef PDD_EXACT_MIN
 #define PDD_EXACT_MIN 0   // measured slower on sm_100a (C5 coarse 31 vs 24 ms): kept as an option
 #endif
@@ -307,11 +310,17 @@ __global__ void __launch_bounds__(CT * CT) k_coarse_sweep_tiles(
     const int i = tx * CT + (int)(threadIdx.x % CT), j = ty * CT + (int)(threadIdx.x / CT);
     const int ib = tx * CT - CH, jb = ty * CT - CH;
     __shared__ double sV[CSW * CSW];
+    extern __shared__ CoarseRowEntry sRT[];      // the tile's CT rows of the row table (if sized)
     const bool staged = rowtab && PDD_COARSE_SMEM && s_act && stage_ok;
     if (staged) {
         for (int e = threadIdx.x; e < CSW * CSW; e += CT * CT) {
             const int gi = ib + e % CSW, gj = jb + e / CSW;
             sV[e] = (gi >= 0 && gj >= 0 && gi < n && gj < n) ? Vin[(int64_t)gj * n + gi] : 0.0;
+        }
+        if (stage_ok > 1) {
+            const int rows = min(CT, n - ty * CT);
+            for (int e = threadIdx.x; e < rows * P.na; e += CT * CT)
+                sRT[e] = rowtab[(int64_t)ty * CT * P.na + e];
         }
         __syncthreads();
     }
@@ -323,7 +332,9 @@ __global__ void __launch_bounds__(CT * CT) k_coarse_sweep_tiles(
         if (!s_act || P.kind[k] != 0) {
             Vout[k] = vin;
         } else {
-            const double v = staged ? canon_node_update_rt_s(P, sV, i, j, ib, jb, rowtab + (int64_t)j * P.na)
+            const double v = staged ? canon_node_update_rt_s(P, sV, i, j, ib, jb,
+                                                             stage_ok > 1 ? sRT + (j - ty * CT) * P.na
+                                                                          : rowtab + (int64_t)j * P.na)
                            : rowtab ? canon_node_update_rt(P, Vin, i, j, rowtab + (int64_t)j * P.na)
                                     : canon_node_update(P, Vin, i, j);
             Vout[k] = v;
@@ -652,8 +663,22 @@ void launch_coarse_sweep_tiles(const DProblem &P, const double *Vin, double *Vou
                                int stage_ok, cudaStream_t s)
 {
     const int tx = (P.n + CT - 1) / CT;
-    k_coarse_sweep_tiles<<<tx * tx, CT * CT, 0, s>>>(P, Vin, Vout, tol, res_hist, sweep,
-                                                     sweeps_done, fprev, fout, tx, rowtab, stage_ok);
+    // stage the tile's rows of the row table too when they fit (stage_ok = 2)
+    size_t dyn = 0;
+    if (stage_ok && rowtab && PDD_COARSE_RTSMEM) {
+        dyn = sizeof(CoarseRowEntry) * CT * (size_t)P.na;
+        if (dyn > 64 * 1024) dyn = 0;
+        else {
+            static bool attr = false;
+            if (!attr) {
+                cudaFuncSetAttribute(k_coarse_sweep_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+                attr = true;
+            }
+            stage_ok = 2;
+        }
+    }
+    k_coarse_sweep_tiles<<<tx * tx, CT * CT, dyn, s>>>(P, Vin, Vout, tol, res_hist, sweep,
+                                                       sweeps_done, fprev, fout, tx, rowtab, stage_ok);
 }
 
 int coarse_halo() { return CH; }
