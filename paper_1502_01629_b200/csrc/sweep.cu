@@ -950,25 +950,46 @@ __global__ void k_tile_init(DProblem P, TileGeom g, const double *uhat, const in
         if (labels) {
             const int lab = labels[k];
             if (lab >= 0) {
+                // most nodes of a tile share its first label: look before claiming a slot
                 for (int sl = 0; sl < 4; ++sl) {
-                    const int old = atomicCAS(&s_lab[sl], -1, lab);
-                    if (old == -1 || old == lab) break;
+                    const int cur = ((volatile int *)s_lab)[sl];
+                    if (cur == lab) break;
+                    if (cur == -1) {
+                        const int old = atomicCAS(&s_lab[sl], -1, lab);
+                        if (old == -1 || old == lab) break;
+                    }
                 }
             }
         }
     }
-    atomicAdd(&s_free, cnt);
-    if (uhat) {
-        atomicAdd(&s_dx, dx);
-        atomicAdd(&s_dy, dy);
-        atomicAdd(&s_sx[0], sx[0]);
-        atomicAdd(&s_sx[1], sx[1]);
-        atomicAdd(&s_sy[0], sy[0]);
-        atomicAdd(&s_sy[1], sy[1]);
+    // warp-level reductions first: one shared atomic per warp and quantity
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        cnt += __shfl_xor_sync(FULL, cnt, o);
+        mn = fmin(mn, __shfl_xor_sync(FULL, mn, o));
+        mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
+        sm += __shfl_xor_sync(FULL, sm, o);
+        dx += __shfl_xor_sync(FULL, dx, o);
+        dy += __shfl_xor_sync(FULL, dy, o);
+        sx[0] += __shfl_xor_sync(FULL, sx[0], o);
+        sx[1] += __shfl_xor_sync(FULL, sx[1], o);
+        sy[0] += __shfl_xor_sync(FULL, sy[0], o);
+        sy[1] += __shfl_xor_sync(FULL, sy[1], o);
     }
-    if (mn < INFINITY) atomicMin(&s_min, (unsigned long long)__double_as_longlong(fmax(mn, 0.0)));
-    if (mx > 0.0) atomicMax(&s_max, (unsigned long long)__double_as_longlong(mx));
-    if (sm != 0.0) atomicAdd(&s_sum, sm);
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&s_free, cnt);
+        if (uhat) {
+            atomicAdd(&s_dx, dx);
+            atomicAdd(&s_dy, dy);
+            atomicAdd(&s_sx[0], sx[0]);
+            atomicAdd(&s_sx[1], sx[1]);
+            atomicAdd(&s_sy[0], sy[0]);
+            atomicAdd(&s_sy[1], sy[1]);
+        }
+        if (mn < INFINITY) atomicMin(&s_min, (unsigned long long)__double_as_longlong(fmax(mn, 0.0)));
+        if (mx > 0.0) atomicMax(&s_max, (unsigned long long)__double_as_longlong(mx));
+        if (sm != 0.0) atomicAdd(&s_sum, sm);
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
         T.tile_free[t] = s_free;
