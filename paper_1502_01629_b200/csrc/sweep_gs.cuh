@@ -77,7 +77,7 @@ __device__ __forceinline__ int prog_acquire(volatile int *p)
 // row against the 8-warp row pipeline's 2 x 8 = 16 groups of lead, so the ring of warps has slack
 // and a single-sweep visit fills / drains the pipeline in 62 instead of 78 group steps.
 #ifndef PDD_P3_WIDE
-#define PDD_P3_WIDE 1
+#define PDD_P3_WIDE 0
 #endif
 #ifndef PDD_P3_TW
 #define PDD_P3_TW (PDD_P3_WIDE ? 128 : 64)
