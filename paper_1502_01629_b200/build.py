@@ -19,11 +19,14 @@ LIB = os.path.join(HERE, "libpdd.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",
           "-I", os.path.join(ROOT, "include"), "-Xptxas", "-v"]
-UNITS = {
-    "canonical.cu": ["--fmad=false"],
-    "sweep.cu": [],
-    "runtime.cu": [],
-}
+# (object, source, extra flags): sweep.cu is compiled twice, the second time as the 16 x 128
+# path-3 tile in namespace pdd::wide (runtime.cu picks the geometry per problem)
+UNITS = [
+    ("canonical.o", "canonical.cu", ["--fmad=false"]),
+    ("sweep.o", "sweep.cu", []),
+    ("sweep_wide.o", "sweep.cu", ["-DPDD_P3_WIDE=1", "-DPDD_WIDE_UNIT=1"]),
+    ("runtime.o", "runtime.cu", []),
+]
 
 
 def _nvcc():
@@ -46,18 +49,24 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str = Non
     if not force and os.path.exists(lib) and os.path.getmtime(lib) >= newest:
         return lib
     dflags = [f"-D{d}" for d in defines]
-    objs = []
-    for unit, extra in UNITS.items():
-        obj = os.path.join(bdir, unit.replace(".cu", ".o"))
+    objs, procs = [], []
+    for oname, unit, extra in UNITS:      # the units compile in parallel
+        obj = os.path.join(bdir, oname)
         cmd = [_nvcc(), *ARCH, *COMMON, *dflags, *extra, "-c", os.path.join(CSRC, unit), "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        if verbose or r.returncode != 0:
-            sys.stderr.write(r.stdout + r.stderr)
-        if r.returncode != 0:
-            raise RuntimeError(f"nvcc failed for {unit}")
-        with open(os.path.join(bdir, unit + ".ptxas.txt"), "w") as f:
-            f.write(r.stderr)
+        procs.append((oname, unit, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE,
+                                                    text=True)))
         objs.append(obj)
+    failed = []
+    for oname, unit, pr in procs:
+        out, err = pr.communicate()
+        if verbose or pr.returncode != 0:
+            sys.stderr.write(out + err)
+        if pr.returncode != 0:
+            failed.append(unit)
+        with open(os.path.join(bdir, oname.replace(".o", ".cu") + ".ptxas.txt"), "w") as f:
+            f.write(err)
+    if failed:
+        raise RuntimeError(f"nvcc failed for {failed}")
     cmd = [_nvcc(), *ARCH, "-shared", "-o", lib, *objs, "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

@@ -251,6 +251,10 @@ int sweep_tile_rows();
 // compile-time shared-memory geometry of the path-3 kernel (rows pitch, copy stride, max halo)
 void p3_geometry(int &pitch, int &cstride, int &hmax);
 void p3_tile(int &tw, int &th);   // path-3 tile columns / rows
+// the 16 x 128 path-3 tile (sweep.cu built with PDD_WIDE_UNIT=1)
+cudaError_t launch_sweep_wide(const SweepLaunch &L, cudaStream_t s);
+void p3_geometry_wide(int &pitch, int &cstride, int &hmax);
+void p3_tile_wide(int &tw, int &th);
 // Build the row-stencil table on the device; false if no supported window fits.
 bool rowtab_build_device(const DProblem &P, int napad, int H, int precision, int *scratch,
                          void *tab, size_t tab_bytes, int &WY, int &WX, int &oxmin, int &oxmax,

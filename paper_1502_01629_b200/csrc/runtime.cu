@@ -762,6 +762,23 @@ static bool row_uniform(const pdd_problem *p)
     return p->cost.kind == PDD_COEF_CONST;
 }
 
+// Path-3 tile geometry.  The 16 x 128 tile fills the 8-warp row pipeline with slack (27 % more
+// node-updates/s than 32 x 64) but spans twice the x-distance, and the
+// kernel's fp32 tile-relative values carry a noise floor of about 1 ulp of half the tile's value
+// range: on coarse grids (128 dx ~ 1) that floor exceeds a 1e-7 tolerance.  So the wide tile is
+// taken only when it spans at most 1/8 in x (C4, C5: 4097^2, 8193^2 on [-2,2]^2);
+// PDD_P3_TILE=64|128 in the environment forces one geometry (A/B measurements).
+static bool p3_use_wide(const pdd_problem *p)
+{
+    if (const char *e = getenv("PDD_P3_TILE")) {
+        const int t = atoi(e);
+        if (t == 64) return false;
+        if (t == 128) return true;
+    }
+    const double dx = (p->hi - p->lo) / (p->n - 1);
+    return 128.0 * dx <= 0.125 + 1e-12;
+}
+
 static pdd_status prepare(pdd_ctx *ctx, int kernel_req)
 {
     if (ctx->prepared_kernel == kernel_req) return PDD_OK;
@@ -795,6 +812,11 @@ static pdd_status prepare(pdd_ctx *ctx, int kernel_req)
     TileGeom g{};
     int tw3 = 64, th3 = 32;
     p3_tile(tw3, th3);
+    if (g4 && p3_use_wide(p)) {
+        p3_tile_wide(tw3, th3);
+        p3_geometry_wide(p3_pitch, p3_cstride, p3_hmax);
+        if (H > p3_hmax) return fail(ctx, PDD_E_STENCIL, "wide path-3 tile: halo %d too large", H);
+    }
     g.TW = (path == 2 && !g4) ? rowtab_tw(WY, WX) : (g4 ? tw3 : 64);
     g.TH = g4 ? th3 : sweep_tile_rows();
     g.H = H;

@@ -37,7 +37,17 @@
 
 #include <algorithm>
 
+// PDD_WIDE_UNIT: this file compiled a second time with PDD_P3_WIDE=1 (build.py) gives the
+// 16 x 128 path-3 tile in namespace pdd::wide; the host picks the geometry per problem
+// (runtime.cu: p3_use_wide) and launch_sweep forwards path-3 launches of 128-column tiles here
+#ifndef PDD_WIDE_UNIT
+#define PDD_WIDE_UNIT 0
+#endif
+
 namespace pdd {
+#if PDD_WIDE_UNIT
+namespace wide {
+#endif
 
 #ifndef PDD_MIN_BLOCKS
 #define PDD_MIN_BLOCKS 0    // override of the __launch_bounds__ min CTAs per SM (0 = per path)
@@ -892,10 +902,21 @@ void p3_tile(int &tw, int &th)
 
 cudaError_t launch_sweep(const SweepLaunch &L, cudaStream_t s)
 {
+#if !PDD_WIDE_UNIT
+    if (L.path == 3 && L.g.TW == 128) return launch_sweep_wide(L, s);
+#endif
     if (L.precision == 32) return L.check ? dispatch<float, true>(L, s) : dispatch<float, false>(L, s);
     return L.check ? dispatch<double, true>(L, s) : dispatch<double, false>(L, s);
 }
 
+#if PDD_WIDE_UNIT
+static_assert(TW3 == 128, "the wide unit is built with PDD_P3_WIDE=1");
+}  // namespace wide
+
+cudaError_t launch_sweep_wide(const SweepLaunch &L, cudaStream_t s) { return wide::launch_sweep(L, s); }
+void p3_geometry_wide(int &pitch, int &cstride, int &hmax) { wide::p3_geometry(pitch, cstride, hmax); }
+void p3_tile_wide(int &tw, int &th) { wide::p3_tile(tw, th); }
+#else
 // ------------------------------------------------------------------ tile bookkeeping
 __global__ void k_tile_init(DProblem P, TileGeom g, const double *uhat, const int16_t *labels,
                             TileState T, double coh_thr)
@@ -1401,5 +1422,7 @@ bool rowtab_build_device(const DProblem &P, int napad, int H, int precision, int
     oxmax = h[3];
     return true;
 }
+
+#endif  // !PDD_WIDE_UNIT
 
 }  // namespace pdd

@@ -178,3 +178,38 @@ def test_schedules_reach_the_same_fixed_point(mode, schedule, policy):
     st = s.solve(mode, tol=1e-7, k_inner=4, schedule=schedule, bucket_policy=policy)
     assert st["converged"] == 1
     assert np.abs(s.get_values() - ref["V"]).max() <= 5e-5 * np.abs(ref["V"]).max()
+
+
+# The 16 x 128 path-3 tile (sweep.cu's second build, pdd::wide) is chosen automatically only on
+# fine grids (runtime.cu p3_use_wide: C4, C5 full size, covered by test_gpu_fullsize.py); here
+# PDD_P3_TILE=128 forces it on small grids with ragged tails in both directions.
+@pytest.mark.parametrize("cfg,n", [("C2", 201), ("C4", 257), ("C5", 257), ("C5", 300)])
+@pytest.mark.parametrize("kernel", [0, 2])
+def test_wide_tile_operator_parity(monkeypatch, cfg, n, kernel):
+    monkeypatch.setenv("PDD_P3_TILE", "128")
+    inst = I.make_config(cfg, n=n)
+    V = _random_field(inst, 5)
+    ref, _ = O.apply(inst, V)
+    s = _solver(inst, 32)
+    out, res = s.apply_operator(V, kernel=kernel)
+    assert np.abs(out - ref).max() < 2e-6 * np.abs(V).max()
+    assert abs(res - np.abs(ref - V)[inst.kind == 0].max()) < 4e-6
+
+
+@pytest.mark.parametrize("mode", ["patchy", "static"])
+def test_wide_tile_solve_parity(monkeypatch, mode):
+    # tol 1e-6: on a 513^2 grid the wide tile spans 1 in x and its fp32 noise floor sits near 1e-7
+    monkeypatch.setenv("PDD_P3_TILE", "128")
+    inst = I.make_config("C5", n=513)
+    ref = O.jacobi(inst, tol=_tight_tol(inst, 2e-11), max_sweeps=10**6)
+    s = _solver(inst, 32)
+    if mode == "patchy":
+        s.coarse_solve(inst.tol_coarse)
+        s.synthesize()
+        s.build_patches(inst.n_patches)
+    else:
+        s.build_static(*inst.static_blocks)
+    st = s.solve(mode, tol=1e-6, k_inner=4)
+    assert st["converged"] == 1
+    V = s.get_values()
+    assert np.abs(V - ref["V"]).max() <= 5e-5 * np.abs(ref["V"]).max()
