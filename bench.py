@@ -343,6 +343,10 @@ def main():
             "kernel_node_updates_per_s": nu / max(t_sweep, 1e-12),
             "kernel_seconds_share_of_step": t_sweep / max(t_local, 1e-12),
             "peak_basis": "derived: 148 SM x 128 FP32 lanes x 2 x 1965 MHz (guide unit counts)"}
+    if static:
+        # the same kernel in the static solve's full rounds (16 x 128 path-3 tiles at C4/C5,
+        # runtime.cu p3_use_wide; the patchy step above runs 32 x 64 tiles)
+        static["kernel_alu_frac"] = static["kernel_node_updates_per_s"] * flop_per_update / 1e12 / peak
     prof = os.path.join(ROOT, "profiles", "sweep_traffic.json")
     if os.path.exists(prof):
         try:
@@ -406,6 +410,7 @@ def main():
                                    f"tol {args.tol:g}) on {inst.n}^2",
                        "grid": inst.n, "controls": inst.n_controls, "branches": 2 * inst.p,
                        "patches": inst.n_patches, "k_inner": args.k_inner if args.k_inner is not None else {"patchy": "auto (1)", "static": "auto (4)"},
+                       "path3_tile": {"patchy": "32x64", "static": "16x128" if 128 * inst.dx <= 0.125 + 1e-12 else "32x64"},
                        "l2": "inputs larger than L2 (V fp64 %d MB)" % (inst.n * inst.n * 8 >> 20),
                        "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
             "time_to_converge": {"patchy_s": t_solve / args.steps,

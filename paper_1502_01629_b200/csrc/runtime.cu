@@ -141,6 +141,7 @@ struct pdd_ctx {
     TileGeom g{};
     int n_tiles = 0;
     int prepared_kernel = -1;
+    bool prepared_wide = false;      // path-3 tile of the prepared geometry (p3_use_wide)
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     cudaEvent_t evp[2][64] = {};  // per-round sweep-kernel timing inside a batch (lazy)
     long long launches = 0;     // kernels enqueued by this context (all calls)
@@ -766,9 +767,12 @@ static bool row_uniform(const pdd_problem *p)
 // node-updates/s than 32 x 64) but spans twice the x-distance, and the
 // kernel's fp32 tile-relative values carry a noise floor of about 1 ulp of half the tile's value
 // range: on coarse grids (128 dx ~ 1) that floor exceeds a 1e-7 tolerance.  So the wide tile is
-// taken only when it spans at most 1/8 in x (C4, C5: 4097^2, 8193^2 on [-2,2]^2);
-// PDD_P3_TILE=64|128 in the environment forces one geometry (A/B measurements).
-static bool p3_use_wide(const pdd_problem *p)
+// taken only when it spans at most 1/8 in x (C4, C5: 4097^2, 8193^2 on [-2,2]^2), and only for
+// the static squares and operator applications: the patchy schedule's single-sweep visits along
+// the u_hat front do fewer wasted updates on the finer 32 x 64 tiles (measured C5 pipeline
+// 182 vs 191 ms, C4 172 vs 183 ms), the static rounds gain the kernel's throughput (C5 0.78 vs
+// 1.07 s).  PDD_P3_TILE=64|128 in the environment forces one geometry (A/B measurements).
+static bool p3_use_wide(const pdd_problem *p, bool patchy)
 {
     if (const char *e = getenv("PDD_P3_TILE")) {
         const int t = atoi(e);
@@ -776,13 +780,14 @@ static bool p3_use_wide(const pdd_problem *p)
         if (t == 128) return true;
     }
     const double dx = (p->hi - p->lo) / (p->n - 1);
-    return 128.0 * dx <= 0.125 + 1e-12;
+    return !patchy && 128.0 * dx <= 0.125 + 1e-12;
 }
 
-static pdd_status prepare(pdd_ctx *ctx, int kernel_req)
+static pdd_status prepare(pdd_ctx *ctx, int kernel_req, bool patchy)
 {
-    if (ctx->prepared_kernel == kernel_req) return PDD_OK;
     const pdd_problem *p = &ctx->fine;
+    const bool want_wide = p3_use_wide(p, patchy);
+    if (ctx->prepared_kernel == kernel_req && ctx->prepared_wide == want_wide) return PDD_OK;
     const DProblem &d = ctx->F.d;
     const int H = halo_of(p);
     if (H > 8) return fail(ctx, PDD_E_STENCIL, "foot points reach %.2f cells; tile halo limited to 8",
@@ -812,7 +817,7 @@ static pdd_status prepare(pdd_ctx *ctx, int kernel_req)
     TileGeom g{};
     int tw3 = 64, th3 = 32;
     p3_tile(tw3, th3);
-    if (g4 && p3_use_wide(p)) {
+    if (g4 && want_wide) {
         p3_tile_wide(tw3, th3);
         p3_geometry_wide(p3_pitch, p3_cstride, p3_hmax);
         if (H > p3_hmax) return fail(ctx, PDD_E_STENCIL, "wide path-3 tile: halo %d too large", H);
@@ -844,6 +849,7 @@ static pdd_status prepare(pdd_ctx *ctx, int kernel_req)
     for (int t = 0; t < ctx->n_tiles; ++t) all[t] = t;
     CK(cudaMemcpy(ctx->T.all_list, all.data(), sizeof(int32_t) * all.size(), cudaMemcpyHostToDevice));
     ctx->prepared_kernel = kernel_req;
+    ctx->prepared_wide = want_wide;
     return PDD_OK;
 }
 
@@ -1038,7 +1044,7 @@ pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
         return fail(ctx, PDD_E_STATE, "patchy solve needs pdd_synthesize and pdd_build_patches");
     if (o->mode == 1 && ctx->labels_mode != 2)
         return fail(ctx, PDD_E_STATE, "static solve needs pdd_build_static");
-    pdd_status ps = prepare(ctx, o->kernel);
+    pdd_status ps = prepare(ctx, o->kernel, o->mode == 0);
     if (ps != PDD_OK) return ps;
     cudaStream_t s = ctx->stream;
     const DProblem &d = ctx->F.d;
@@ -1264,7 +1270,7 @@ pdd_status pdd_apply_operator(pdd_ctx *ctx, double *out, int32_t kernel, double 
 {
     if (!ctx) return fail(nullptr, PDD_E_INVALID, "ctx is NULL");
     if (kernel < 0 || kernel > 3) return fail(ctx, PDD_E_INVALID, "kernel must be 0..3");
-    pdd_status ps = prepare(ctx, kernel);
+    pdd_status ps = prepare(ctx, kernel, false);
     if (ps != PDD_OK) return ps;
     cudaStream_t s = ctx->stream;
     const size_t N = (size_t)ctx->fine.n * ctx->fine.n;
