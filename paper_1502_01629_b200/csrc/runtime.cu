@@ -770,7 +770,7 @@ static bool row_uniform(const pdd_problem *p)
 // taken only when it spans at most 1/8 in x (C4, C5: 4097^2, 8193^2 on [-2,2]^2), and only for
 // the static squares and operator applications: the patchy schedule's single-sweep visits along
 // the u_hat front do fewer wasted updates on the finer 32 x 64 tiles (measured C5 pipeline
-// 182 vs 191 ms, C4 172 vs 183 ms), the static rounds gain the kernel's throughput (C5 0.78 vs
+// 182 vs 188 ms, C4 the same), the static rounds gain the kernel's throughput (C5 0.78 vs
 // 1.07 s).  PDD_P3_TILE=64|128 in the environment forces one geometry (A/B measurements).
 static bool p3_use_wide(const pdd_problem *p, bool patchy)
 {
