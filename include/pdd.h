@@ -117,7 +117,10 @@ typedef struct {
     int64_t max_rounds;  /* cap on tile rounds                                               */
     double delta;        /* patchy bucket width in value units; 0 = automatic; < 0 = off      */
     int32_t kernel;      /* 0 auto, 1 general stencil, 2 row-table stencil, 3 row-table one
-                            node per warp step (A/B only)                                    */
+                            node per warp step (A/B only).  The fp32 row-table kernel's tile
+                            is 32 x 64 nodes, or 16 x 128 for static solves on grids where
+                            128 dx <= 1/8 (env PDD_P3_TILE=64|128
+                            forces one geometry)                                             */
     int32_t schedule;    /* 0 rounds (default): rounds over the list of active tiles, every
                             tile visit an in-tile Gauss-Seidel solve; patchy admits tiles in
                             buckets of min u_hat of width delta;
