@@ -355,7 +355,7 @@ def main():
             roof["traffic"] = pj["dram_bytes_per_node_update"] * per_launch_updates
             roof["traffic_basis"] = ("dram bytes per node-update from ncu --set full (%s) x the "
                                      "average node-updates per sweep launch of this run; "
-                                     "algorithmic bytes per node-update ~4.6" % pj["source"])
+                                     "algorithmic bytes per node-update ~18.4 at k_inner 1" % pj["source"])
         except Exception:
             pass
 
