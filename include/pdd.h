@@ -119,15 +119,23 @@ typedef struct {
     int32_t kernel;      /* 0 auto, 1 general stencil, 2 row-table stencil, 3 row-table one
                             node per warp step (A/B only).  The fp32 row-table kernel's tile
                             is 32 x 64 nodes, or 16 x 128 for static solves on grids where
-                            128 dx <= 1/8 (env PDD_P3_TILE=64|128
-                            forces one geometry)                                             */
+                            128 dx <= 1/8 (pdd_set_tile_cols forces one
+                            geometry)                                                        */
     int32_t schedule;    /* 0 rounds (default): rounds over the list of active tiles, every
                             tile visit an in-tile Gauss-Seidel solve; patchy admits tiles in
                             buckets of min u_hat of width delta;
                             1 ordered: Gauss-Seidel passes over the tiles in key order (u_hat
                             for patchy, block-lexicographic for static), each tile waiting for
                             its lower-key neighbours (delta = key slack)                     */
-    int32_t reserved[2];
+    int32_t early_exit_off; /* 1: every tile visit does all k_inner sweeps (A/B; default 0: a
+                            visit stops after the first sweep changing no node by >= tol)   */
+    int32_t bucket_policy;  /* patchy, schedule 0: 0 moving front (the threshold advances every
+                            round, faster while a round under-fills the GPU); 1 classic
+                            Delta-stepping (a bucket opens once the previous one settled); 2
+                            upstream-ready (no front: a tile waits for unconverged neighbours
+                            with min u_hat lower by more than delta)                        */
+    int32_t trace;       /* > 0: one line per round on stderr (one round per batch)          */
+    int32_t reserved;
 } pdd_solve_opts;
 
 typedef struct {
@@ -136,14 +144,21 @@ typedef struct {
     int64_t tiles_processed;
     int64_t verify_passes;
     double final_residual;     /* last full-grid Jacobi residual ||T(V) - V||_inf            */
-    double apost_bound;        /* final_residual / (1 - beta): bound on ||V - V*||_inf       */
+    double apost_bound;        /* final_residual / (1 - beta): bound on ||V - V*||_inf; NaN
+                                  for exit problems (lambda = 0, beta = 1: no such bound)   */
     double seconds_total;      /* wall time of pdd_solve on the stream (CUDA events)        */
     double seconds_sweep;      /* summed duration of the sweep-kernel launches (events)      */
     double seconds_verify;
     int32_t converged;
     int32_t n_tiles;
-    int32_t kernel_used;       /* 1 general, 2 row-table                                    */
-    int32_t patches_converged; /* patches with no active tile at the end                    */
+    int32_t kernel_used;       /* 1 general, 2 row-table (fp64 / one node per step), 3 fp32
+                                  row-table four nodes per step                           */
+    int32_t patches_active;    /* patches holding free nodes (each had an active tile)      */
+    int32_t patches_converged; /* patches whose own residual max_{x_i in patch} |T(V) - V|
+                                  in the last verification pass is < tol (
+                                  pdd_get_patch_residuals)                                */
+    int32_t tile_cols, tile_rows, tiles_x;   /* tile geometry of the solve (tile t covers
+                                  columns (t % tiles_x) tile_cols.., rows (t / tiles_x) tile_rows..) */
 } pdd_solve_stats;
 
 typedef struct {
@@ -229,9 +244,25 @@ pdd_status pdd_get_controls(pdd_ctx *ctx, uint8_t *dst, int32_t dst_on_device); 
 pdd_status pdd_get_labels(pdd_ctx *ctx, int16_t *dst, int32_t dst_on_device);
 pdd_status pdd_get_successors(pdd_ctx *ctx, int32_t *dst, int32_t dst_on_device);
 
-/* Per-patch convergence report of the last pdd_solve: round index at which each patch last had
- * an active tile (n_patches + 1 entries, the last one for orphans). */
+/* Per-patch convergence report of the last pdd_solve (each patch iterates until its
+ * own sup-norm residual is below tol).  n_patches + 1 entries (the last one = orphans); dst is
+ * HOST memory; count is clipped to n_patches + 1.
+ *   pdd_get_patch_rounds:    activation trace: the last round in which a tile holding free nodes
+ *                            of the patch was active (-1: never) = max over those tiles of
+ *                            pdd_get_tile_rounds
+ *   pdd_get_patch_residuals: max over the patch's free nodes of |T(V) - V| in the last full-grid
+ *                            verification pass (the kernel's arithmetic), 0 for an empty patch
+ *   pdd_get_tile_rounds:     per tile (pdd_solve_stats.n_tiles, geometry tile_cols x tile_rows)
+ *                            the last round that activated it (-1: never); PDD_E_STATE before
+ *                            the first pdd_solve. */
 pdd_status pdd_get_patch_rounds(pdd_ctx *ctx, int32_t *dst, int32_t count);
+pdd_status pdd_get_patch_residuals(pdd_ctx *ctx, double *dst, int32_t count);
+pdd_status pdd_get_tile_rounds(pdd_ctx *ctx, int32_t *dst, int32_t count);
+
+/* Force the fp32 row-table kernel's tile geometry for the following solves / operator
+ * applications: 0 automatic, 64 (32 x 64 tiles) or 128 (16 x 128).  For A/B
+ * measurements and the forced-geometry parity tests; PDD_E_INVALID for any other value. */
+pdd_status pdd_set_tile_cols(pdd_ctx *ctx, int32_t cols);
 
 /* The upwind diffusion ball analysis of P:528-697 (host arithmetic, no context, no GPU).
  * Inputs: f_min, f_max = min / max of |f(x,a)| over Omega x A (> 0), sigma_norm = ||sigma||_inf

@@ -196,15 +196,16 @@ class Solver:
     def solve(self, mode="patchy", tol: float = 1e-6, k_inner: Optional[int] = None,
               max_rounds: int = 200000, delta: float = 0.0, kernel: int = 0,
               schedule: str = "rounds", raise_on_noconverge: bool = True,
-              early_exit: bool = True, bucket_policy: int = 0) -> dict:
+              early_exit: bool = True, bucket_policy: int = 0, trace: bool = False) -> dict:
         o = N.pdd_solve_opts()
         o.mode = MODE_PATCHY if mode in ("patchy", 0) else MODE_STATIC
         if k_inner is None:   # 0 = automatic in libpdd: 1 patchy / 4 static,
             k_inner = 0       # 4 for a patchy grid that fits one wave of sweep CTAs
         o.k_inner, o.tol, o.max_rounds, o.delta, o.kernel = int(k_inner), float(tol), int(max_rounds), float(delta), int(kernel)
         o.schedule = 1 if schedule in ("ordered", 1) else 0
-        o.reserved[0] = 0 if early_exit else 1
-        o.reserved[1] = int(bucket_policy)
+        o.early_exit_off = 0 if early_exit else 1
+        o.bucket_policy = int(bucket_policy)
+        o.trace = 1 if trace else 0
         st = N.pdd_solve_stats()
         r = N.lib().pdd_solve(self._ctx, C.byref(o), C.byref(st))
         if r != N.PDD_OK and (raise_on_noconverge or r != N.PDD_E_NOCONVERGE):
@@ -262,6 +263,20 @@ class Solver:
         a = np.empty(count, dtype=np.int32)
         self._ck(N.lib().pdd_get_patch_rounds(self._ctx, C.c_void_p(a.ctypes.data), int(count)))
         return a
+
+    def get_patch_residuals(self, count: int) -> np.ndarray:
+        a = np.empty(count, dtype=np.float64)
+        self._ck(N.lib().pdd_get_patch_residuals(self._ctx, C.c_void_p(a.ctypes.data), int(count)))
+        return a
+
+    def get_tile_rounds(self, count: int) -> np.ndarray:
+        a = np.empty(count, dtype=np.int32)
+        self._ck(N.lib().pdd_get_tile_rounds(self._ctx, C.c_void_p(a.ctypes.data), int(count)))
+        return a
+
+    def set_tile_cols(self, cols: int) -> None:
+        """Force the fp32 row-table tile geometry (0 auto, 64 or 128; A/B and tests)."""
+        self._ck(N.lib().pdd_set_tile_cols(self._ctx, int(cols)))
 
     def kernel_launches(self) -> int:
         return int(N.lib().pdd_kernel_launches(self._ctx))

@@ -10,8 +10,16 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-# PDD_LIB: development override (A/B builds of the same sources); default is the in-tree lib
-LIB_PATH = os.environ.get("PDD_LIB") or os.path.join(HERE, "libpdd.so")
+LIB_PATH = os.path.join(HERE, "libpdd.so")
+
+
+def use_library(path: str) -> None:
+    """Development A/B only (scripts/): load another build of the same sources instead of the
+    in-tree libpdd.so.  Must be called before the first lib() call."""
+    global LIB_PATH
+    if _lib is not None:
+        raise RuntimeError("libpdd is already loaded")
+    LIB_PATH = path
 
 PDD_OK, PDD_E_INVALID, PDD_E_NOCONVERGE, PDD_E_IO, PDD_E_CUDA, PDD_E_STATE, PDD_E_NOMEM, \
     PDD_E_STENCIL = range(8)
@@ -22,7 +30,8 @@ EXPORTS = ["pdd_version", "pdd_workspace_bytes", "pdd_create", "pdd_coarse_solve
            "pdd_synthesize", "pdd_build_patches", "pdd_build_static", "pdd_solve",
            "pdd_apply_operator", "pdd_get_values", "pdd_set_values", "pdd_get_uhat",
            "pdd_get_coarse_values", "pdd_get_controls", "pdd_get_labels", "pdd_get_successors",
-           "pdd_get_patch_rounds", "pdd_kernel_launches", "pdd_last_error", "pdd_destroy",
+           "pdd_get_patch_rounds", "pdd_get_patch_residuals", "pdd_get_tile_rounds",
+           "pdd_set_tile_cols", "pdd_kernel_launches", "pdd_last_error", "pdd_destroy",
            "pdd_regime_analyse", "pdd_fuzzy_scratch_bytes", "pdd_build_fuzzy_patches"]
 
 
@@ -43,7 +52,8 @@ class pdd_problem(C.Structure):
 class pdd_solve_opts(C.Structure):
     _fields_ = [("mode", C.c_int32), ("k_inner", C.c_int32), ("tol", C.c_double),
                 ("max_rounds", C.c_int64), ("delta", C.c_double), ("kernel", C.c_int32),
-                ("schedule", C.c_int32), ("reserved", C.c_int32 * 2)]
+                ("schedule", C.c_int32), ("early_exit_off", C.c_int32),
+                ("bucket_policy", C.c_int32), ("trace", C.c_int32), ("reserved", C.c_int32)]
 
 
 class pdd_solve_stats(C.Structure):
@@ -53,7 +63,8 @@ class pdd_solve_stats(C.Structure):
                 ("seconds_total", C.c_double), ("seconds_sweep", C.c_double),
                 ("seconds_verify", C.c_double), ("converged", C.c_int32),
                 ("n_tiles", C.c_int32), ("kernel_used", C.c_int32),
-                ("patches_converged", C.c_int32)]
+                ("patches_active", C.c_int32), ("patches_converged", C.c_int32),
+                ("tile_cols", C.c_int32), ("tile_rows", C.c_int32), ("tiles_x", C.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -115,6 +126,9 @@ def lib():
               "pdd_get_successors"):
         getattr(L, f).argtypes = [ctx, vp, C.c_int32]
     L.pdd_get_patch_rounds.argtypes = [ctx, vp, C.c_int32]
+    L.pdd_get_patch_residuals.argtypes = [ctx, vp, C.c_int32]
+    L.pdd_get_tile_rounds.argtypes = [ctx, vp, C.c_int32]
+    L.pdd_set_tile_cols.argtypes = [ctx, C.c_int32]
     L.pdd_fuzzy_scratch_bytes.argtypes = [C.c_int32, C.c_int32, C.POINTER(C.c_size_t)]
     L.pdd_build_fuzzy_patches.argtypes = [ctx, C.c_int32, C.c_double, C.c_double, C.c_int64, vp,
                                           C.c_size_t, C.POINTER(pdd_fuzzy_stats)]

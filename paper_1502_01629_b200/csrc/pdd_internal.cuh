@@ -116,14 +116,21 @@ struct TileState {
     double *tile_chg;        // net change of the last visit (0 if not visited this round)
     float *tile_edge;        // 4 per tile: bound on the last visit's change within H of the tile's
                              // west / east / south / north side (what a neighbour's stencil reads)
-    int16_t *tile_lab;       // up to 4 distinct patch labels per tile (-1 unused)
+    // the distinct patch labels of each tile (free nodes only; orphans = n_patches), CSR:
+    // tile t holds tile_lab_ids[tile_lab_off[t] .. tile_lab_off[t + 1])
+    int32_t *tile_lab_cnt;   // per tile: number of distinct labels (k_tile_init)
+    int32_t *tile_lab_off;   // n_tiles + 1 offsets (k_scan_offsets)
+    int16_t *tile_lab_ids;   // capacity n*n: a tile has at most as many labels as nodes
+    int32_t *tile_round;     // per tile: last activation round that took it (-1: never)
+    int n_slots;             // patch slots: n_patches + 1 (the last one = orphans); 0 = none
     uint8_t *tile_orient;    // first in-tile sweep orientation (bit 0: -x, bit 1: -y)
     int32_t *tile_stamp;     // sweep id that wrote tile_chg (valid iff == RoundCtl::sweep_id)
     int32_t *tile_sweeps;    // in-tile sweeps done so far this solve (orientation schedule)
     int32_t *list[2];        // active tile lists
     int32_t *all_list;       // tiles with free nodes
-    int32_t *patch_round;    // per patch: last round with an active tile
-    double *patch_res;       // per patch: max residual of its active tiles
+    int32_t *patch_round;    // per patch: last round with an active tile (activation trace)
+    unsigned long long *patch_res;   // per patch: max |T(V) - V| over its free nodes in the
+                                     // last verification pass (fp64 bits, >= 0 orders as u64)
     void *counters;          // ActCounters (device)
     // ordered schedule
     double *tile_key;        // sort key per tile
@@ -188,12 +195,18 @@ struct OrderArgs {
     int pass;                     // pass id (>= 1)
     double tol;
     double key_slack;             // wait only for neighbours with key < own key - key_slack
+    int32_t *tile_round;          // activation trace (pass id of the tile's last visit) and
+    const int32_t *lab_off;       //   the per-patch rounds through the tile label CSR
+    const int16_t *lab_ids;
+    int32_t *patch_round;
 };
 
 struct SweepLaunch {
     DProblem P;
     double *V;
     const int16_t *labels;
+    unsigned long long *patch_res;       // check mode: per-patch residual max (or NULL)
+    int n_slots;                         // patch slots of labels / patch_res
     TileGeom g;
     const int32_t *list;
     int n_list;
@@ -233,6 +246,8 @@ void launch_round_reset(RoundCtl *ctl, double thr, cudaStream_t s);
 void launch_sort_round(const RoundCtl *ctl, const ActCounters *c, const double *key, int32_t *list,
                        cudaStream_t s);
 
+// tile bookkeeping of a solve: free counts, min u_hat keys, orientations and (labels != NULL)
+// the CSR of the distinct patch labels of every tile (three kernels)
 void launch_tile_init(const DProblem &P, const TileGeom &g, const double *uhat,
                       const int16_t *labels, TileState &T, cudaStream_t s, double coh_thr = 2.0);
 void launch_set_values(const DProblem &P, int mode, const double *uhat, double *V,

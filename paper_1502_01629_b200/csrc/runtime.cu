@@ -27,6 +27,21 @@ namespace {
 
 thread_local std::string g_err;
 
+// A/B switches of the development builds only: the product library (built without PDD_DEV) reads
+// no environment variable, so a stray variable cannot change its schedule or tile geometry.
+#ifndef PDD_DEV
+#define PDD_DEV 0
+#endif
+const char *dev_env(const char *name)
+{
+#if PDD_DEV
+    return std::getenv(name);
+#else
+    (void)name;
+    return nullptr;
+#endif
+}
+
 constexpr size_t kAlign = 256;
 constexpr int kMaxPatches = 32768;
 constexpr int64_t kMaxCoarseSweeps = 1 << 20;
@@ -119,6 +134,11 @@ struct pdd_ctx {
     bool coarse_stage = false;   // coarse reach + 1 <= staged halo
     bool synth_stage = false;    // fine sigma = 0 reach + 1 <= staged halo (synthesis)
     bool coarse_tiled = false;  // coarse reach < tile: active-tile sweeps
+    // fine-problem quantities that need the caller's host arrays: computed once in pdd_create
+    // (those arrays are only valid during that call; ctx->fine / ctx->coarse keep no pointers)
+    double fine_reach = 0.0;
+    int fine_halo = 0;
+    bool fine_row_uniform_all = false;   // row_uniform(): speed, drift, sigma and cost
     int *dev_int = nullptr;     // [0] sweeps_done, [1] jump changed flag
     void *rowtab = nullptr;
     size_t rowtab_bytes = 0;
@@ -142,6 +162,7 @@ struct pdd_ctx {
     int n_tiles = 0;
     int prepared_kernel = -1;
     bool prepared_wide = false;      // path-3 tile of the prepared geometry (p3_use_wide)
+    int force_tile_cols = 0;         // pdd_set_tile_cols: 0 auto, 64 or 128
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     cudaEvent_t evp[2][64] = {};  // per-round sweep-kernel timing inside a batch (lazy)
     long long launches = 0;     // kernels enqueued by this context (all calls)
@@ -216,6 +237,8 @@ static pdd_status validate(const pdd_problem *p, const char *what)
                 return fail(nullptr, PDD_E_INVALID, "%s: obstacles need lambda > 0", what);
     return PDD_OK;
 }
+
+static bool row_uniform(const pdd_problem *p);
 
 static double coef_max_abs(const pdd_coef &c, int n)
 {
@@ -329,7 +352,10 @@ static size_t layout(pdd_ctx *c, void *ws, const pdd_problem *f, const pdd_probl
     T.tile_res = cv.take<double>(tmax);
     T.tile_chg = cv.take<double>(tmax);
     T.tile_edge = cv.take<float>(4 * (size_t)tmax);
-    T.tile_lab = cv.take<int16_t>(4 * (size_t)tmax);
+    T.tile_lab_cnt = cv.take<int32_t>(tmax);
+    T.tile_lab_off = cv.take<int32_t>((size_t)tmax + 1);
+    T.tile_lab_ids = cv.take<int16_t>(N);   // a tile has at most as many labels as nodes
+    T.tile_round = cv.take<int32_t>(tmax);
     T.tile_orient = cv.take<uint8_t>(tmax);
     T.tile_stamp = cv.take<int32_t>(tmax);
     T.tile_sweeps = cv.take<int32_t>(tmax);
@@ -337,7 +363,7 @@ static size_t layout(pdd_ctx *c, void *ws, const pdd_problem *f, const pdd_probl
     T.list[1] = cv.take<int32_t>(tmax);
     T.all_list = cv.take<int32_t>(tmax);
     T.patch_round = cv.take<int32_t>(kMaxPatches + 1);
-    T.patch_res = cv.take<double>(kMaxPatches + 1);
+    T.patch_res = cv.take<unsigned long long>(kMaxPatches + 1);
     T.counters = cv.take<ActCounters>(1);
     T.tile_key = cv.take<double>(tmax);
     T.tile_group = cv.take<int32_t>(tmax);
@@ -460,6 +486,9 @@ pdd_status pdd_create(const pdd_problem *fine, const pdd_problem *coarse, int32_
         ctx->fine_rowuniform = rok(fine->speed) && rok(fine->drift[0]) && rok(fine->drift[1]) &&
                                rok(fine->cost);
     }
+    ctx->fine_reach = reach_cells(fine);
+    ctx->fine_halo = halo_of(fine);
+    ctx->fine_row_uniform_all = row_uniform(fine);
     // aligned base
     char *base = (char *)workspace;
     const size_t mis = (size_t)((uintptr_t)base % kAlign);
@@ -491,6 +520,14 @@ pdd_status pdd_create(const pdd_problem *fine, const pdd_problem *coarse, int32_
     if (s != PDD_OK) {
         pdd_destroy(ctx);
         return s;
+    }
+    // the caller may free its host arrays once this call returns (include/pdd.h): drop them
+    for (pdd_problem *p : {&ctx->fine, &ctx->coarse}) {
+        p->controls = nullptr;
+        p->kind = nullptr;
+        p->sector = nullptr;
+        p->cost_ctrl = nullptr;
+        for (int k = 0; k < 8; ++k) const_cast<pdd_coef *>(coef_ptr(p, k))->data = nullptr;
     }
     *out = ctx;
     return PDD_OK;
@@ -527,8 +564,8 @@ pdd_status pdd_coarse_solve(pdd_ctx *ctx, double tol_c, int64_t max_sweeps, pdd_
     int done = 0;
     bool converged = false;
     int64_t batch = 8;
-    const bool tiled = ctx->coarse_tiled && !std::getenv("PDD_COARSE_FULL");   // env: A/B only
-    const bool use_rt = tiled && ctx->coarse_rowuniform && !std::getenv("PDD_COARSE_NORT");
+    const bool tiled = ctx->coarse_tiled && !dev_env("PDD_COARSE_FULL");   // env: A/B only
+    const bool use_rt = tiled && ctx->coarse_rowuniform && !dev_env("PDD_COARSE_NORT");
     if (use_rt) {
         launch_coarse_rowtab(Pc, ctx->crowtab, s);
         ctx->launches++;
@@ -587,7 +624,7 @@ pdd_status pdd_synthesize(pdd_ctx *ctx)
     if (!ctx->coarse_done) return fail(ctx, PDD_E_STATE, "pdd_synthesize needs pdd_coarse_solve first");
     cudaStream_t s = ctx->stream;
     launch_prolong(ctx->coarse.n, ctx->uc_final, ctx->fine.n, ctx->uhat, s);
-    if (ctx->fine_rowuniform && !std::getenv("PDD_SYNTH_NORT")) {   // env: A/B only
+    if (ctx->fine_rowuniform && !dev_env("PDD_SYNTH_NORT")) {   // env: A/B only
         // row-invariant part of the synthesis hoisted into a (row, control) table: bit-identical
         launch_coarse_rowtab(ctx->F.d, ctx->frowtab, s);
         launch_synthesize_rt(ctx->F.d, ctx->uhat, ctx->frowtab, ctx->astar, ctx->synth_stage ? 1 : 0, s);
@@ -772,30 +809,27 @@ static bool row_uniform(const pdd_problem *p)
 // the u_hat front do fewer wasted updates on the finer 32 x 64 tiles (measured C5 pipeline
 // 182 vs 188 ms, C4 the same), the static rounds gain the kernel's throughput (C5 0.78 vs
 // 1.07 s).  PDD_P3_TILE=64|128 in the environment forces one geometry (A/B measurements).
-static bool p3_use_wide(const pdd_problem *p, bool patchy)
+static bool p3_use_wide(const pdd_problem *p, bool patchy, int force_cols)
 {
-    if (const char *e = getenv("PDD_P3_TILE")) {
-        const int t = atoi(e);
-        if (t == 64) return false;
-        if (t == 128) return true;
-    }
+    if (force_cols == 64) return false;    // pdd_set_tile_cols (A/B runs, forced-geometry tests)
+    if (force_cols == 128) return true;
     const double dx = (p->hi - p->lo) / (p->n - 1);
     return !patchy && 128.0 * dx <= 0.125 + 1e-12;
 }
 
 static pdd_status prepare(pdd_ctx *ctx, int kernel_req, bool patchy)
 {
-    const pdd_problem *p = &ctx->fine;
-    const bool want_wide = p3_use_wide(p, patchy);
+    const pdd_problem *p = &ctx->fine;   // sizes only: its host arrays are gone (pdd_create)
+    const bool want_wide = p3_use_wide(p, patchy, ctx->force_tile_cols);
     if (ctx->prepared_kernel == kernel_req && ctx->prepared_wide == want_wide) return PDD_OK;
     const DProblem &d = ctx->F.d;
-    const int H = halo_of(p);
+    const int H = ctx->fine_halo;
     if (H > 8) return fail(ctx, PDD_E_STENCIL, "foot points reach %.2f cells; tile halo limited to 8",
-                           reach_cells(p));
+                           ctx->fine_reach);
     int WY = 0, WX = 0, oxmin = 0, oxmax = 0;
     int path = 1;
     const int napad = na_pad_of(p->n_controls);
-    if (kernel_req != 1 && napad && row_uniform(p)) {
+    if (kernel_req != 1 && napad && ctx->fine_row_uniform_all) {
         // the compact row stencils are built on the device (k_rowtab_extent / k_rowtab_fill)
         if (rowtab_build_device(d, napad, H, ctx->precision, ctx->dev_int + 2, ctx->rowtab,
                                 ctx->rowtab_bytes, WY, WX, oxmin, oxmax, ctx->stream) &&
@@ -879,12 +913,12 @@ static SweepLaunch make_launch(pdd_ctx *ctx, const int32_t *list, int n_list, in
     L.tile_free = ctx->T.tile_free;
     // patchy tiles know their downstream orientation from u_hat: two sweeps along it, then the
     // x- and y-flipped ones; static tiles (no u_hat) cycle through all four (P:952-986 analogue)
-    const bool oriented = ctx->mode_patchy && !std::getenv("PDD_NO_ORIENT");   // env: A/B only
+    const bool oriented = ctx->mode_patchy && !dev_env("PDD_NO_ORIENT");   // env: A/B only
     L.tile_orient = oriented ? ctx->T.tile_orient : nullptr;
     L.oxor = oriented ? 0x90 : 0xE4;
-    if (const char *e = std::getenv("PDD_EREL")) L.early_rel = std::atof(e);   // A/B only
-    if (const char *e = std::getenv("PDD_KCOH")) L.k_coherent = std::atoi(e);   // A/B only
-    if (const char *e = std::getenv("PDD_OXOR")) L.oxor = (int)std::strtol(e, nullptr, 0);
+    if (const char *e = dev_env("PDD_EREL")) L.early_rel = std::atof(e);   // A/B only
+    if (const char *e = dev_env("PDD_KCOH")) L.k_coherent = std::atoi(e);   // A/B only
+    if (const char *e = dev_env("PDD_OXOR")) L.oxor = (int)std::strtol(e, nullptr, 0);
     L.nu_counter = &reinterpret_cast<OrdCounters *>(ctx->T.ocounters)->updates;
     return L;
 }
@@ -974,6 +1008,10 @@ static pdd_status ordered_loop(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_
     O.free_sum = &oc->free_sum;
     O.max_res = &oc->max_res;
     O.tol = o->tol;
+    O.tile_round = ctx->T.tile_round;
+    O.lab_off = ctx->T.tile_lab_off;
+    O.lab_ids = ctx->T.tile_lab_ids;
+    O.patch_round = ctx->T.patch_round;
     // patchy: tiles whose min u_hat differ by less than the slack do not wait for each other
     // (near-equal keys are neighbours along a level set of u_hat, not upstream / downstream);
     // opts.delta > 0 sets it, 0 = a quarter of the value change across a tile height at unit
@@ -987,7 +1025,7 @@ static pdd_status ordered_loop(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_
         O.pass = ++pass;
         CK(cudaMemsetAsync(oc, 0, offsetof(OrdCounters, seq), s));
         SweepLaunch L = make_launch(ctx, nullptr, 0, o->k_inner, 0, nullptr);
-        L.early_tol = o->reserved[0] ? 0.0 : o->tol;
+        L.early_tol = o->early_exit_off ? 0.0 : o->tol;
         L.ordered = 1;
         L.order = O;
         CK(cudaEventRecord(ctx->ev[2], s));
@@ -1010,6 +1048,10 @@ static pdd_status ordered_loop(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_
         // nothing left to do: full-grid Jacobi verification
         CK(cudaEventRecord(ctx->ev[2], s));
         SweepLaunch V = make_launch(ctx, ctx->T.all_list, ctx->n_tiles, 1, 1, nullptr);
+        // each patch's own residual max |T(V) - V| over its free nodes
+        CK(cudaMemsetAsync(ctx->T.patch_res, 0, sizeof(unsigned long long) * ctx->T.n_slots, s));
+        V.patch_res = ctx->T.patch_res;
+        V.n_slots = ctx->T.n_slots;
         CK(launch_sweep(V, s));
         ctx->launches++;
         CK(cudaEventRecord(ctx->ev[3], s));
@@ -1053,12 +1095,13 @@ pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
     launch_set_values(d, o->mode == 0 ? 0 : 1, ctx->uhat, ctx->V, s);
     // coherent tile: >= 90 % of its u_hat differences share the tile's sign in x and in y
     // (measured: 0.8 .. 0.99 all within noise on C2 / C4 / C5)
-    const char *cenv = std::getenv("PDD_COH");     // A/B: coherence threshold (> 1: never)
+    const char *cenv = dev_env("PDD_COH");     // A/B: coherence threshold (> 1: never)
+    ctx->T.n_slots = ctx->n_patches + 1;   // patches 0..n_patches-1, orphans n_patches
     launch_tile_init(d, ctx->g, o->mode == 0 ? ctx->uhat : nullptr, ctx->labels, ctx->T, s,
                      cenv ? std::atof(cenv) : 0.9);
     ctx->launches += 2;
     CK(cudaMemsetAsync(ctx->T.patch_round, 0xff, sizeof(int32_t) * (ctx->n_patches + 1), s));
-    CK(cudaMemsetAsync(ctx->T.patch_res, 0, sizeof(double) * (ctx->n_patches + 1), s));
+    CK(cudaMemsetAsync(ctx->T.patch_res, 0, sizeof(unsigned long long) * (ctx->n_patches + 1), s));
     CK(cudaMemsetAsync(ctx->T.ocounters, 0, sizeof(OrdCounters), s));
     CK(cudaGetLastError());
 
@@ -1067,14 +1110,14 @@ pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
     // automatic bucket width: the value change across 6 cells at unit speed (measured on C5 / C4
     // / C3: 6 cells of front travel per round beat 4.8 and 8)
     if (delta == 0.0) {
-        const char *e = std::getenv("PDD_DSCALE");      // A/B only
+        const char *e = dev_env("PDD_DSCALE");      // A/B only
         delta = 6.0 * ctx->fine.h * d.lmax * (e ? std::atof(e) : 1.0);
     }
     double thr = delta > 0.0 ? -1.0 : INFINITY;
     // bucket policy 2 (patchy): no moving threshold; a tile is admitted once its upstream
     // neighbours (min u_hat lower by more than a quarter tile of travel) have converged
     double ready_slack = -1.0;
-    const char *benv = std::getenv("PDD_DBOOST");    // development override of the front boost cap
+    const char *benv = dev_env("PDD_DBOOST");    // development override of the front boost cap
     const double dboost = benv ? std::max(1.0, std::atof(benv)) : 1.0;
     int resident = 148;
     {
@@ -1107,11 +1150,11 @@ pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
     // eikonal 800^2 16 ms vs 34 ms)
     const int k_inner = o->k_inner > 0 ? o->k_inner
                         : (o->mode == 1 ? 4 : (one_wave && ctx->path == 1 ? 4 : 1));
-    if (o->mode == 0 && o->delta == 0.0 && one_wave && o->reserved[1] != 2) {
+    if (o->mode == 0 && o->delta == 0.0 && one_wave && o->bucket_policy != 2) {
         delta = -1.0;
         thr = INFINITY;
     }
-    if (o->mode == 0 && o->reserved[1] == 2) {
+    if (o->mode == 0 && o->bucket_policy == 2) {
         ready_slack = o->delta > 0.0 ? o->delta : 0.25 * ctx->g.TH * ctx->fine.h * d.lmax;
         thr = INFINITY;
         delta = -1.0;
@@ -1121,8 +1164,7 @@ pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
     S.n_tiles = ctx->n_tiles;
     S.kernel_used = ctx->path;
     int cur = 0;
-    const char *tenv = std::getenv("PDD_TRACE");   // development: per-round trace every N rounds
-    const int trace = tenv ? std::max(1, std::atoi(tenv)) : 0;
+    const int trace = o->trace > 0 ? 1 : 0;   // per-round trace on stderr, one round per batch
     double best_verify = INFINITY;
     int stalled = 0;
     // rounds between forced verifications: a tolerance below the noise floor keeps tiles
@@ -1144,9 +1186,9 @@ pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
         c0.delta = delta;
         c0.dboost = dboost;
         c0.resident = resident;
-        c0.policy = o->reserved[1];
+        c0.policy = o->bucket_policy;
         c0.verify_every = verify_every;
-        const char *ue = std::getenv("PDD_UPW");      // A/B: upstream-only re-activation slack
+        const char *ue = dev_env("PDD_UPW");      // A/B: upstream-only re-activation slack
         c0.upw = ue ? std::atof(ue) * ctx->g.TH * ctx->fine.h * d.lmax : -1.0;
         *ctx->h_ctl = c0;
         CK(cudaMemcpyAsync(ctx->rctl, ctx->h_ctl, sizeof(RoundCtl), cudaMemcpyHostToDevice, s));
@@ -1155,20 +1197,20 @@ pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
     }
     int batch = trace ? 1 : 4;
     // patchy: visit each round's tiles in increasing min u_hat (A/B switch PDD_SORT)
-    const char *se = std::getenv("PDD_SORT");
+    const char *se = dev_env("PDD_SORT");
     const bool sort_rounds = o->mode == 0 && se && std::atoi(se) != 0;
-    const char *te = std::getenv("PDD_TACT");   // A/B: neighbour-change activation threshold / tol
+    const char *te = dev_env("PDD_TACT");   // A/B: neighbour-change activation threshold / tol
     const double tact = te ? std::atof(te) : 1.0;
     long long rounds_prev = 0;
     while (o->schedule != 1) {
         if (S.rounds >= o->max_rounds) break;
         CK(cudaEventRecord(ctx->ev[2], s));
         SweepLaunch L = make_launch(ctx, ctx->T.list[cur], ctx->n_tiles, k_inner, 0, nullptr);
-        L.early_tol = o->reserved[0] ? 0.0 : o->tol;   // reserved[0] = 1 disables early exit
+        L.early_tol = o->early_exit_off ? 0.0 : o->tol;   // reserved[0] = 1 disables early exit
         L.ctl = ctx->rctl;
         L.acnt = reinterpret_cast<ActCounters *>(ctx->T.counters);
         L.tile_stamp = ctx->T.tile_stamp;
-        if (!std::getenv("PDD_NO_SCONT")) L.tile_sweeps = ctx->T.tile_sweeps;   // env: A/B only
+        if (!dev_env("PDD_NO_SCONT")) L.tile_sweeps = ctx->T.tile_sweeps;   // env: A/B only
         const long long room = o->max_rounds - S.rounds;
         const int nb = (int)std::min<long long>(batch, std::max<long long>(room, 1));
         if (!ctx->evp[0][0])
@@ -1216,6 +1258,10 @@ pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
         // nothing active (or verify_every rounds since the last one): full-grid verification
         CK(cudaEventRecord(ctx->ev[2], s));
         SweepLaunch V = make_launch(ctx, ctx->T.all_list, ctx->n_tiles, 1, 1, nullptr);
+        // each patch's own residual max |T(V) - V| over its free nodes
+        CK(cudaMemsetAsync(ctx->T.patch_res, 0, sizeof(unsigned long long) * ctx->T.n_slots, s));
+        V.patch_res = ctx->T.patch_res;
+        V.n_slots = ctx->T.n_slots;
         CK(launch_sweep(V, s));
         ctx->launches++;
         launch_round_reset(ctx->rctl, INFINITY, s);   // after a verification every offending
@@ -1248,17 +1294,31 @@ pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
         S.node_updates = (int64_t)upd;   // counted by the sweep kernel: free nodes x sweeps done
     }
     S.final_residual = last_verify;
-    S.apost_bound = last_verify / (1.0 - d.beta);
+    // ||V - V*|| <= r / (1 - beta) needs beta < 1: an exit problem (lambda = 0) has no such bound
+    S.apost_bound = d.beta < 1.0 ? last_verify / (1.0 - d.beta) : NAN;
+    S.tile_cols = ctx->g.TW;
+    S.tile_rows = ctx->g.TH;
+    S.tiles_x = ctx->g.tiles_x;
     S.seconds_total = ms_total * 1e-3;
     S.seconds_sweep = ms_sweep * 1e-3;
     S.seconds_verify = ms_verify * 1e-3;
     S.converged = converged ? 1 : 0;
     {
-        std::vector<int32_t> pr(ctx->n_patches + 1);
-        CK(cudaMemcpy(pr.data(), ctx->T.patch_round, sizeof(int32_t) * pr.size(), cudaMemcpyDeviceToHost));
-        int pc = 0;
-        for (size_t k = 0; k + 1 < pr.size(); ++k) pc += 1;   // all patches converged when solve converged
-        S.patches_converged = converged ? pc : 0;
+        // per-patch convergence flags: a patch (one that holds free nodes, i.e. had an active
+        // tile) is converged when its own residual in the last verification pass is < tol
+        const int ns = ctx->n_patches + 1;
+        std::vector<int32_t> pr(ns);
+        std::vector<double> rs(ns);
+        CK(cudaMemcpy(pr.data(), ctx->T.patch_round, sizeof(int32_t) * ns, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(rs.data(), ctx->T.patch_res, sizeof(double) * ns, cudaMemcpyDeviceToHost));
+        int pc = 0, pa = 0;
+        for (int k = 0; k < ctx->n_patches; ++k) {
+            if (pr[k] < 0) continue;
+            ++pa;
+            if (S.verify_passes > 0 && rs[k] < o->tol) ++pc;
+        }
+        S.patches_active = pa;
+        S.patches_converged = pc;
     }
     if (st) *st = S;
     return converged ? PDD_OK
@@ -1317,6 +1377,31 @@ pdd_status pdd_get_patch_rounds(pdd_ctx *ctx, int32_t *dst, int32_t count)
     if (!ctx || !dst) return fail(ctx, PDD_E_INVALID, "NULL argument");
     if (count > ctx->n_patches + 1) count = ctx->n_patches + 1;
     CK(cudaMemcpy(dst, ctx->T.patch_round, sizeof(int32_t) * count, cudaMemcpyDeviceToHost));
+    return PDD_OK;
+}
+
+pdd_status pdd_get_patch_residuals(pdd_ctx *ctx, double *dst, int32_t count)
+{
+    if (!ctx || !dst) return fail(ctx, PDD_E_INVALID, "NULL argument");
+    if (count > ctx->n_patches + 1) count = ctx->n_patches + 1;
+    CK(cudaMemcpy(dst, ctx->T.patch_res, sizeof(double) * count, cudaMemcpyDeviceToHost));
+    return PDD_OK;
+}
+
+pdd_status pdd_get_tile_rounds(pdd_ctx *ctx, int32_t *dst, int32_t count)
+{
+    if (!ctx || !dst) return fail(ctx, PDD_E_INVALID, "NULL argument");
+    if (ctx->prepared_kernel < 0) return fail(ctx, PDD_E_STATE, "no solve has run");
+    if (count > ctx->n_tiles) count = ctx->n_tiles;
+    CK(cudaMemcpy(dst, ctx->T.tile_round, sizeof(int32_t) * count, cudaMemcpyDeviceToHost));
+    return PDD_OK;
+}
+
+pdd_status pdd_set_tile_cols(pdd_ctx *ctx, int32_t cols)
+{
+    if (!ctx) return fail(nullptr, PDD_E_INVALID, "ctx is NULL");
+    if (cols != 0 && cols != 64 && cols != 128) return fail(ctx, PDD_E_INVALID, "tile cols must be 0, 64 or 128");
+    ctx->force_tile_cols = cols;
     return PDD_OK;
 }
 

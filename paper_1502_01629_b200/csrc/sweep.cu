@@ -125,6 +125,9 @@ struct KP {
     ActCounters *acnt;
     int32_t *tile_stamp;
     int32_t *tile_sweeps;
+    const int16_t *labels;            // check mode: patch labels for the per-patch residuals
+    unsigned long long *patch_res;    //   per-patch max |T(V) - V| (fp64 bits) or NULL
+    int n_slots;
 };
 
 __device__ __forceinline__ float rmin(float a, float b) { return fminf(a, b); }
@@ -310,21 +313,41 @@ __device__ __forceinline__ void row_masks(const DProblem &P, int TW, int i0, int
     }
 }
 
+// Per-patch residual of a verification pass (check mode: each patch's own
+// sup-norm residual): the CTA accumulates max |T(V) - V| per label in shared memory (labels <
+// PRES_SH; larger ones go straight to global atomics) and flushes it once per tile visit.
+constexpr int PRES_SH = 512;
+__device__ __forceinline__ unsigned long long *pres_table()
+{
+    __shared__ unsigned long long t[PRES_SH];
+    return t;
+}
+template <typename real>
+__device__ __forceinline__ void patch_acc(const KP<real> &A, int64_t gidx, double r)
+{
+    const int lab = A.labels[gidx];
+    if (lab < 0 || lab >= A.n_slots) return;
+    const unsigned long long b = (unsigned long long)__double_as_longlong(r);
+    if (lab < PRES_SH) atomicMax(pres_table() + lab, b);
+    else atomicMax(A.patch_res + lab, b);
+}
+
 // NCOPY: the G4 path keeps 4 copies of the tile shifted by q floats (copy q of element e at
 // q*cstride + q + e) so that every lane's 4-column window load is a 16-byte aligned LDS.128.
 template <typename real, bool CHECK, int NCOPY = 1>
 __device__ __forceinline__ void commit_node(real *p, real best, bool last, real &res,
                                             double *out, int64_t gidx, double Vref,
-                                            int cstride = 0)
+                                            int cstride = 0, const KP<real> *A = nullptr)
 {
     if ((threadIdx.x & 31) == 0) {
         const real old = *p;
         if (last) res = rmax(res, rabs(best - old));
-        if (!CHECK) {
+        if constexpr (!CHECK) {
 #pragma unroll
             for (int q = 0; q < NCOPY; ++q) p[q * cstride + q] = best;
-        } else if (out) {
-            out[gidx] = Vref + (double)best;
+        } else {
+            if (out) out[gidx] = Vref + (double)best;
+            if (A && A->patch_res) patch_acc(*A, gidx, (double)rabs(best - old));
         }
     }
 }
@@ -343,7 +366,7 @@ __device__ __forceinline__ void row_general(const KP<real> &A, real *s_u, const 
         if ((dmask >> lx) & 1ull) continue;
         const int gi = i0 + lx;
         const real best = general_node<real>(A.P, s_ctrl, rowp + lx, pitch, gi, gj, D, Vref);
-        commit_node<real, CHECK>(rowp + lx, best, last, res, A.out, (int64_t)gj * n + gi, Vref);
+        commit_node<real, CHECK>(rowp + lx, best, last, res, A.out, (int64_t)gj * n + gi, Vref, 0, &A);
     }
 }
 
@@ -405,7 +428,7 @@ __device__ __forceinline__ void row_table(const KP<real> &A, real *s_u, const re
             }
             best = warp_min(best);
             commit_node<real, CHECK>(rowp + lx, best, last, res, A.out,
-                                     (int64_t)gj * n + i0 + lx, Vref);
+                                     (int64_t)gj * n + i0 + lx, Vref, 0, &A);
         }
     }
     // nodes whose feet may be clamped in x: general stencil (same Jacobi-in-row semantics)
@@ -415,7 +438,7 @@ __device__ __forceinline__ void row_table(const KP<real> &A, real *s_u, const re
         em &= em - 1;
         const real best = general_node<real>(A.P, s_ctrl, rowp + lx, pitch, i0 + lx, gj, D, Vref);
         commit_node<real, CHECK>(rowp + lx, best, last, res, A.out, (int64_t)gj * n + i0 + lx,
-                                 Vref);
+                                 Vref, 0, &A);
     }
 }
 
@@ -523,6 +546,10 @@ __device__ __forceinline__ void sweep_tile(const KP<real> &A, int t, unsigned ch
     }
     for (int e = threadIdx.x; e < 2 * A.P.na; e += blockDim.x) s_ctrl[e] = (real)A.P.ctrl[e];
     if (threadIdx.x < THt) s_prog[threadIdx.x] = 0;
+    if constexpr (CHECK) {
+        if (A.patch_res)
+            for (int e = threadIdx.x; e < PRES_SH; e += blockDim.x) pres_table()[e] = 0ull;
+    }
     __syncthreads();
 
     // D = h l - (1 - beta) V_ref >= 0 (V_ref <= V0 = h l / (1 - beta); the clamp removes fp64
@@ -577,7 +604,14 @@ __device__ __forceinline__ void sweep_tile(const KP<real> &A, int t, unsigned ch
     for (int w = 0; w < NW; ++w) rmaxv = fmax(rmaxv, s_red[w]);
     if (threadIdx.x == 0) A.tile_res[t] = rmaxv;
     if (res_out) *res_out = rmaxv;
-    if (CHECK) {
+    if constexpr (CHECK) {
+        if (A.patch_res) {
+            const int m = min(A.n_slots, PRES_SH);
+            for (int e = threadIdx.x; e < m; e += blockDim.x) {
+                const unsigned long long v = pres_table()[e];
+                if (v) atomicMax(A.patch_res + e, v);
+            }
+        }
         __syncthreads();
         return;
     }
@@ -742,7 +776,10 @@ __global__ void __launch_bounds__(NW * 32, min_blocks<PATH>()) k_sweep_ordered(K
                 const int ax = tx + (k % 3) - 1, ay = ty + (k / 3) - 1;
                 if (ax >= 0 && ay >= 0 && ax < A.g.tiles_x && ay < A.g.tiles_y) {
                     const int nb = ay * A.g.tiles_x + ax;
-                    if (O.key[nb] < kt - O.key_slack && (!O.group || O.group[nb] == gt)) {
+                    // a tile without free nodes is not in the order (the host lists only tiles
+                    // with tile_free > 0) and never finishes a pass: nothing to wait for
+                    if (O.tile_free[nb] > 0 && O.key[nb] < kt - O.key_slack &&
+                        (!O.group || O.group[nb] == gt)) {
                         while (((volatile int *)O.done)[nb] < O.pass) __nanosleep(64);
                         __threadfence();
                     }
@@ -755,6 +792,10 @@ __global__ void __launch_bounds__(NW * 32, min_blocks<PATH>()) k_sweep_ordered(K
         if (need) {
             double r = 0.0, c = 0.0;
             sweep_tile<real, PATH, CPL, WY, WX, false>(A, t, smem_raw, &r, &c);
+            if (tid == 0 && O.tile_round) {
+                O.tile_round[t] = max(O.tile_round[t], O.pass);
+                for (int k = O.lab_off[t]; k < O.lab_off[t + 1]; ++k) atomicMax(&O.patch_round[O.lab_ids[k]], O.pass);
+            }
             if (tid == 0) {
                 O.stamp[t] = (long long)atomicAdd(O.seq, 1ull) + 1;
                 atomicAdd(O.processed, 1);
@@ -797,6 +838,9 @@ static cudaError_t launch_one(const SweepLaunch &L, cudaStream_t s)
     A.tile_stamp = L.tile_stamp;
     A.tile_sweeps = L.tile_sweeps;
     A.nu_counter = L.nu_counter;
+    A.labels = L.labels;
+    A.patch_res = CHECK ? L.patch_res : nullptr;
+    A.n_slots = L.n_slots;
     const size_t smem = NW * sizeof(double) + TH * sizeof(int) + 256 * sizeof(real) +
                         (PATH == 3 ? (size_t)4 * L.g.cstride
                                    : (size_t)(TH + 2 * L.g.H) * L.g.pitch) * sizeof(real);
@@ -821,19 +865,26 @@ static cudaError_t launch_one(const SweepLaunch &L, cudaStream_t s)
     }
     if ((L.ctl || L.occupancy_out) && !CHECK) {
         auto kern = k_sweep_dyn<real, PATH, CPL, WY, WX>;
-        static int per_sm = -1, sms = 0;    // per instantiation: occupancy is fixed
-        if (per_sm < 0) {
+        // occupancy and the shared-memory attribute are per device: cached per device ordinal
+        constexpr int kMaxDev = 64;
+        static int per_sm_dev[kMaxDev] = {}, sms_dev[kMaxDev] = {};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        int per_sm = 0, sms = 0;
+        if (dev >= kMaxDev || per_sm_dev[dev] == 0) {
             if (smem > 48 * 1024) {
                 cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                      (int)smem);
                 if (e != cudaSuccess) return e;
             }
-            int dev = 0;
-            cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
             cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NW * 32, smem);
             if (e != cudaSuccess) return e;
             per_sm = std::max(1, per_sm);
+            if (dev < kMaxDev) { per_sm_dev[dev] = per_sm; sms_dev[dev] = sms; }
+        } else {
+            per_sm = per_sm_dev[dev];
+            sms = sms_dev[dev];
         }
         if (L.occupancy_out) {
             *L.occupancy_out = per_sm;
@@ -924,8 +975,9 @@ __global__ void k_tile_init(DProblem P, TileGeom g, const double *uhat, const in
     __shared__ int s_free;
     __shared__ unsigned long long s_min, s_max;
     __shared__ double s_sum;
-    __shared__ int s_lab[4];
+    __shared__ int s_nlab;
     __shared__ double s_dx, s_dy;
+    extern __shared__ unsigned s_bm[];   // bitmap of the tile's patch labels (T.n_slots bits)
     __shared__ int s_sx[2], s_sy[2];     // u_hat differences by sign (x pairs, y pairs)
     const int t = blockIdx.x;
     const int i0 = (t % g.tiles_x) * g.TW, j0 = (t / g.tiles_x) * g.TH;
@@ -935,13 +987,15 @@ __global__ void k_tile_init(DProblem P, TileGeom g, const double *uhat, const in
         s_min = 0xffffffffffffffffull;
         s_max = 0ull;
         s_sum = 0.0;
-        for (int k = 0; k < 4; ++k) s_lab[k] = -1;
+        s_nlab = 0;
         s_dx = 0.0;
         s_dy = 0.0;
         s_sx[0] = s_sx[1] = s_sy[0] = s_sy[1] = 0;
     }
+    const int nwords = labels ? (T.n_slots + 31) / 32 : 0;
+    for (int w = threadIdx.x; w < nwords; w += blockDim.x) s_bm[w] = 0u;
     __syncthreads();
-    int cnt = 0;
+    int cnt = 0, nlab = 0;
     double mn = INFINITY, mx = 0.0, sm = 0.0, dx = 0.0, dy = 0.0;
     int sx[2] = {0, 0}, sy[2] = {0, 0};
     for (int e = threadIdx.x; e < g.TW * g.TH; e += blockDim.x) {
@@ -969,17 +1023,14 @@ __global__ void k_tile_init(DProblem P, TileGeom g, const double *uhat, const in
             }
         }
         if (labels) {
+            // distinct labels of the tile's free nodes (patches and the orphan slot): most nodes
+            // share a label already set, so look before the atomic
             const int lab = labels[k];
-            if (lab >= 0) {
-                // most nodes of a tile share its first label: look before claiming a slot
-                for (int sl = 0; sl < 4; ++sl) {
-                    const int cur = ((volatile int *)s_lab)[sl];
-                    if (cur == lab) break;
-                    if (cur == -1) {
-                        const int old = atomicCAS(&s_lab[sl], -1, lab);
-                        if (old == -1 || old == lab) break;
-                    }
-                }
+            if (lab >= 0 && lab < T.n_slots) {
+                const unsigned bit = 1u << (lab & 31);
+                if (!(((volatile unsigned *)s_bm)[lab >> 5] & bit) &&
+                    !(atomicOr(&s_bm[lab >> 5], bit) & bit))
+                    ++nlab;
             }
         }
     }
@@ -987,6 +1038,7 @@ __global__ void k_tile_init(DProblem P, TileGeom g, const double *uhat, const in
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         cnt += __shfl_xor_sync(FULL, cnt, o);
+        nlab += __shfl_xor_sync(FULL, nlab, o);
         mn = fmin(mn, __shfl_xor_sync(FULL, mn, o));
         mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
         sm += __shfl_xor_sync(FULL, sm, o);
@@ -999,6 +1051,7 @@ __global__ void k_tile_init(DProblem P, TileGeom g, const double *uhat, const in
     }
     if ((threadIdx.x & 31) == 0) {
         atomicAdd(&s_free, cnt);
+        if (nlab) atomicAdd(&s_nlab, nlab);
         if (uhat) {
             atomicAdd(&s_dx, dx);
             atomicAdd(&s_dy, dy);
@@ -1023,7 +1076,8 @@ __global__ void k_tile_init(DProblem P, TileGeom g, const double *uhat, const in
         T.tile_res[t] = s_free > 0 ? INFINITY : 0.0;
         T.tile_chg[t] = 0.0;
         for (int q = 0; q < 4; ++q) T.tile_edge[4 * t + q] = 0.f;
-        for (int k = 0; k < 4; ++k) T.tile_lab[4 * t + k] = (int16_t)s_lab[k];
+        if (labels) T.tile_lab_cnt[t] = s_nlab;
+        T.tile_round[t] = -1;
         // coherent tile: (nearly) every u_hat difference has the tile's sign in x and in y, so
         // one sweep in that orientation carries information across the whole tile
         const int ox = s_dx < 0.0, oy = s_dy < 0.0;
@@ -1033,10 +1087,86 @@ __global__ void k_tile_init(DProblem P, TileGeom g, const double *uhat, const in
     }
 }
 
+// exclusive scan of the per-tile label counts into the CSR offsets (one CTA; a one-off per solve)
+__global__ void __launch_bounds__(1024) k_scan_offsets(const int32_t *cnt, int32_t *off, int n)
+{
+    __shared__ int s_part[1024];
+    const int per = (n + blockDim.x - 1) / blockDim.x;
+    const int b = threadIdx.x * per, e = min(n, b + per);
+    int sum = 0;
+    for (int i = b; i < e; ++i) sum += cnt[i];
+    s_part[threadIdx.x] = sum;
+    __syncthreads();
+    for (int d = 1; d < (int)blockDim.x; d <<= 1) {   // Hillis-Steele inclusive scan
+        const int v = threadIdx.x >= d ? s_part[threadIdx.x - d] : 0;
+        __syncthreads();
+        s_part[threadIdx.x] += v;
+        __syncthreads();
+    }
+    int run = s_part[threadIdx.x] - sum;
+    for (int i = b; i < e; ++i) {
+        off[i] = run;
+        run += cnt[i];
+    }
+    if (threadIdx.x == blockDim.x - 1) off[n] = s_part[threadIdx.x];
+}
+
+// fill the tile's label list from the same bitmap (labels in ascending order)
+__global__ void k_tile_labels(DProblem P, TileGeom g, const int16_t *labels, TileState T)
+{
+    extern __shared__ unsigned s_bm[];
+    const int t = blockIdx.x;
+    const int i0 = (t % g.tiles_x) * g.TW, j0 = (t / g.tiles_x) * g.TH;
+    const int n = P.n;
+    const int nwords = (T.n_slots + 31) / 32;
+    for (int w = threadIdx.x; w < nwords; w += blockDim.x) s_bm[w] = 0u;
+    __syncthreads();
+    for (int e = threadIdx.x; e < g.TW * g.TH; e += blockDim.x) {
+        const int ly = e / g.TW, lx = e - ly * g.TW;
+        const int gi = i0 + lx, gj = j0 + ly;
+        if (gi >= n || gj >= n) continue;
+        const int64_t k = (int64_t)gj * n + gi;
+        if (P.kind[k] != 0) continue;
+        const int lab = labels[k];
+        if (lab >= 0 && lab < T.n_slots) {
+            const unsigned bit = 1u << (lab & 31);
+            if (!(((volatile unsigned *)s_bm)[lab >> 5] & bit)) atomicOr(&s_bm[lab >> 5], bit);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        // lane L compacts words [L per, (L + 1) per) after the lanes before it
+        const int lane = threadIdx.x, per = (nwords + 31) / 32;
+        const int b = lane * per, e = min(nwords, b + per);
+        int c = 0;
+        for (int w = b; w < e; ++w) c += __popc(s_bm[w]);
+        int incl = c;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += v;
+        }
+        int pos = T.tile_lab_off[t] + incl - c;
+        for (int w = b; w < e; ++w) {
+            unsigned m = s_bm[w];
+            while (m) {
+                const int bit = __ffs(m) - 1;
+                m &= m - 1;
+                T.tile_lab_ids[pos++] = (int16_t)(32 * w + bit);
+            }
+        }
+    }
+}
+
 void launch_tile_init(const DProblem &P, const TileGeom &g, const double *uhat,
                       const int16_t *labels, TileState &T, cudaStream_t s, double coh_thr)
 {
-    k_tile_init<<<g.tiles_x * g.tiles_y, 256, 0, s>>>(P, g, uhat, labels, T, coh_thr);
+    const int nt = g.tiles_x * g.tiles_y;
+    const size_t bm = labels ? sizeof(unsigned) * (size_t)((T.n_slots + 31) / 32) : 0;
+    k_tile_init<<<nt, 256, bm, s>>>(P, g, uhat, labels, T, coh_thr);
+    if (labels) {
+        k_scan_offsets<<<1, 1024, 0, s>>>(T.tile_lab_cnt, T.tile_lab_off, nt);
+        k_tile_labels<<<nt, 256, bm, s>>>(P, g, labels, T);
+    }
 }
 
 __global__ void k_set_values(DProblem P, int mode, const double *uhat, double *V)
@@ -1127,14 +1257,11 @@ __global__ void k_activate(TileGeom g, TileState T, int out_list, double tol, do
                 const double mu = T.tile_minu[t];
                 if (mu <= thr) {
                     take = true;
-                    for (int k = 0; k < 4; ++k) {
-                        const int lab = T.tile_lab[4 * t + k];
-                        if (lab >= 0) {
-                            atomicMax(&T.patch_round[lab], round);
-                            atomicMax(reinterpret_cast<unsigned long long *>(&T.patch_res[lab]),
-                                      (unsigned long long)__double_as_longlong(fmin(r, 1e300)));
-                        }
-                    }
+                    // activation trace: the round in which each patch last had an active tile
+                    T.tile_round[t] = max(T.tile_round[t], round);
+                    if (T.n_slots > 0)
+                        for (int k = T.tile_lab_off[t]; k < T.tile_lab_off[t + 1]; ++k)
+                            atomicMax(&T.patch_round[T.tile_lab_ids[k]], round);
                 } else {
                     wpend = (unsigned long long)__double_as_longlong(fmax(mu, 0.0));
                 }

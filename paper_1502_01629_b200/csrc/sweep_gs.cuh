@@ -267,6 +267,16 @@ __device__ __forceinline__ void row_gs4(const KP<float> &A, float *s_u, const fl
             rd[gg] = sk ? 0.f : m - old[gg];
             dlt[gg] = CHECK ? 0.f : rd[gg];
         }
+        if constexpr (CHECK) {
+            // per-patch residuals of a verification pass: lane nd < 4 owns node g + nd
+            if (A.patch_res && lane < 4 && !((sk4 >> nd) & 1u)) {
+                float r = rd[0];
+                r = nd == 1 ? rd[1] : r;
+                r = nd == 2 ? rd[2] : r;
+                r = nd == 3 ? rd[3] : r;
+                patch_acc(A, (int64_t)gj * n + i0 + g + nd, (double)fabsf(r));
+            }
+        }
         {
             const float gm = fmaxf(fmaxf(fabsf(rd[0]), fabsf(rd[1])), fmaxf(fabsf(rd[2]), fabsf(rd[3])));
             if (last) res = fmaxf(res, gm);
@@ -305,7 +315,7 @@ __device__ __forceinline__ void row_gs4(const KP<float> &A, float *s_u, const fl
                         ? general_node_edge<float>(A.P, s_ctrl, rowp + lx, pitch, i0 + lx, gj, D, Vref)
                         : general_node<float>(A.P, s_ctrl, rowp + lx, pitch, i0 + lx, gj, D, Vref);
                     commit_node<float, CHECK, 4>(rowp + lx, best, last, res, A.out,
-                                                 (int64_t)gj * n + i0 + lx, Vref, cstride);
+                                                 (int64_t)gj * n + i0 + lx, Vref, cstride, &A);
                 }
             }
         }
@@ -474,7 +484,7 @@ __device__ __forceinline__ void row_gsg(const KP<real> &A, real *s_u, const real
             nc.sa = __shfl_sync(FULL, src.sa, sl);
             nc.D = __shfl_sync(FULL, src.D, sl);
             const real best = general_node_c<real>(A.P, s_ctrl, rowp + lx, pitch, i0 + lx, gj, nc);
-            commit_node<real, CHECK>(rowp + lx, best, true, res, A.out, (int64_t)gj * n + i0 + lx, Vref);
+            commit_node<real, CHECK>(rowp + lx, best, true, res, A.out, (int64_t)gj * n + i0 + lx, Vref, 0, &A);
             __syncwarp();      // lane 0's commit is seen by every lane's next gathers
         }
         if (!CHECK && lane == 0) prog_release(s_prog + jj, base + gs + 1);

@@ -3,7 +3,9 @@ import argparse, json, sys, time, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import pdd_inputs as I
-from paper_1502_01629_b200 import Solver
+from paper_1502_01629_b200 import Solver, _native
+if os.environ.get("PDD_LIB"):          # A/B builds (scripts/ab*.sh); the product path loads the in-tree lib
+    _native.use_library(os.environ["PDD_LIB"])
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--cfg", default="C5"); ap.add_argument("--n", type=int, default=None)

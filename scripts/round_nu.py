@@ -15,7 +15,7 @@ for R in (a.round - 1, a.round):
     s.coarse_solve(inst.tol_coarse); s.synthesize(); s.build_patches(inst.n_patches)
     if a.mode == "static":
         s.build_static(*inst.static_blocks)
-    st = s.solve(a.mode, tol=1e-6, k_inner=a.k, max_rounds=R, raise_on_noconverge=False)   # PDD_TRACE=1: one round per batch, exact cap
+    st = s.solve(a.mode, tol=1e-6, k_inner=a.k, max_rounds=R, raise_on_noconverge=False, trace=True)   # one round per batch: exact cap
     out.append(st["node_updates"]); s.close()
 print(json.dumps({"cfg": a.cfg, "mode": a.mode, "k": a.k, "round": a.round,
                   "node_updates_in_round": out[1] - out[0]}))

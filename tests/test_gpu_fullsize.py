@@ -1,15 +1,18 @@
-"""Full-size parity at BASELINE.json's own grids (C3 2049^2, C4 4097^2, C5 8193^2), in the launch
-configuration bench.py times (patchy pipeline, fp32, rounds schedule, k_inner = 4).
+"""Full-size parity at BASELINE.json's own grids (C3 2049^2, C4 4097^2, C5 8193^2), element by
+element, in the launch configuration bench.py times (patchy pipeline, fp32, rounds schedule,
+automatic k_inner: one in-tile sweep per visit).
 
-The oracle cannot run the fine solve at these sizes (C5: ~5.8k Jacobi sweeps, hours), so:
-  * everything the oracle CAN compute one by one is compared exactly: u_c (full coarse grid,
-    bit-exact), u_hat and a* at sampled nodes (bit-exact), patch labels at sampled nodes (the
-    oracle chases the successor chain, synthesising a* on the fly: bit-exact), static labels;
-  * V is checked through properties that hold at any size: the oracle's fp64 operator T applied
-    to the GPU's V at sampled nodes gives a residual <= 2 tol (the GPU verified < tol in fp32),
-    0 <= V <= h l_max / (1 - beta), V = 0 on the target;
-  * C5 in fp64: the oracle evaluates T(V) on ALL 67 M nodes; the residual r certifies
-    ||V - V*|| <= r / (1 - beta) (contraction, R29) <= 1e-10.
+north_star: labels bit-exact and V within tolerance on all five configs (the outputs of the
+paper's pipeline).  At these sizes the oracle computes every
+array of the pre-computation in seconds, so all of them are compared on EVERY node:
+  * u_c (full coarse grid), u_hat (prolongation), a* (synthesis): bit-exact (canonical fp64, R30);
+  * successors and patch labels (R18), static labels (R19): bit-exact; decomposition quality
+    (orphan fraction, non-empty patches) is asserted where the rule is non-degenerate;
+  * V: the oracle cannot run the fine solve (C5: ~5.8k Jacobi sweeps, hours), so the reference
+    is the GPU's fp64 patchy solve driven to r <= 0.2e-10 (1 - beta), CERTIFIED by the oracle's
+    fp64 operator on all nodes: ||V64 - V*|| <= r_oracle / (1 - beta) <= 1e-10 (contraction,
+    R29).  The fp32 V of the bench configuration is then compared with V64 on every node against
+    the north star's 5e-5 max|V| (the certification adds at most 1e-10).
 """
 import numpy as np
 import pytest
@@ -19,68 +22,14 @@ import pdd_inputs as I
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
-_CACHE = {}
+# decomposition quality at full size (oracle, this container):
+# C3 0 % orphans, 64/64 patches; C4 1.38 % / 128/128; C5 0 % / 248/256
+QUALITY = {"C3": (0.0, 64), "C4": (0.02, 128), "C5": (0.0, 240)}
 
 
-def _instance(cfg):
-    if cfg not in _CACHE:
-        _CACHE[cfg] = I.make_config(cfg)
-    return _CACHE[cfg]
-
-
-def _free_sample(inst, m, seed):
-    rng = np.random.default_rng(seed)
-    free = np.nonzero(inst.kind == I.KIND_FREE)[0]
-    return np.sort(rng.choice(free, size=min(m, free.size), replace=False)).astype(np.int64)
-
-
-@pytest.mark.parametrize("cfg", ["C3", "C4", "C5"])
-def test_fullsize_pipeline_parity(cfg):
+def _certified_fp64(inst):
+    """GPU fp64 patchy solve certified by the oracle: returns V64 with ||V64 - V*|| <= 1e-10."""
     from paper_1502_01629_b200 import Solver
-    inst = _instance(cfg)
-    ref_c = O.coarse_solve(inst)
-    s = Solver(inst, precision=32)
-    cs = s.coarse_solve(inst.tol_coarse)
-    assert cs["sweeps"] == ref_c["sweeps"]
-    assert np.array_equal(s.get_coarse_values().view(np.uint64), ref_c["V"].view(np.uint64))
-    s.synthesize()
-    idx = _free_sample(inst, 20000, 1)
-    uhat = s.get_uhat()
-    assert np.array_equal(uhat[idx].view(np.uint64), O.uhat_at(inst, ref_c["V"], idx).view(np.uint64))
-    a = s.get_controls()
-    assert np.array_equal(a[idx].astype(np.int32), O.astar_at(inst, ref_c["V"], idx))
-    s.build_patches(inst.n_patches)
-    lab = s.get_labels()
-    for k in _free_sample(inst, 150, 2):
-        assert lab[k] == O.label_at(inst, ref_c["V"], int(k)), k
-    # the fine solve in the bench's configuration
-    st = s.solve("patchy", tol=inst.tol, k_inner=4)
-    assert st["converged"] == 1 and st["final_residual"] < inst.tol
-    V = s.get_values()
-    vmax = inst.h * 1.0 / (1.0 - inst.beta)
-    assert np.all(V[inst.kind == I.KIND_TARGET] == 0.0)
-    free = inst.kind == I.KIND_FREE
-    assert V[free].min() > 0.0 and V[free].max() <= vmax
-    if cfg == "C4":
-        assert np.all(V[inst.kind == I.KIND_OBSTACLE] == 1.0 / inst.lam)
-    idx = _free_sample(inst, 200000, 3)
-    T, _ = O.apply_at(inst, V, idx)
-    assert np.abs(T - V[idx]).max() <= 2 * inst.tol
-    # static decomposition: labels closed form, same fixed point within the fp32 bar
-    s.build_static(*inst.static_blocks)
-    sl = s.get_labels()
-    ref_sl = O.static_labels(inst)
-    assert np.array_equal(sl, ref_sl)
-    st2 = s.solve("static", tol=inst.tol, k_inner=4)
-    assert st2["converged"] == 1
-    V2 = s.get_values()
-    assert np.abs(V2 - V).max() <= 5e-5 * V.max()
-    s.close()
-
-
-def test_fullsize_c5_fp64_certified():
-    from paper_1502_01629_b200 import Solver
-    inst = _instance("C5")
     s = Solver(inst, precision=64)
     s.coarse_solve(inst.tol_coarse)
     s.synthesize()
@@ -90,5 +39,61 @@ def test_fullsize_c5_fp64_certified():
     assert st["converged"] == 1
     V = s.get_values()
     s.close()
-    _, r = O.apply(inst, V)                       # oracle fp64 T on all 67 M nodes
+    _, r = O.apply(inst, V)                       # oracle fp64 T on every node
     assert r / (1.0 - inst.beta) <= bound, r
+    return V
+
+
+@pytest.mark.parametrize("cfg", ["C3", "C4", "C5"])
+def test_fullsize_pipeline_parity(cfg):
+    from paper_1502_01629_b200 import Solver
+    inst = I.make_config(cfg)
+    free = inst.kind == I.KIND_FREE
+    ref_c = O.coarse_solve(inst)
+    s = Solver(inst, precision=32)
+    cs = s.coarse_solve(inst.tol_coarse)
+    assert cs["sweeps"] == ref_c["sweeps"]
+    assert np.array_equal(s.get_coarse_values().view(np.uint64), ref_c["V"].view(np.uint64))
+    s.synthesize()
+    uref = O.prolong(inst.coarse.n, ref_c["V"], inst.n)
+    assert np.array_equal(s.get_uhat().view(np.uint64), uref.view(np.uint64))
+    aref = O.synthesize(inst, uref)
+    assert np.array_equal(s.get_controls(), aref)
+    s.build_patches(inst.n_patches)
+    sref = O.successor(inst, aref)
+    assert np.array_equal(s.get_successors().astype(np.int64), sref)
+    lref = O.labels(inst, sref)
+    lab = s.get_labels()
+    assert np.array_equal(lab, lref)
+    orph = float((lab[free] == inst.n_patches).mean())
+    used = int(np.unique(lab[free & (lab < inst.n_patches)]).size)
+    print(f"{cfg}: orphan fraction {orph:.4f}, non-empty patches {used}/{inst.n_patches}")
+    max_orph, min_used = QUALITY[cfg]
+    assert orph <= max_orph and used >= min_used
+    del uref, aref, sref, lref
+
+    # the fine solve in the bench's configuration (automatic k_inner)
+    st = s.solve("patchy", tol=inst.tol)
+    assert st["converged"] == 1 and st["final_residual"] < inst.tol
+    V = s.get_values()
+    vmax = inst.h * 1.0 / (1.0 - inst.beta)
+    assert np.all(V[inst.kind == I.KIND_TARGET] == 0.0)
+    assert V[free].min() > 0.0 and V[free].max() <= vmax
+    if cfg == "C4":
+        assert np.all(V[inst.kind == I.KIND_OBSTACLE] == 1.0 / inst.lam)
+
+    # static decomposition: labels closed form, same fixed point
+    s.build_static(*inst.static_blocks)
+    assert np.array_equal(s.get_labels(), O.static_labels(inst))
+    st2 = s.solve("static", tol=inst.tol)
+    assert st2["converged"] == 1
+    V2 = s.get_values()
+    s.close()
+
+    # fp32 V against the certified fp64 V, on every node
+    V64 = _certified_fp64(inst)
+    vm = float(np.abs(V64).max())
+    e1 = float(np.abs(V - V64).max()) / vm
+    e2 = float(np.abs(V2 - V64).max()) / vm
+    print(f"{cfg}: fp32 patchy max|V - V64| = {e1:.2e} max|V|, static {e2:.2e} max|V|")
+    assert e1 <= 5e-5 and e2 <= 5e-5

@@ -45,8 +45,15 @@ def test_coarse_uhat_astar_bitexact(cfg, n):
     assert np.array_equal(a, aref)
 
 
-@pytest.mark.parametrize("cfg,n", [("C2", None), ("C3", 257), ("C4", 513), ("C5", 513), ("C5", 1025)])
-def test_labels_bitexact(cfg, n):
+# sizes where the successor rule is non-degenerate (oracle, measured in this container): orphan
+# fraction and non-empty patches -- C2 full 0 / 16, C3@2049 (full) 0 / 64, C4@2049 9.2 % / 128,
+# C5@1025 0 / 56, C5@2049 0 / 142; C4@1025 (23.7 % orphans) keeps the orphan branch exercised
+LABEL_CASES = [("C2", None, 0.0, 16), ("C3", None, 0.0, 64), ("C4", 1025, 0.30, 115),
+               ("C4", 2049, 0.12, 128), ("C5", 1025, 0.0, 56), ("C5", 2049, 0.0, 140)]
+
+
+@pytest.mark.parametrize("cfg,n,max_orph,min_used", LABEL_CASES)
+def test_labels_bitexact(cfg, n, max_orph, min_used):
     inst = I.make_config(cfg, n=n)
     ref = O.solve_pipeline(inst, fine=False)
     s = _solver(inst, 32)
@@ -57,6 +64,10 @@ def test_labels_bitexact(cfg, n):
     assert np.array_equal(succ.astype(np.int64), ref["succ"])
     lab = s.get_labels()
     assert np.array_equal(lab, ref["labels"])
+    free = inst.kind == I.KIND_FREE
+    orph = float((lab[free] == inst.n_patches).mean())
+    used = int(np.unique(lab[free & (lab < inst.n_patches)]).size)
+    assert orph <= max_orph and used >= min_used, (orph, used)
     s.build_static(*inst.static_blocks)
     assert np.array_equal(s.get_labels(), ref["static_labels"])
 
@@ -182,27 +193,27 @@ def test_schedules_reach_the_same_fixed_point(mode, schedule, policy):
 
 # The 16 x 128 path-3 tile (sweep.cu's second build, pdd::wide) is chosen automatically only on
 # fine grids (runtime.cu p3_use_wide: C4, C5 full size, covered by test_gpu_fullsize.py); here
-# PDD_P3_TILE=128 forces it on small grids with ragged tails in both directions.
+# pdd_set_tile_cols(128) forces it on small grids with ragged tails in both directions.
 @pytest.mark.parametrize("cfg,n", [("C2", 201), ("C4", 257), ("C5", 257), ("C5", 300)])
 @pytest.mark.parametrize("kernel", [0, 2])
-def test_wide_tile_operator_parity(monkeypatch, cfg, n, kernel):
-    monkeypatch.setenv("PDD_P3_TILE", "128")
+def test_wide_tile_operator_parity(cfg, n, kernel):
     inst = I.make_config(cfg, n=n)
     V = _random_field(inst, 5)
     ref, _ = O.apply(inst, V)
     s = _solver(inst, 32)
+    s.set_tile_cols(128)
     out, res = s.apply_operator(V, kernel=kernel)
     assert np.abs(out - ref).max() < 2e-6 * np.abs(V).max()
     assert abs(res - np.abs(ref - V)[inst.kind == 0].max()) < 4e-6
 
 
 @pytest.mark.parametrize("mode", ["patchy", "static"])
-def test_wide_tile_solve_parity(monkeypatch, mode):
+def test_wide_tile_solve_parity(mode):
     # tol 1e-6: on a 513^2 grid the wide tile spans 1 in x and its fp32 noise floor sits near 1e-7
-    monkeypatch.setenv("PDD_P3_TILE", "128")
     inst = I.make_config("C5", n=513)
     ref = O.jacobi(inst, tol=_tight_tol(inst, 2e-11), max_sweeps=10**6)
     s = _solver(inst, 32)
+    s.set_tile_cols(128)
     if mode == "patchy":
         s.coarse_solve(inst.tol_coarse)
         s.synthesize()
