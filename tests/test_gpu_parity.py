@@ -224,3 +224,26 @@ def test_wide_tile_solve_parity(mode):
     assert st["converged"] == 1
     V = s.get_values()
     assert np.abs(V - ref["V"]).max() <= 5e-5 * np.abs(ref["V"]).max()
+
+
+def test_ordered_static_with_tiles_without_free_nodes():
+    """The ordered schedule lists only tiles with free nodes; a static-block neighbour lying
+    entirely inside the target or an obstacle must not be waited for (it never finishes a pass).
+    C4 at 2049^2: obstacle discs and the target cover whole tiles.  Same fixed point as the
+    rounds schedule within the fp32 bar."""
+    inst = I.make_config("C4", n=2049)
+    s = _solver(inst, 32)
+    s.build_static(*inst.static_blocks)
+    st = s.solve("static", tol=1e-6, k_inner=4, schedule="ordered")
+    assert st["converged"] == 1
+    V1 = s.get_values()
+    n = inst.n
+    j, i = np.divmod(np.arange(n * n), n)
+    tile = (j // st["tile_rows"]) * st["tiles_x"] + i // st["tile_cols"]
+    free_per_tile = np.bincount(tile, weights=(inst.kind == I.KIND_FREE), minlength=st["n_tiles"])
+    assert (free_per_tile == 0).sum() > 0
+    st2 = s.solve("static", tol=1e-6, k_inner=4)
+    assert st2["converged"] == 1
+    V2 = s.get_values()
+    s.close()
+    assert np.abs(V1 - V2).max() <= 5e-5 * np.abs(V2).max()
