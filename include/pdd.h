@@ -126,7 +126,11 @@ typedef struct {
                             buckets of min u_hat of width delta;
                             1 ordered: Gauss-Seidel passes over the tiles in key order (u_hat
                             for patchy, block-lexicographic for static), each tile waiting for
-                            its lower-key neighbours (delta = key slack)                     */
+                            its lower-key neighbours (delta = key slack);
+                            2 queue: one persistent launch whose CTAs pop dirty tiles from a
+                            work queue and mark the neighbours of changed tiles dirty (no
+                            rounds); patchy admits tiles in min-u_hat order while fewer tiles
+                            than resident CTAs are queued; then the verification pass     */
     int32_t early_exit_off; /* 1: every tile visit does all k_inner sweeps (A/B; default 0: a
                             visit stops after the first sweep changing no node by >= tol)   */
     int32_t bucket_policy;  /* patchy, schedule 0: 0 moving front (the threshold advances every

@@ -202,7 +202,7 @@ class Solver:
         if k_inner is None:   # 0 = automatic in libpdd: 1 patchy / 4 static,
             k_inner = 0       # 4 for a patchy grid that fits one wave of sweep CTAs
         o.k_inner, o.tol, o.max_rounds, o.delta, o.kernel = int(k_inner), float(tol), int(max_rounds), float(delta), int(kernel)
-        o.schedule = 1 if schedule in ("ordered", 1) else 0
+        o.schedule = {"rounds": 0, "ordered": 1, "queue": 2}.get(schedule, schedule)
         o.early_exit_off = 0 if early_exit else 1
         o.bucket_policy = int(bucket_policy)
         o.trace = 1 if trace else 0

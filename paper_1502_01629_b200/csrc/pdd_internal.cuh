@@ -201,6 +201,37 @@ struct OrderArgs {
     int32_t *patch_round;
 };
 
+// Work-queue schedule (k_sweep_queue): persistent CTAs pop dirty tiles from a ring, visit them
+// and mark their neighbours dirty -- asynchronous (chaotic) relaxation of the same monotone
+// contraction (R29) without rounds.  Tiles enter the queue in key order (min u_hat for patchy,
+// all at once for static) while the queue holds fewer than `fill` tiles.
+struct QueueCtl {
+    unsigned long long head, tail;   // ring cursors (monotone)
+    unsigned long long visits;       // tile visits so far (the visit sequence number)
+    unsigned long long max_visits;   // stop once reached (non-convergence guard)
+    int work;                        // tiles queued or being visited
+    int adm;                         // tiles admitted from the key order
+    int lock;                        // admission lock
+    int stop;
+    unsigned long long max_res;      // ordered bits of the max visit residual (report)
+};
+struct QueueArgs {
+    QueueCtl *ctl;
+    int32_t *ring;                   // capacity cap (power of two, >= 2 n_tiles), 0 = empty slot
+    unsigned cap;
+    const int32_t *order;            // tiles with free nodes in key order
+    const int32_t *rank;             // position of each tile in order (INT_MAX: not listed)
+    int n_order;
+    int fill;                        // admission keeps >= fill tiles queued while tiles remain
+    int *state;                      // per tile: 0 clean, 1 queued, 2 visiting, 3 visiting + dirty
+    double tol;                      // re-queue a tile whose last sweep changed >= tol
+    double tol_act;                  // mark the 8 neighbours dirty when the visit changed >= tol_act
+    int32_t *tile_round;             // per tile: sequence number of its last visit
+    const int32_t *lab_off;          // tile label CSR -> per-patch last visit sequence
+    const int16_t *lab_ids;
+    int32_t *patch_round;
+};
+
 struct SweepLaunch {
     DProblem P;
     double *V;
@@ -223,6 +254,8 @@ struct SweepLaunch {
     int precision;           // 32 | 64
     int ordered;             // 1: k_sweep_ordered with `order` (one pass)
     OrderArgs order;
+    int queued = 0;          // 1: k_sweep_queue with `queue`
+    QueueArgs queue{};
     double early_tol;        // > 0: a tile visit stops after the first sweep changing < early_tol
     const int32_t *tile_free;            // free nodes per tile (node-update accounting)
     const uint8_t *tile_orient;          // per-tile first sweep orientation (or null: +x+y)
@@ -237,6 +270,16 @@ struct SweepLaunch {
     int *occupancy_out = nullptr;        // != NULL: report the device-driven kernel's resident
                                          //   CTAs per SM and launch nothing
 };
+
+// work-queue schedule: (re-)seed the queue with the tiles whose residual is >= tol (after a
+// verification pass), n_order = 0 keeps admission closed
+void launch_queue_seed(const TileGeom &g, const TileState &T, const QueueArgs &Q, int n_tiles,
+                       double tol, cudaStream_t s);
+// order / rank of the tiles with free nodes by key (NULL: tile index order); scratch of
+// queue_order_scratch_ints() ints
+void launch_queue_order(const TileState &T, const double *key, int n_tiles, int32_t *scratch,
+                        int32_t *order, int32_t *rank, cudaStream_t s);
+size_t queue_order_scratch_ints();
 
 // device-driven round kernels (one thread each) around the activation and the sweep
 void launch_round_begin(RoundCtl *ctl, ActCounters *c, cudaStream_t s);

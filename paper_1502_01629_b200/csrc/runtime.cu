@@ -144,6 +144,13 @@ struct pdd_ctx {
     size_t rowtab_bytes = 0;
     TileState T{};
     int max_tiles = 0;
+    // work-queue schedule (schedule 2)
+    QueueCtl *qctl = nullptr;
+    int32_t *qring = nullptr;
+    unsigned qcap = 0;
+    int *qstate = nullptr;
+    int32_t *qrank = nullptr;
+    int32_t *qscratch = nullptr;
     double *outbuf = nullptr;
     // host pinned
     ActCounters *h_cnt = nullptr;
@@ -372,8 +379,21 @@ static size_t layout(pdd_ctx *c, void *ws, const pdd_problem *f, const pdd_probl
     T.stamp = cv.take<long long>(tmax);
     T.ocounters = cv.take<OrdCounters>(1);
     RoundCtl *rctl = cv.take<RoundCtl>(1);
+    unsigned qcap = 1;
+    while (qcap < 2u * (unsigned)tmax) qcap <<= 1;
+    QueueCtl *qctl = cv.take<QueueCtl>(1);
+    int32_t *qring = cv.take<int32_t>(qcap);
+    int *qstate = cv.take<int>(tmax);
+    int32_t *qrank = cv.take<int32_t>(tmax);
+    int32_t *qscr = cv.take<int32_t>(queue_order_scratch_ints());
     if (c) {
         c->rctl = rctl;
+        c->qctl = qctl;
+        c->qring = qring;
+        c->qcap = qcap;
+        c->qstate = qstate;
+        c->qrank = qrank;
+        c->qscratch = qscr;
         c->F = F;
         c->Cc = Cc;
         c->V = V;
@@ -1073,6 +1093,95 @@ static pdd_status ordered_loop(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_
     return PDD_OK;
 }
 
+// Work-queue schedule: one persistent launch (k_sweep_queue) relaxes dirty tiles until the queue
+// is empty and every tile has been admitted, then a full-grid Jacobi verification
+// re-seeds the queue with the offending tiles.
+static pdd_status queue_loop(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats &S, int trace,
+                             int k_inner, int resident, int tiles_free, bool &converged,
+                             double &last_verify, float &ms_sweep, float &ms_verify)
+{
+    cudaStream_t s = ctx->stream;
+    const int nt = ctx->n_tiles;
+    // tiles in key order: min u_hat (patchy) or index order (static)
+    launch_queue_order(ctx->T, o->mode == 0 ? ctx->T.tile_minu : nullptr, nt, ctx->qscratch,
+                       ctx->T.order, ctx->qrank, s);
+    CK(cudaMemsetAsync(ctx->qstate, 0, sizeof(int) * nt, s));
+    CK(cudaMemsetAsync(ctx->T.tile_sweeps, 0, sizeof(int32_t) * nt, s));
+    CK(cudaMemsetAsync(ctx->qring, 0, sizeof(int32_t) * ctx->qcap, s));
+    QueueCtl qc{};
+    // cap on visits ~ max_rounds waves of resident CTAs (non-convergence guard)
+    qc.max_visits = (unsigned long long)std::max<int64_t>(1, o->max_rounds) * (unsigned long long)resident;
+    qc.adm = o->mode == 0 ? 0 : tiles_free;   // static: every tile at once (seeded below)
+    CK(cudaMemcpyAsync(ctx->qctl, &qc, sizeof qc, cudaMemcpyHostToDevice, s));
+    QueueArgs Q{};
+    Q.ctl = ctx->qctl;
+    Q.ring = ctx->qring;
+    Q.cap = ctx->qcap;
+    Q.order = ctx->T.order;
+    Q.rank = ctx->qrank;
+    Q.n_order = tiles_free;
+    Q.fill = o->mode == 0 ? std::max(1, resident) : tiles_free;
+    Q.state = ctx->qstate;
+    Q.tol = o->tol;
+    Q.tol_act = o->tol;
+    Q.tile_round = ctx->T.tile_round;
+    Q.lab_off = ctx->T.tile_lab_off;
+    Q.lab_ids = ctx->T.tile_lab_ids;
+    Q.patch_round = ctx->T.patch_round;
+    if (o->mode != 0) launch_queue_seed(ctx->g, ctx->T, Q, nt, -1.0, s);   // tile_res = inf
+    double best = INFINITY;
+    int stalled = 0;
+    for (;;) {
+        SweepLaunch L = make_launch(ctx, nullptr, 0, k_inner, 0, nullptr);
+        L.early_tol = o->early_exit_off ? 0.0 : o->tol;
+        L.tile_sweeps = ctx->T.tile_sweeps;
+        L.queued = 1;
+        L.queue = Q;
+        CK(cudaEventRecord(ctx->ev[2], s));
+        CK(launch_sweep(L, s));
+        ctx->launches++;
+        CK(cudaEventRecord(ctx->ev[3], s));
+        QueueCtl h{};
+        CK(cudaMemcpyAsync(&h, ctx->qctl, sizeof h, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]);
+        ms_sweep += ms;
+        S.rounds++;
+        S.tiles_processed = (int64_t)h.visits;
+        if (trace)
+            fprintf(stderr, "[pdd] queue launch: visits %llu maxres %.3e stop %d %.3f ms\n", h.visits,
+                    bits_to_double(h.max_res), h.stop, ms);
+        if (h.stop) break;   // visit cap reached
+        // full-grid verification with each patch's own residual
+        CK(cudaEventRecord(ctx->ev[2], s));
+        SweepLaunch V = make_launch(ctx, ctx->T.all_list, nt, 1, 1, nullptr);
+        CK(cudaMemsetAsync(ctx->T.patch_res, 0, sizeof(unsigned long long) * ctx->T.n_slots, s));
+        V.patch_res = ctx->T.patch_res;
+        V.n_slots = ctx->T.n_slots;
+        CK(launch_sweep(V, s));
+        ctx->launches++;
+        CK(cudaEventRecord(ctx->ev[3], s));
+        S.rounds++;
+        S.verify_passes++;
+        pdd_status r = activate(ctx, 0, INFINITY, INFINITY, 0);   // max residual readback only
+        if (r != PDD_OK) return r;
+        cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]);
+        ms_verify += ms;
+        last_verify = bits_to_double(ctx->h_cnt->max_res);
+        if (trace) fprintf(stderr, "[pdd] verify residual %.3e\n", last_verify);
+        if (last_verify < o->tol) {
+            converged = true;
+            break;
+        }
+        if (last_verify < 0.9 * best) { best = last_verify; stalled = 0; }
+        else if (++stalled >= 8) break;   // below the arithmetic's noise floor: give up
+        launch_queue_seed(ctx->g, ctx->T, Q, nt, o->tol, s);
+        ctx->launches++;
+    }
+    return PDD_OK;
+}
+
 extern "C" {
 
 pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
@@ -1080,6 +1189,7 @@ pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
     if (!ctx) return fail(nullptr, PDD_E_INVALID, "ctx is NULL");
     if (!o) return fail(ctx, PDD_E_INVALID, "opts is NULL");
     if (o->mode != 0 && o->mode != 1) return fail(ctx, PDD_E_INVALID, "mode must be 0 or 1");
+    if (o->schedule < 0 || o->schedule > 2) return fail(ctx, PDD_E_INVALID, "schedule must be 0, 1 or 2");
     if (o->k_inner < 0 || o->k_inner > 1024) return fail(ctx, PDD_E_INVALID, "k_inner outside 0..1024");
     if (!(o->tol > 0.0)) return fail(ctx, PDD_E_INVALID, "tol must be > 0");
     if (o->mode == 0 && (!ctx->synth_done || ctx->labels_mode != 1))
@@ -1177,10 +1287,15 @@ pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
         pdd_status r = ordered_loop(ctx, o, S, trace, converged, last_verify, ms_sweep, ms_verify);
         if (r != PDD_OK) return r;
     }
+    if (o->schedule == 2) {
+        pdd_status r = queue_loop(ctx, o, S, trace, k_inner, resident, tiles_free, converged,
+                                  last_verify, ms_sweep, ms_verify);
+        if (r != PDD_OK) return r;
+    }
     // Device-driven rounds (schedule 0): batches of (begin, activate, sweep, end) are enqueued
     // without a host round trip; the RoundCtl block carries the front threshold and the stop
     // flag between them.  The host syncs once per batch and runs the verification pass.
-    if (o->schedule != 1) {
+    if (o->schedule == 0) {
         RoundCtl c0{};
         c0.thr = thr;
         c0.delta = delta;
@@ -1202,7 +1317,7 @@ pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
     const char *te = dev_env("PDD_TACT");   // A/B: neighbour-change activation threshold / tol
     const double tact = te ? std::atof(te) : 1.0;
     long long rounds_prev = 0;
-    while (o->schedule != 1) {
+    while (o->schedule == 0) {
         if (S.rounds >= o->max_rounds) break;
         CK(cudaEventRecord(ctx->ev[2], s));
         SweepLaunch L = make_launch(ctx, ctx->T.list[cur], ctx->n_tiles, k_inner, 0, nullptr);

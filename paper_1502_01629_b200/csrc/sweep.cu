@@ -811,6 +811,178 @@ __global__ void __launch_bounds__(NW * 32, min_blocks<PATH>()) k_sweep_ordered(K
     }
 }
 
+// ------------------------------------------------------------------ work-queue schedule
+// Tile states: 0 clean, 1 queued, 2 visiting, 3 visiting and dirtied meanwhile.  A queued or
+// visiting tile holds one unit of ctl->work; the queue is empty for good when work == 0 and every
+// tile has been admitted.
+__device__ __forceinline__ unsigned long long q_ld64(const unsigned long long *p)
+{
+    return *(volatile const unsigned long long *)p;
+}
+__device__ __forceinline__ int q_ld(const int *p) { return *(volatile const int *)p; }
+
+__device__ __forceinline__ void q_enqueue(const QueueArgs &Q, int t)
+{
+    const unsigned long long pos = atomicAdd(&Q.ctl->tail, 1ull);
+    volatile int32_t *slot = Q.ring + (pos & (unsigned long long)(Q.cap - 1));
+    while (*slot != 0) __nanosleep(32);   // a slow consumer of the previous lap still reads it
+    *slot = t + 1;
+}
+
+// a neighbour (or the admission) dirtied tile t
+__device__ __forceinline__ void q_mark_dirty(const QueueArgs &Q, int t)
+{
+    int st = q_ld(Q.state + t);
+    for (;;) {
+        if (st == 0) {
+            const int o = atomicCAS(Q.state + t, 0, 1);
+            if (o == 0) {
+                atomicAdd(&Q.ctl->work, 1);
+                q_enqueue(Q, t);
+                return;
+            }
+            st = o;
+        } else if (st == 2) {
+            const int o = atomicCAS(Q.state + t, 2, 3);
+            if (o == 2) return;
+            st = o;
+        } else {
+            return;   // already queued, or visiting and already dirty
+        }
+    }
+}
+
+// thread 0: the next action of the CTA.  Returns a tile to visit (>= 0), -1 when the queue is
+// finished (or stopped), or -2 after reserving an admission (*a0, *m, *pos0: the next m tiles of
+// the key order go to ring positions pos0.., the lock is held until the CTA publishes them).
+__device__ int q_next(const QueueArgs &Q, int *a0, int *m, unsigned long long *pos0)
+{
+    QueueCtl *c = Q.ctl;
+    for (;;) {
+        if (q_ld(&c->stop)) return -1;
+        const unsigned long long h = q_ld64(&c->head), tl = q_ld64(&c->tail);
+        const int adm = q_ld(&c->adm);
+        if (adm < Q.n_order && (long long)(tl - h) < Q.fill && atomicCAS(&c->lock, 0, 1) == 0) {
+            // tiles are admitted in key order (nodes processed in increasing u_hat)
+            // while the queue holds fewer than `fill` tiles: the GPU stays full, the front
+            // moves as fast as the tiles behind it converge
+            const int a = q_ld(&c->adm);
+            const long long ql = (long long)(q_ld64(&c->tail) - q_ld64(&c->head));
+            const int k = (int)min((long long)(Q.n_order - a), (long long)Q.fill - ql);
+            if (k > 0) {
+                *a0 = a;
+                *m = k;
+                atomicAdd(&c->work, k);
+                *pos0 = atomicAdd(&c->tail, (unsigned long long)k);
+                return -2;
+            }
+            atomicExch(&c->lock, 0);
+            continue;
+        }
+        if (h < tl) {
+            if (atomicCAS(&c->head, h, h + 1) == h) {
+                volatile int32_t *slot = Q.ring + (h & (unsigned long long)(Q.cap - 1));
+                int v;
+                while ((v = *slot) == 0) __nanosleep(32);   // the producer's store is on its way
+                *slot = 0;
+                const int t = v - 1;
+                atomicExch(Q.state + t, 2);   // queued -> visiting (only the popper changes 1)
+                __threadfence();
+                return t;
+            }
+            continue;
+        }
+        if (q_ld(&c->work) == 0 && adm >= Q.n_order) return -1;
+        __nanosleep(64);
+    }
+}
+
+// the whole CTA publishes an admission reserved by q_next: states first (a neighbour that sees
+// the new adm must find the tile queued), then adm, then the ring slots
+__device__ void q_admit_cta(const QueueArgs &Q, int a0, int m, unsigned long long pos0)
+{
+    for (int k = threadIdx.x; k < m; k += blockDim.x) Q.state[Q.order[a0 + k]] = 1;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        *(volatile int *)&Q.ctl->adm = a0 + m;
+        __threadfence();
+        atomicExch(&Q.ctl->lock, 0);
+    }
+    for (int k = threadIdx.x; k < m; k += blockDim.x) {
+        volatile int32_t *slot = Q.ring + ((pos0 + k) & (unsigned long long)(Q.cap - 1));
+        while (*slot != 0) __nanosleep(32);
+        *slot = Q.order[a0 + k] + 1;
+    }
+}
+
+// after the visit: back to the queue when dirtied meanwhile or not converged, else clean
+__device__ __forceinline__ void q_finish(const QueueArgs &Q, int t, bool self_dirty)
+{
+    if (self_dirty) {
+        atomicExch(Q.state + t, 1);
+        q_enqueue(Q, t);
+        return;
+    }
+    if (atomicCAS(Q.state + t, 2, 0) == 2) {
+        atomicSub(&Q.ctl->work, 1);
+        return;
+    }
+    atomicExch(Q.state + t, 1);   // 3: a neighbour changed during the visit
+    q_enqueue(Q, t);
+}
+
+template <typename real, int PATH, int CPL, int WY, int WX>
+__global__ void __launch_bounds__(NW * 32, min_blocks<PATH>()) k_sweep_queue(KP<real> A, QueueArgs Q)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ int s_t, s_a0, s_m;
+    __shared__ unsigned long long s_pos;
+    const int tid = threadIdx.x;
+    for (;;) {
+        if (tid == 0) {
+            int a0 = 0, m = 0;
+            unsigned long long pos = 0;
+            s_t = q_next(Q, &a0, &m, &pos);
+            s_a0 = a0;
+            s_m = m;
+            s_pos = pos;
+        }
+        __syncthreads();
+        const int t = s_t;
+        if (t == -2) {
+            q_admit_cta(Q, s_a0, s_m, s_pos);
+            __syncthreads();
+            continue;
+        }
+        if (t < 0) return;
+        double r = 0.0, c = 0.0;
+        sweep_tile<real, PATH, CPL, WY, WX, false>(A, t, smem_raw, &r, &c);   // ends with a barrier
+        if (tid < 9) {
+            __threadfence();   // this visit's V writes before anyone sees the dirty marks
+            if (tid == 4) {
+                const unsigned long long seq = atomicAdd(&Q.ctl->visits, 1ull) + 1;
+                atomicMax(&Q.ctl->max_res, (unsigned long long)__double_as_longlong(r));
+                if (Q.tile_round) {
+                    Q.tile_round[t] = (int32_t)seq;
+                    for (int k = Q.lab_off[t]; k < Q.lab_off[t + 1]; ++k)
+                        atomicMax(&Q.patch_round[Q.lab_ids[k]], (int32_t)seq);
+                }
+                if (seq >= Q.ctl->max_visits) atomicExch(&Q.ctl->stop, 1);
+                q_finish(Q, t, r >= Q.tol);
+            } else if (c >= Q.tol_act) {
+                const int tx = t % A.g.tiles_x, ty = t / A.g.tiles_x;
+                const int ax = tx + (tid % 3) - 1, ay = ty + (tid / 3) - 1;
+                if (ax >= 0 && ay >= 0 && ax < A.g.tiles_x && ay < A.g.tiles_y) {
+                    const int nb = ay * A.g.tiles_x + ax;
+                    // only admitted tiles: the others are dirty anyway and enter on admission
+                    if (Q.rank[nb] < q_ld(&Q.ctl->adm)) q_mark_dirty(Q, nb);
+                }
+            }
+        }
+    }
+}
+
 template <typename real, int PATH, int CPL, int WY, int WX, bool CHECK>
 static cudaError_t launch_one(const SweepLaunch &L, cudaStream_t s)
 {
@@ -861,6 +1033,22 @@ static cudaError_t launch_one(const SweepLaunch &L, cudaStream_t s)
         if (grid > L.order.n_order) grid = L.order.n_order;
         if (grid <= 0) return cudaSuccess;
         kern<<<grid, NW * 32, smem, s>>>(A, L.order);
+        return cudaGetLastError();
+    }
+    if (L.queued && !CHECK) {
+        auto kern = k_sweep_queue<real, PATH, CPL, WY, WX>;
+        if (smem > 48 * 1024) {
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)smem);
+            if (e != cudaSuccess) return e;
+        }
+        int per_sm = 0, dev = 0, sms = 148;
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NW * 32, smem);
+        if (e != cudaSuccess) return e;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        // every CTA must be resident at once: idle CTAs spin on the queue
+        kern<<<std::max(1, per_sm) * sms, NW * 32, smem, s>>>(A, L.queue);
         return cudaGetLastError();
     }
     if ((L.ctl || L.occupancy_out) && !CHECK) {
@@ -1403,6 +1591,92 @@ __global__ void k_round_reset(RoundCtl *ctl, double thr)
     ctl->since_verify = 0;
     ctl->sweep_id += 1;   // the verification supersedes every recorded tile change
     ctl->round += 1;
+}
+
+// Key order of the tiles with free nodes for the work queue (a counting sort on NB buckets of the
+// min-u_hat key: admission needs the order of the front, not a total order of near-equal keys;
+// key == NULL: tile index order).  rank[t] = position, INT_MAX for tiles without free nodes.
+constexpr int QNB = 32768;
+__global__ void k_qo_max(const TileState T, const double *key, int n_tiles, unsigned long long *kmax)
+{
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long b = 0ull;
+    if (t < n_tiles && T.tile_free[t] > 0 && key && isfinite(key[t]))
+        b = (unsigned long long)__double_as_longlong(fmax(key[t], 0.0));
+    for (int o = 16; o > 0; o >>= 1) b = max(b, __shfl_xor_sync(FULL, b, o));
+    if ((threadIdx.x & 31) == 0 && b) atomicMax(kmax, b);
+}
+__device__ __forceinline__ int qo_bucket(const double *key, int t, const unsigned long long *kmax)
+{
+    if (!key) return 0;
+    const double km = __longlong_as_double((long long)*kmax);
+    const double k = key[t];
+    if (!(km > 0.0) || !isfinite(k)) return isfinite(k) ? 0 : QNB - 1;
+    return min(QNB - 1, max(0, (int)(fmax(k, 0.0) / km * (QNB - 1))));
+}
+__global__ void k_qo_hist(const TileState T, const double *key, int n_tiles,
+                          const unsigned long long *kmax, int32_t *hist, int32_t *rank)
+{
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n_tiles) return;
+    rank[t] = 0x7fffffff;
+    if (T.tile_free[t] > 0) atomicAdd(hist + qo_bucket(key, t, kmax), 1);
+}
+__global__ void k_qo_scatter(const TileState T, const double *key, int n_tiles,
+                             const unsigned long long *kmax, const int32_t *off, int32_t *cursor,
+                             int32_t *order, int32_t *rank)
+{
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n_tiles || T.tile_free[t] <= 0) return;
+    const int b = qo_bucket(key, t, kmax);
+    const int pos = off[b] + atomicAdd(cursor + b, 1);
+    order[pos] = t;
+    rank[t] = pos;
+}
+
+void launch_queue_order(const TileState &T, const double *key, int n_tiles, int32_t *scratch,
+                        int32_t *order, int32_t *rank, cudaStream_t s)
+{
+    // scratch: QNB hist + (QNB + 1) offsets + QNB cursors + 2 (kmax)
+    int32_t *hist = scratch, *off = scratch + QNB, *cur = off + QNB + 1;
+    unsigned long long *kmax = reinterpret_cast<unsigned long long *>(cur + QNB + 1);
+    cudaMemsetAsync(hist, 0, sizeof(int32_t) * QNB, s);
+    cudaMemsetAsync(cur, 0, sizeof(int32_t) * QNB, s);
+    cudaMemsetAsync(kmax, 0, sizeof(unsigned long long), s);
+    const int g = (n_tiles + 255) / 256;
+    k_qo_max<<<g, 256, 0, s>>>(T, key, n_tiles, kmax);
+    k_qo_hist<<<g, 256, 0, s>>>(T, key, n_tiles, kmax, hist, rank);
+    k_scan_offsets<<<1, 1024, 0, s>>>(hist, off, QNB);
+    k_qo_scatter<<<g, 256, 0, s>>>(T, key, n_tiles, kmax, off, cur, order, rank);
+}
+size_t queue_order_scratch_ints() { return 3 * (size_t)QNB + 1 + 4; }
+
+// (re-)seed the work queue after a verification pass: every tile whose residual is >= tol
+// (all tiles clean, admission complete): warp-aggregated reservations of work and ring slots
+__global__ void k_queue_seed(TileState T, QueueArgs Q, int n_tiles, double tol)
+{
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool take = t < n_tiles && T.tile_free[t] > 0 && T.tile_res[t] >= tol;
+    const unsigned m = __ballot_sync(FULL, take);
+    if (!m) return;
+    const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+    unsigned long long pos = 0;
+    if (lane == leader) {
+        atomicAdd(&Q.ctl->work, __popc(m));
+        pos = atomicAdd(&Q.ctl->tail, (unsigned long long)__popc(m));
+    }
+    pos = __shfl_sync(FULL, pos, leader);
+    if (take) {
+        Q.state[t] = 1;
+        Q.ring[(pos + __popc(m & ((1u << lane) - 1u))) & (unsigned long long)(Q.cap - 1)] = t + 1;
+    }
+}
+
+void launch_queue_seed(const TileGeom &g, const TileState &T, const QueueArgs &Q, int n_tiles,
+                       double tol, cudaStream_t s)
+{
+    (void)g;
+    k_queue_seed<<<(n_tiles + 255) / 256, 256, 0, s>>>(T, Q, n_tiles, tol);
 }
 
 void launch_round_begin(RoundCtl *ctl, ActCounters *c, cudaStream_t s) { k_round_begin<<<1, 1, 0, s>>>(ctl, c); }

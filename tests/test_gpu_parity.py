@@ -173,7 +173,7 @@ def test_solve_parity_random_general_fp64():
 
 @pytest.mark.parametrize("mode,schedule,policy", [
     ("patchy", "ordered", 0), ("static", "ordered", 0), ("patchy", "rounds", 1),
-    ("patchy", "rounds", 2)])
+    ("patchy", "rounds", 2), ("patchy", "queue", 0), ("static", "queue", 0)])
 def test_schedules_reach_the_same_fixed_point(mode, schedule, policy):
     """Every tile schedule (ordered Gauss-Seidel passes, Delta-stepping buckets, upstream-ready
     admission) converges to the oracle's fixed point (R29)."""
