@@ -114,32 +114,38 @@ typedef struct {
                             (the signs of u_hat's differences over the tile); incoherent tiles
                             continue an orientation cycle across visits                     */
     double tol;          /* sup-norm residual tolerance eps                                  */
-    int64_t max_rounds;  /* cap on tile rounds                                               */
+    int64_t max_rounds;  /* cap on tile rounds (schedule 2: on the average number of visits
+                            per tile with free nodes)                                      */
     double delta;        /* patchy bucket width in value units; 0 = automatic; < 0 = off      */
     int32_t kernel;      /* 0 auto, 1 general stencil, 2 row-table stencil, 3 row-table one
                             node per warp step (A/B only).  The fp32 row-table kernel's tile
                             is 32 x 64 nodes, or 16 x 128 for static solves on grids where
                             128 dx <= 1/8 (pdd_set_tile_cols forces one
                             geometry)                                                        */
-    int32_t schedule;    /* 0 rounds (default): rounds over the list of active tiles, every
-                            tile visit an in-tile Gauss-Seidel solve; patchy admits tiles in
-                            buckets of min u_hat of width delta;
+    int32_t schedule;    /* 0 automatic (= 2);
                             1 ordered: Gauss-Seidel passes over the tiles in key order (u_hat
                             for patchy, block-lexicographic for static), each tile waiting for
                             its lower-key neighbours (delta = key slack);
-                            2 queue: one persistent launch whose CTAs pop dirty tiles from a
-                            work queue and mark the neighbours of changed tiles dirty (no
-                            rounds); patchy admits tiles in min-u_hat order while fewer tiles
-                            than resident CTAs are queued; then the verification pass     */
+                            2 queue: one persistent launch whose CTAs take dirty tiles from a
+                            work queue, visit them (an in-tile Gauss-Seidel solve) and mark the
+                            neighbours of changed tiles dirty -- asynchronous relaxation, no
+                            rounds; patchy admits tiles in min-u_hat order:
+                            a tile that converges admits the next one, so that about
+                            queue_target tiles are queued or being visited; a full-grid
+                            verification pass re-seeds the queue if needed;
+                            3 rounds: rounds over the list of active tiles (one launch per
+                            round); patchy admits tiles in buckets of min u_hat of width
+                            delta                                                            */
     int32_t early_exit_off; /* 1: every tile visit does all k_inner sweeps (A/B; default 0: a
                             visit stops after the first sweep changing no node by >= tol)   */
-    int32_t bucket_policy;  /* patchy, schedule 0: 0 moving front (the threshold advances every
+    int32_t bucket_policy;  /* patchy, schedule 3: 0 moving front (the threshold advances every
                             round, faster while a round under-fills the GPU); 1 classic
                             Delta-stepping (a bucket opens once the previous one settled); 2
                             upstream-ready (no front: a tile waits for unconverged neighbours
                             with min u_hat lower by more than delta)                        */
     int32_t trace;       /* > 0: one line per round on stderr (one round per batch)          */
-    int32_t reserved;
+    int32_t queue_target; /* schedule 2, patchy: tiles kept queued or visiting; 0 = automatic
+                            (two waves of resident sweep CTAs)                             */
 } pdd_solve_opts;
 
 typedef struct {

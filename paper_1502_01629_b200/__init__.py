@@ -195,14 +195,16 @@ class Solver:
 
     def solve(self, mode="patchy", tol: float = 1e-6, k_inner: Optional[int] = None,
               max_rounds: int = 200000, delta: float = 0.0, kernel: int = 0,
-              schedule: str = "rounds", raise_on_noconverge: bool = True,
-              early_exit: bool = True, bucket_policy: int = 0, trace: bool = False) -> dict:
+              schedule: str = "auto", raise_on_noconverge: bool = True,
+              early_exit: bool = True, bucket_policy: int = 0, trace: bool = False,
+              queue_target: int = 0) -> dict:
         o = N.pdd_solve_opts()
         o.mode = MODE_PATCHY if mode in ("patchy", 0) else MODE_STATIC
         if k_inner is None:   # 0 = automatic in libpdd: 1 patchy / 4 static,
             k_inner = 0       # 4 for a patchy grid that fits one wave of sweep CTAs
         o.k_inner, o.tol, o.max_rounds, o.delta, o.kernel = int(k_inner), float(tol), int(max_rounds), float(delta), int(kernel)
-        o.schedule = {"rounds": 0, "ordered": 1, "queue": 2}.get(schedule, schedule)
+        o.schedule = {"auto": 0, "ordered": 1, "queue": 2, "rounds": 3}.get(schedule, schedule)
+        o.queue_target = int(queue_target)
         o.early_exit_off = 0 if early_exit else 1
         o.bucket_policy = int(bucket_policy)
         o.trace = 1 if trace else 0

@@ -53,7 +53,7 @@ class pdd_solve_opts(C.Structure):
     _fields_ = [("mode", C.c_int32), ("k_inner", C.c_int32), ("tol", C.c_double),
                 ("max_rounds", C.c_int64), ("delta", C.c_double), ("kernel", C.c_int32),
                 ("schedule", C.c_int32), ("early_exit_off", C.c_int32),
-                ("bucket_policy", C.c_int32), ("trace", C.c_int32), ("reserved", C.c_int32)]
+                ("bucket_policy", C.c_int32), ("trace", C.c_int32), ("queue_target", C.c_int32)]
 
 
 class pdd_solve_stats(C.Structure):

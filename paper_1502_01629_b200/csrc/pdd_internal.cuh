@@ -201,28 +201,34 @@ struct OrderArgs {
     int32_t *patch_round;
 };
 
-// Work-queue schedule (k_sweep_queue): persistent CTAs pop dirty tiles from a ring, visit them
-// and mark their neighbours dirty -- asynchronous (chaotic) relaxation of the same monotone
-// contraction (R29) without rounds.  Tiles enter the queue in key order (min u_hat for patchy,
-// all at once for static) while the queue holds fewer than `fill` tiles.
+// Work-queue schedule (k_sweep_queue): persistent CTAs take dirty tiles from a ticket ring, visit
+// them and mark the neighbours of changed tiles dirty -- asynchronous (chaotic) relaxation of the
+// same monotone contraction (R29) without rounds.  Patchy: tiles enter in key order (min u_hat,
+// P:744-749) so that about `target` tiles are queued or being visited at any time: a tile that
+// converges admits the next one of the order (a sliding window of the lowest unconverged keys).
+// Static: every tile is queued at the start.
 struct QueueCtl {
-    unsigned long long head, tail;   // ring cursors (monotone)
+    unsigned long long head;         // consumer tickets handed out (monotone)
+    unsigned long long tail;         // ring positions handed to producers (monotone)
     unsigned long long visits;       // tile visits so far (the visit sequence number)
-    unsigned long long max_visits;   // stop once reached (non-convergence guard)
-    int work;                        // tiles queued or being visited
-    int adm;                         // tiles admitted from the key order
-    int lock;                        // admission lock
-    int stop;
+    unsigned long long max_visits;   // stop = 2 once reached (non-convergence guard)
+    unsigned long long verify_at;    // stop = 3 once reached: the host runs a verification pass (a
+                                     // tolerance below the arithmetic's noise floor keeps tiles
+                                     // re-queuing each other; the Jacobi check is authoritative)
+    int work;                        // tiles queued or being visited (+ admissions in flight)
+    int adm;                         // next position of the key order to admit (>= n_order: all in)
+    int stop;                        // 1: queue drained for good, 2: visit cap, 3: verification due
+    int pad;
     unsigned long long max_res;      // ordered bits of the max visit residual (report)
 };
 struct QueueArgs {
     QueueCtl *ctl;
-    int32_t *ring;                   // capacity cap (power of two, >= 2 n_tiles), 0 = empty slot
-    unsigned cap;
+    int32_t *ring;                   // cap slots, 0 = empty, else tile + 1
+    unsigned cap;                    // power of two > tiles + resident CTAs
     const int32_t *order;            // tiles with free nodes in key order
     const int32_t *rank;             // position of each tile in order (INT_MAX: not listed)
     int n_order;
-    int fill;                        // admission keeps >= fill tiles queued while tiles remain
+    int target;                      // admission keeps about this many tiles queued or visiting
     int *state;                      // per tile: 0 clean, 1 queued, 2 visiting, 3 visiting + dirty
     double tol;                      // re-queue a tile whose last sweep changed >= tol
     double tol_act;                  // mark the 8 neighbours dirty when the visit changed >= tol_act
@@ -271,10 +277,12 @@ struct SweepLaunch {
                                          //   CTAs per SM and launch nothing
 };
 
-// work-queue schedule: (re-)seed the queue with the tiles whose residual is >= tol (after a
-// verification pass), n_order = 0 keeps admission closed
-void launch_queue_seed(const TileGeom &g, const TileState &T, const QueueArgs &Q, int n_tiles,
-                       double tol, cudaStream_t s);
+// work-queue schedule: (re-)seed the zeroed ring -- first > 0: with the first `first` tiles of the
+// key order (start of a patchy solve); else with every tile among the first `adm` of the order
+// whose residual is >= tol (static start: tol < 0 takes all; after a verification pass: the
+// offending tiles)
+void launch_queue_seed(const TileState &T, const QueueArgs &Q, int n_tiles, double tol, int first,
+                       int adm, cudaStream_t s);
 // order / rank of the tiles with free nodes by key (NULL: tile index order); scratch of
 // queue_order_scratch_ints() ints
 void launch_queue_order(const TileState &T, const double *key, int n_tiles, int32_t *scratch,

@@ -379,8 +379,8 @@ static size_t layout(pdd_ctx *c, void *ws, const pdd_problem *f, const pdd_probl
     T.stamp = cv.take<long long>(tmax);
     T.ocounters = cv.take<OrdCounters>(1);
     RoundCtl *rctl = cv.take<RoundCtl>(1);
-    unsigned qcap = 1;
-    while (qcap < 2u * (unsigned)tmax) qcap <<= 1;
+    unsigned qcap = 1;   // > tiles + resident sweep CTAs (ticket ring, sweep.cu)
+    while (qcap < 2u * (unsigned)tmax + 8192u) qcap <<= 1;
     QueueCtl *qctl = cv.take<QueueCtl>(1);
     int32_t *qring = cv.take<int32_t>(qcap);
     int *qstate = cv.take<int>(tmax);
@@ -1105,14 +1105,9 @@ static pdd_status queue_loop(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_st
     // tiles in key order: min u_hat (patchy) or index order (static)
     launch_queue_order(ctx->T, o->mode == 0 ? ctx->T.tile_minu : nullptr, nt, ctx->qscratch,
                        ctx->T.order, ctx->qrank, s);
+    ctx->launches += 4;
     CK(cudaMemsetAsync(ctx->qstate, 0, sizeof(int) * nt, s));
     CK(cudaMemsetAsync(ctx->T.tile_sweeps, 0, sizeof(int32_t) * nt, s));
-    CK(cudaMemsetAsync(ctx->qring, 0, sizeof(int32_t) * ctx->qcap, s));
-    QueueCtl qc{};
-    // cap on visits ~ max_rounds waves of resident CTAs (non-convergence guard)
-    qc.max_visits = (unsigned long long)std::max<int64_t>(1, o->max_rounds) * (unsigned long long)resident;
-    qc.adm = o->mode == 0 ? 0 : tiles_free;   // static: every tile at once (seeded below)
-    CK(cudaMemcpyAsync(ctx->qctl, &qc, sizeof qc, cudaMemcpyHostToDevice, s));
     QueueArgs Q{};
     Q.ctl = ctx->qctl;
     Q.ring = ctx->qring;
@@ -1120,39 +1115,65 @@ static pdd_status queue_loop(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_st
     Q.order = ctx->T.order;
     Q.rank = ctx->qrank;
     Q.n_order = tiles_free;
-    Q.fill = o->mode == 0 ? std::max(1, resident) : tiles_free;
+    // patchy: about two waves of resident CTAs queued or visiting at any time (A/B: PDD_QW)
+    const char *qe = dev_env("PDD_QW");
+    Q.target = o->queue_target > 0 ? o->queue_target : std::max(1, (int)((qe ? std::atof(qe) : 2.0) * resident));
     Q.state = ctx->qstate;
     Q.tol = o->tol;
-    Q.tol_act = o->tol;
+    const char *te = dev_env("PDD_TACT");   // A/B: neighbour-change activation threshold / tol
+    Q.tol_act = o->tol * (te ? std::atof(te) : 1.0);
     Q.tile_round = ctx->T.tile_round;
     Q.lab_off = ctx->T.tile_lab_off;
     Q.lab_ids = ctx->T.tile_lab_ids;
     Q.patch_round = ctx->T.patch_round;
-    if (o->mode != 0) launch_queue_seed(ctx->g, ctx->T, Q, nt, -1.0, s);   // tile_res = inf
+    if ((unsigned)(nt + resident) >= ctx->qcap) return fail(ctx, PDD_E_NOMEM, "work-queue ring too small");
+    QueueCtl qc{};
+    // cap on visits: max_rounds visits per tile with free nodes (non-convergence guard)
+    qc.max_visits = (unsigned long long)std::max<int64_t>(1, o->max_rounds) *
+                    (unsigned long long)std::max(1, tiles_free);
+    qc.adm = o->mode == 0 ? 0 : tiles_free;   // static: every tile is seeded at once
     double best = INFINITY;
     int stalled = 0;
+    bool first = true;
     for (;;) {
+        // ring and cursors start empty at every launch (tickets abandoned at the last stop)
+        CK(cudaMemsetAsync(ctx->qring, 0, sizeof(int32_t) * ctx->qcap, s));
+        qc.head = qc.tail = 0;
+        qc.work = 0;
+        qc.stop = 0;
+        // a launch ends for a verification after 32 visits per tile (legitimate solves need about
+        // as many in total; the check costs one sweep-equivalent)
+        qc.verify_at = qc.visits + 32ull * (unsigned long long)std::max(1, tiles_free) + 1024ull;
+        CK(cudaMemcpyAsync(ctx->qctl, &qc, sizeof qc, cudaMemcpyHostToDevice, s));
+        if (first && o->mode == 0)
+            launch_queue_seed(ctx->T, Q, nt, 0.0, std::min(Q.target, tiles_free), 0, s);
+        else
+            launch_queue_seed(ctx->T, Q, nt, first ? -1.0 : o->tol, 0, qc.adm, s);   // static start: tile_res = inf
+        ctx->launches++;
+        first = false;
         SweepLaunch L = make_launch(ctx, nullptr, 0, k_inner, 0, nullptr);
         L.early_tol = o->early_exit_off ? 0.0 : o->tol;
         L.tile_sweeps = ctx->T.tile_sweeps;
         L.queued = 1;
         L.queue = Q;
         CK(cudaEventRecord(ctx->ev[2], s));
-        CK(launch_sweep(L, s));
-        ctx->launches++;
+        if (tiles_free > 0) {
+            CK(launch_sweep(L, s));
+            ctx->launches++;
+        }
         CK(cudaEventRecord(ctx->ev[3], s));
-        QueueCtl h{};
-        CK(cudaMemcpyAsync(&h, ctx->qctl, sizeof h, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(&qc, ctx->qctl, sizeof qc, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         float ms = 0.f;
         cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]);
         ms_sweep += ms;
         S.rounds++;
-        S.tiles_processed = (int64_t)h.visits;
+        S.tiles_processed = (int64_t)qc.visits;
         if (trace)
-            fprintf(stderr, "[pdd] queue launch: visits %llu maxres %.3e stop %d %.3f ms\n", h.visits,
-                    bits_to_double(h.max_res), h.stop, ms);
-        if (h.stop) break;   // visit cap reached
+            fprintf(stderr, "[pdd] queue launch: visits %llu maxres %.3e stop %d adm %d %.3f ms\n", qc.visits,
+                    bits_to_double(qc.max_res), qc.stop, qc.adm, ms);
+        if (qc.stop == 2) break;   // visit cap reached
+        if (qc.stop != 3) qc.adm = std::max(qc.adm, tiles_free);
         // full-grid verification with each patch's own residual
         CK(cudaEventRecord(ctx->ev[2], s));
         SweepLaunch V = make_launch(ctx, ctx->T.all_list, nt, 1, 1, nullptr);
@@ -1176,8 +1197,7 @@ static pdd_status queue_loop(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_st
         }
         if (last_verify < 0.9 * best) { best = last_verify; stalled = 0; }
         else if (++stalled >= 8) break;   // below the arithmetic's noise floor: give up
-        launch_queue_seed(ctx->g, ctx->T, Q, nt, o->tol, s);
-        ctx->launches++;
+        CK(cudaMemsetAsync(ctx->qstate, 0, sizeof(int) * nt, s));
     }
     return PDD_OK;
 }
@@ -1189,7 +1209,9 @@ pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
     if (!ctx) return fail(nullptr, PDD_E_INVALID, "ctx is NULL");
     if (!o) return fail(ctx, PDD_E_INVALID, "opts is NULL");
     if (o->mode != 0 && o->mode != 1) return fail(ctx, PDD_E_INVALID, "mode must be 0 or 1");
-    if (o->schedule < 0 || o->schedule > 2) return fail(ctx, PDD_E_INVALID, "schedule must be 0, 1 or 2");
+    if (o->schedule < 0 || o->schedule > 3) return fail(ctx, PDD_E_INVALID, "schedule must be 0..3");
+    if (o->queue_target < 0) return fail(ctx, PDD_E_INVALID, "queue_target must be >= 0");
+    const int sched = o->schedule == 0 ? 2 : o->schedule;   // automatic: the work queue
     if (o->k_inner < 0 || o->k_inner > 1024) return fail(ctx, PDD_E_INVALID, "k_inner outside 0..1024");
     if (!(o->tol > 0.0)) return fail(ctx, PDD_E_INVALID, "tol must be > 0");
     if (o->mode == 0 && (!ctx->synth_done || ctx->labels_mode != 1))
@@ -1283,19 +1305,19 @@ pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
     bool converged = false;
     double last_verify = INFINITY;
     float ms_sweep = 0.f, ms_verify = 0.f;
-    if (o->schedule == 1) {
+    if (sched == 1) {
         pdd_status r = ordered_loop(ctx, o, S, trace, converged, last_verify, ms_sweep, ms_verify);
         if (r != PDD_OK) return r;
     }
-    if (o->schedule == 2) {
+    if (sched == 2) {
         pdd_status r = queue_loop(ctx, o, S, trace, k_inner, resident, tiles_free, converged,
                                   last_verify, ms_sweep, ms_verify);
         if (r != PDD_OK) return r;
     }
-    // Device-driven rounds (schedule 0): batches of (begin, activate, sweep, end) are enqueued
+    // Device-driven rounds (schedule 3): batches of (begin, activate, sweep, end) are enqueued
     // without a host round trip; the RoundCtl block carries the front threshold and the stop
     // flag between them.  The host syncs once per batch and runs the verification pass.
-    if (o->schedule == 0) {
+    if (sched == 3) {
         RoundCtl c0{};
         c0.thr = thr;
         c0.delta = delta;
@@ -1317,11 +1339,11 @@ pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
     const char *te = dev_env("PDD_TACT");   // A/B: neighbour-change activation threshold / tol
     const double tact = te ? std::atof(te) : 1.0;
     long long rounds_prev = 0;
-    while (o->schedule == 0) {
+    while (sched == 3) {
         if (S.rounds >= o->max_rounds) break;
         CK(cudaEventRecord(ctx->ev[2], s));
         SweepLaunch L = make_launch(ctx, ctx->T.list[cur], ctx->n_tiles, k_inner, 0, nullptr);
-        L.early_tol = o->early_exit_off ? 0.0 : o->tol;   // reserved[0] = 1 disables early exit
+        L.early_tol = o->early_exit_off ? 0.0 : o->tol;   // early_exit_off = 1 disables early exit
         L.ctl = ctx->rctl;
         L.acnt = reinterpret_cast<ActCounters *>(ctx->T.counters);
         L.tile_stamp = ctx->T.tile_stamp;

@@ -464,13 +464,39 @@ __device__ __forceinline__ void row_table(const KP<real> &A, real *s_u, const re
 
 constexpr bool kRawMinRef = PDD_RAWMIN != 0;   // fp32 path 3: V_ref = staged min (sweep_gs.cuh)
 
+// PDD_TIMING (development builds): thread 0 of every CTA adds the cycles of each phase of a tile
+// visit to g_phase (0 fetch / queue, 1 stage loads, 2 convert + smem stores, 3 sweeps, 4 residual
+// reduction, 5 write-back, 6 bookkeeping); read and reset by pdd_dev_phases()
+#ifndef PDD_TIMING
+#define PDD_TIMING 0
+#endif
+#if PDD_TIMING
+__device__ unsigned long long g_phase[8];
+__device__ __forceinline__ void phase_mark(int i, long long &t_prev)
+{
+    if (threadIdx.x == 0) {
+        const long long now = clock64();
+        atomicAdd(&g_phase[i], (unsigned long long)(now - t_prev));
+        t_prev = now;
+    }
+}
+#define PDD_PHASE(i) phase_mark(i, t_phase)
+#else
+#define PDD_PHASE(i) ((void)0)
+#endif
+
 // ------------------------------------------------------------------ one tile visit
 // Stage tile + halo, relax k_inner times, write back.  Global V is read with ld.global.cg (L2):
 // in the ordered (persistent) schedule other CTAs update V during the launch.
 template <typename real, int PATH, int CPL, int WY, int WX, bool CHECK>
 __device__ __forceinline__ void sweep_tile(const KP<real> &A, int t, unsigned char *smem_raw,
-                                           double *res_out, double *chg_out)
+                                           double *res_out, double *chg_out
+#if PDD_TIMING
+                                           , long long &t_phase
+#endif
+                                           )
 {
+    PDD_PHASE(0);
     constexpr int TW = PATH == 2 ? TWOf<WY, WX>::value : PATH == 3 ? TW3 : TW_GENERAL;
     constexpr int THt = PATH == 3 ? TH3 : TH;      // tile rows of this path
     constexpr int NCOPY = PATH == 3 ? 4 : 1;
@@ -508,6 +534,7 @@ __device__ __forceinline__ void sweep_tile(const KP<real> &A, int t, unsigned ch
     for (int o = 16; o > 0; o >>= 1) vmin = fmin(vmin, __shfl_xor_sync(FULL, vmin, o));
     if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = vmin;
     __syncthreads();
+    PDD_PHASE(1);
     // V_ref <= V0 keeps D = h l - (1 - beta) V_ref >= 0 also for inputs above the supersolution
     // V0 (pdd_apply_operator on arbitrary V, u_hat above V0 in enclosed regions)
     double Vref;
@@ -551,6 +578,7 @@ __device__ __forceinline__ void sweep_tile(const KP<real> &A, int t, unsigned ch
             for (int e = threadIdx.x; e < PRES_SH; e += blockDim.x) pres_table()[e] = 0ull;
     }
     __syncthreads();
+    PDD_PHASE(2);
 
     // D = h l - (1 - beta) V_ref >= 0 (V_ref <= V0 = h l / (1 - beta); the clamp removes fp64
     // rounding noise at V_ref = V0) for a constant cost; a cost field uses D per node in the
@@ -595,6 +623,7 @@ __device__ __forceinline__ void sweep_tile(const KP<real> &A, int t, unsigned ch
         }
     }
 
+    PDD_PHASE(3);
     // tile residual of the last sweep (path 3 commits from lanes 0, 8, 16, 24)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) res = rmax(res, __shfl_xor_sync(FULL, res, o));
@@ -616,6 +645,7 @@ __device__ __forceinline__ void sweep_tile(const KP<real> &A, int t, unsigned ch
         return;
     }
     __syncthreads();
+    PDD_PHASE(4);
 
     // write back changed interior nodes, net change of the visit
     double chg = 0.0;
@@ -648,12 +678,13 @@ __device__ __forceinline__ void sweep_tile(const KP<real> &A, int t, unsigned ch
         if (gi >= n || gj >= n) continue;
         const int64_t gidx = (int64_t)gj * n + gi;
         if (A.P.kind[gidx] != 0) continue;
-        const real u = s_u[(ly + H) * pitch + lx + H];
+        // the visit's net change is measured on the stored values: an update below the
+        // rounding of V = V_ref + u (fp64 runs: |u| << |V|) changes nothing and wakes nobody
+        const double vnew = Vref + (double)s_u[(ly + H) * pitch + lx + H];
         const double vold = __ldcg(A.V + gidx);
-        const real uold = (real)(vold - Vref);
-        if (u != uold) {
-            A.V[gidx] = Vref + (double)u;
-            chg = fmax(chg, fabs((double)u - (double)uold));
+        if (vnew != vold) {
+            A.V[gidx] = vnew;
+            chg = fmax(chg, fabs(vnew - vold));
         }
     }
 #pragma unroll
@@ -674,6 +705,7 @@ __device__ __forceinline__ void sweep_tile(const KP<real> &A, int t, unsigned ch
     }
     if (chg_out) *chg_out = cm;
     __syncthreads();
+    PDD_PHASE(5);
 }
 
 // Round schedule: one CTA per listed tile (chaotic relaxation across the tiles of a launch).
@@ -681,7 +713,12 @@ template <typename real, int PATH, int CPL, int WY, int WX, bool CHECK>
 __global__ void __launch_bounds__(NW * 32, min_blocks<PATH>()) k_sweep(KP<real> A)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    #if PDD_TIMING
+    long long t_phase = clock64();
+    sweep_tile<real, PATH, CPL, WY, WX, CHECK>(A, A.list[blockIdx.x], smem_raw, nullptr, nullptr, t_phase);
+#else
     sweep_tile<real, PATH, CPL, WY, WX, CHECK>(A, A.list[blockIdx.x], smem_raw, nullptr, nullptr);
+#endif
 }
 
 // Device-driven round: persistent CTAs take the activated tiles one at a time (dynamic fetch),
@@ -693,6 +730,9 @@ __global__ void __launch_bounds__(NW * 32, min_blocks<PATH>()) k_sweep_dyn(KP<re
     __shared__ int s_t;
     if (A.ctl->stop) return;
     const int count = A.acnt->count;
+#if PDD_TIMING
+    long long t_phase = clock64();
+#endif
 #if PDD_PREFETCH
     // fetch one tile ahead and pull its tile + halo rows of V into L2 while the current tile is
     // swept, so that the next visit's staging loads hit L2 instead of HBM
@@ -727,7 +767,11 @@ __global__ void __launch_bounds__(NW * 32, min_blocks<PATH>()) k_sweep_dyn(KP<re
                     asm volatile("prefetch.global.L2 [%0];" ::"l"(A.V + (int64_t)gj * n + gi));
             }
         }
+        #if PDD_TIMING
+        sweep_tile<real, PATH, CPL, WY, WX, false>(A, t, smem_raw, nullptr, nullptr, t_phase);
+#else
         sweep_tile<real, PATH, CPL, WY, WX, false>(A, t, smem_raw, nullptr, nullptr);
+#endif
     }
 #else
     for (;;) {
@@ -739,7 +783,11 @@ __global__ void __launch_bounds__(NW * 32, min_blocks<PATH>()) k_sweep_dyn(KP<re
         const int t = s_t;
         __syncthreads();
         if (t < 0) return;
+        #if PDD_TIMING
+        sweep_tile<real, PATH, CPL, WY, WX, false>(A, t, smem_raw, nullptr, nullptr, t_phase);
+#else
         sweep_tile<real, PATH, CPL, WY, WX, false>(A, t, smem_raw, nullptr, nullptr);
+#endif
     }
 #endif
 }
@@ -757,6 +805,9 @@ __global__ void __launch_bounds__(NW * 32, min_blocks<PATH>()) k_sweep_ordered(K
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ int s_idx;
     const int tid = threadIdx.x;
+#if PDD_TIMING
+    long long t_phase = clock64();
+#endif
     for (;;) {
         if (tid == 0) s_idx = atomicAdd(O.counter, 1);
         __syncthreads();
@@ -791,7 +842,11 @@ __global__ void __launch_bounds__(NW * 32, min_blocks<PATH>()) k_sweep_ordered(K
         const bool need = __syncthreads_or(pred) && O.tile_free[t] > 0;
         if (need) {
             double r = 0.0, c = 0.0;
+#if PDD_TIMING
+            sweep_tile<real, PATH, CPL, WY, WX, false>(A, t, smem_raw, &r, &c, t_phase);
+#else
             sweep_tile<real, PATH, CPL, WY, WX, false>(A, t, smem_raw, &r, &c);
+#endif
             if (tid == 0 && O.tile_round) {
                 O.tile_round[t] = max(O.tile_round[t], O.pass);
                 for (int k = O.lab_off[t]; k < O.lab_off[t + 1]; ++k) atomicMax(&O.patch_round[O.lab_ids[k]], O.pass);
@@ -813,23 +868,45 @@ __global__ void __launch_bounds__(NW * 32, min_blocks<PATH>()) k_sweep_ordered(K
 
 // ------------------------------------------------------------------ work-queue schedule
 // Tile states: 0 clean, 1 queued, 2 visiting, 3 visiting and dirtied meanwhile.  A queued or
-// visiting tile holds one unit of ctl->work; the queue is empty for good when work == 0 and every
-// tile has been admitted.
-__device__ __forceinline__ unsigned long long q_ld64(const unsigned long long *p)
-{
-    return *(volatile const unsigned long long *)p;
-}
+// visiting tile holds one unit of ctl->work (an admission in flight reserves one too); the queue
+// is drained for good when work reaches 0 with every tile admitted.
+// The ring is a ticket queue: a consumer takes ticket h = head++ and waits for slot h & (cap - 1)
+// to be filled; a producer takes position p = tail++ and fills slot p & (cap - 1).  No CTA ever
+// polls the cursors, each waits on its own slot (cap > tiles + resident CTAs: two outstanding
+// tickets never share a slot).
 __device__ __forceinline__ int q_ld(const int *p) { return *(volatile const int *)p; }
 
-__device__ __forceinline__ void q_enqueue(const QueueArgs &Q, int t)
+__device__ __forceinline__ void q_push(const QueueArgs &Q, int t)
 {
     const unsigned long long pos = atomicAdd(&Q.ctl->tail, 1ull);
     volatile int32_t *slot = Q.ring + (pos & (unsigned long long)(Q.cap - 1));
-    while (*slot != 0) __nanosleep(32);   // a slow consumer of the previous lap still reads it
+    while (*slot != 0) __nanosleep(32);   // the consumer of the previous lap still reads it
     *slot = t + 1;
 }
 
-// a neighbour (or the admission) dirtied tile t
+// one unit of work is gone; the last one (with every tile admitted) ends the launch
+__device__ __forceinline__ void q_release(const QueueArgs &Q)
+{
+    if (atomicSub(&Q.ctl->work, 1) == 1 && q_ld(&Q.ctl->adm) >= Q.n_order) atomicExch(&Q.ctl->stop, 1);
+}
+
+// admit the next tile of the key order (lock-free: the reservation of a unit of work comes first,
+// so work cannot reach 0 while an admission is in flight)
+__device__ __forceinline__ void q_admit_one(const QueueArgs &Q)
+{
+    atomicAdd(&Q.ctl->work, 1);
+    const int a = atomicAdd(&Q.ctl->adm, 1);
+    if (a < Q.n_order) {
+        const int t = Q.order[a];
+        if (atomicCAS(Q.state + t, 0, 1) == 0) {   // else a neighbour queued it already
+            q_push(Q, t);
+            return;
+        }
+    }
+    q_release(Q);
+}
+
+// a neighbour dirtied tile t
 __device__ __forceinline__ void q_mark_dirty(const QueueArgs &Q, int t)
 {
     int st = q_ld(Q.state + t);
@@ -838,7 +915,7 @@ __device__ __forceinline__ void q_mark_dirty(const QueueArgs &Q, int t)
             const int o = atomicCAS(Q.state + t, 0, 1);
             if (o == 0) {
                 atomicAdd(&Q.ctl->work, 1);
-                q_enqueue(Q, t);
+                q_push(Q, t);
                 return;
             }
             st = o;
@@ -852,114 +929,88 @@ __device__ __forceinline__ void q_mark_dirty(const QueueArgs &Q, int t)
     }
 }
 
-// thread 0: the next action of the CTA.  Returns a tile to visit (>= 0), -1 when the queue is
-// finished (or stopped), or -2 after reserving an admission (*a0, *m, *pos0: the next m tiles of
-// the key order go to ring positions pos0.., the lock is held until the CTA publishes them).
-__device__ int q_next(const QueueArgs &Q, int *a0, int *m, unsigned long long *pos0)
+// thread 0: wait for the next tile (>= 0), or -1 once the queue has stopped
+__device__ __forceinline__ int q_pop(const QueueArgs &Q)
 {
-    QueueCtl *c = Q.ctl;
-    for (;;) {
-        if (q_ld(&c->stop)) return -1;
-        const unsigned long long h = q_ld64(&c->head), tl = q_ld64(&c->tail);
-        const int adm = q_ld(&c->adm);
-        if (adm < Q.n_order && (long long)(tl - h) < Q.fill && atomicCAS(&c->lock, 0, 1) == 0) {
-            // tiles are admitted in key order (nodes processed in increasing u_hat)
-            // while the queue holds fewer than `fill` tiles: the GPU stays full, the front
-            // moves as fast as the tiles behind it converge
-            const int a = q_ld(&c->adm);
-            const long long ql = (long long)(q_ld64(&c->tail) - q_ld64(&c->head));
-            const int k = (int)min((long long)(Q.n_order - a), (long long)Q.fill - ql);
-            if (k > 0) {
-                *a0 = a;
-                *m = k;
-                atomicAdd(&c->work, k);
-                *pos0 = atomicAdd(&c->tail, (unsigned long long)k);
-                return -2;
-            }
-            atomicExch(&c->lock, 0);
-            continue;
+    const unsigned long long h = atomicAdd(&Q.ctl->head, 1ull);
+    volatile int32_t *slot = Q.ring + (h & (unsigned long long)(Q.cap - 1));
+    int v;
+    // watchdog: no visit finished anywhere for ~1 s of waiting (a visit takes ~0.1 ms) can only be
+    // a lost unit of work: stop with the non-convergence code instead of hanging the GPU
+    unsigned long long seen = *(volatile unsigned long long *)&Q.ctl->visits;
+    long long t0 = clock64();
+    while ((v = *slot) == 0) {
+        if (q_ld(&Q.ctl->stop)) return -1;
+        __nanosleep(200);
+        if (clock64() - t0 > (1ll << 31)) {
+            const unsigned long long now = *(volatile unsigned long long *)&Q.ctl->visits;
+            if (now == seen) atomicExch(&Q.ctl->stop, 2);
+            seen = now;
+            t0 = clock64();
         }
-        if (h < tl) {
-            if (atomicCAS(&c->head, h, h + 1) == h) {
-                volatile int32_t *slot = Q.ring + (h & (unsigned long long)(Q.cap - 1));
-                int v;
-                while ((v = *slot) == 0) __nanosleep(32);   // the producer's store is on its way
-                *slot = 0;
-                const int t = v - 1;
-                atomicExch(Q.state + t, 2);   // queued -> visiting (only the popper changes 1)
-                __threadfence();
-                return t;
-            }
-            continue;
-        }
-        if (q_ld(&c->work) == 0 && adm >= Q.n_order) return -1;
-        __nanosleep(64);
     }
+    *slot = 0;
+    const int t = v - 1;
+    atomicExch(Q.state + t, 2);   // queued -> visiting (only the consumer changes state 1)
+    __threadfence();              // the visit's loads come after the state change
+    return t;
 }
 
-// the whole CTA publishes an admission reserved by q_next: states first (a neighbour that sees
-// the new adm must find the tile queued), then adm, then the ring slots
-__device__ void q_admit_cta(const QueueArgs &Q, int a0, int m, unsigned long long pos0)
-{
-    for (int k = threadIdx.x; k < m; k += blockDim.x) Q.state[Q.order[a0 + k]] = 1;
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        *(volatile int *)&Q.ctl->adm = a0 + m;
-        __threadfence();
-        atomicExch(&Q.ctl->lock, 0);
-    }
-    for (int k = threadIdx.x; k < m; k += blockDim.x) {
-        volatile int32_t *slot = Q.ring + ((pos0 + k) & (unsigned long long)(Q.cap - 1));
-        while (*slot != 0) __nanosleep(32);
-        *slot = Q.order[a0 + k] + 1;
-    }
-}
-
-// after the visit: back to the queue when dirtied meanwhile or not converged, else clean
+// after the visit (one thread): back to the queue when dirtied meanwhile or not converged, else
+// clean -- and, patchy, the next tiles of the key order take its place
 __device__ __forceinline__ void q_finish(const QueueArgs &Q, int t, bool self_dirty)
 {
-    if (self_dirty) {
-        atomicExch(Q.state + t, 1);
-        q_enqueue(Q, t);
+    if (!self_dirty && atomicCAS(Q.state + t, 2, 0) == 2) {
+#pragma unroll 1
+        for (int k = 0; k < 4; ++k) {
+            if (q_ld(&Q.ctl->adm) >= Q.n_order || q_ld(&Q.ctl->work) > Q.target) break;
+            q_admit_one(Q);
+        }
+        q_release(Q);
         return;
     }
-    if (atomicCAS(Q.state + t, 2, 0) == 2) {
-        atomicSub(&Q.ctl->work, 1);
-        return;
-    }
-    atomicExch(Q.state + t, 1);   // 3: a neighbour changed during the visit
-    q_enqueue(Q, t);
+    atomicExch(Q.state + t, 1);   // not converged, or 3: a neighbour changed during the visit
+    q_push(Q, t);
 }
 
 template <typename real, int PATH, int CPL, int WY, int WX>
 __global__ void __launch_bounds__(NW * 32, min_blocks<PATH>()) k_sweep_queue(KP<real> A, QueueArgs Q)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ int s_t, s_a0, s_m;
-    __shared__ unsigned long long s_pos;
+    __shared__ int s_t;
     const int tid = threadIdx.x;
+#if PDD_TIMING
+    long long t_phase = clock64();
+#endif
+    // nothing seeded and nothing left to admit: no producer would ever end the wait
+    if (tid == 0 && q_ld(&Q.ctl->work) == 0 && q_ld(&Q.ctl->adm) >= Q.n_order) atomicExch(&Q.ctl->stop, 1);
     for (;;) {
-        if (tid == 0) {
-            int a0 = 0, m = 0;
-            unsigned long long pos = 0;
-            s_t = q_next(Q, &a0, &m, &pos);
-            s_a0 = a0;
-            s_m = m;
-            s_pos = pos;
-        }
+        PDD_PHASE(6);
+        if (tid == 0) s_t = q_pop(Q);
         __syncthreads();
         const int t = s_t;
-        if (t == -2) {
-            q_admit_cta(Q, s_a0, s_m, s_pos);
-            __syncthreads();
-            continue;
+        if (t < 0) {
+            PDD_PHASE(0);
+            return;
         }
-        if (t < 0) return;
         double r = 0.0, c = 0.0;
+#if PDD_TIMING
+        sweep_tile<real, PATH, CPL, WY, WX, false>(A, t, smem_raw, &r, &c, t_phase);
+#else
         sweep_tile<real, PATH, CPL, WY, WX, false>(A, t, smem_raw, &r, &c);   // ends with a barrier
-        if (tid < 9) {
-            __threadfence();   // this visit's V writes before anyone sees the dirty marks
+#endif
+        if (tid < 32) {
+            if (tid < 9 && tid != 4 && c >= Q.tol_act) {
+                __threadfence();   // this visit's V writes before anyone sees the dirty marks
+                const int tx = t % A.g.tiles_x, ty = t / A.g.tiles_x;
+                const int ax = tx + (tid % 3) - 1, ay = ty + (tid / 3) - 1;
+                if (ax >= 0 && ay >= 0 && ax < A.g.tiles_x && ay < A.g.tiles_y) {
+                    const int nb = ay * A.g.tiles_x + ax;
+                    // only admitted tiles: the others are dirty anyway and enter on admission
+                    if (Q.rank[nb] < q_ld(&Q.ctl->adm)) q_mark_dirty(Q, nb);
+                }
+            }
+            __syncwarp();          // the neighbours hold their units of work before t gives up its own
             if (tid == 4) {
                 const unsigned long long seq = atomicAdd(&Q.ctl->visits, 1ull) + 1;
                 atomicMax(&Q.ctl->max_res, (unsigned long long)__double_as_longlong(r));
@@ -968,16 +1019,9 @@ __global__ void __launch_bounds__(NW * 32, min_blocks<PATH>()) k_sweep_queue(KP<
                     for (int k = Q.lab_off[t]; k < Q.lab_off[t + 1]; ++k)
                         atomicMax(&Q.patch_round[Q.lab_ids[k]], (int32_t)seq);
                 }
-                if (seq >= Q.ctl->max_visits) atomicExch(&Q.ctl->stop, 1);
+                if (seq >= Q.ctl->max_visits) atomicExch(&Q.ctl->stop, 2);
+                else if (seq >= Q.ctl->verify_at) atomicCAS(&Q.ctl->stop, 0, 3);
                 q_finish(Q, t, r >= Q.tol);
-            } else if (c >= Q.tol_act) {
-                const int tx = t % A.g.tiles_x, ty = t / A.g.tiles_x;
-                const int ax = tx + (tid % 3) - 1, ay = ty + (tid / 3) - 1;
-                if (ax >= 0 && ay >= 0 && ax < A.g.tiles_x && ay < A.g.tiles_y) {
-                    const int nb = ay * A.g.tiles_x + ax;
-                    // only admitted tiles: the others are dirty anyway and enter on admission
-                    if (Q.rank[nb] < q_ld(&Q.ctl->adm)) q_mark_dirty(Q, nb);
-                }
             }
         }
     }
@@ -1147,6 +1191,16 @@ cudaError_t launch_sweep(const SweepLaunch &L, cudaStream_t s)
     if (L.precision == 32) return L.check ? dispatch<float, true>(L, s) : dispatch<float, false>(L, s);
     return L.check ? dispatch<double, true>(L, s) : dispatch<double, false>(L, s);
 }
+
+#if PDD_TIMING
+void dev_phases(unsigned long long *out8, bool add)
+{
+    unsigned long long h[8], z[8] = {};
+    cudaMemcpyFromSymbol(h, g_phase, sizeof h);
+    cudaMemcpyToSymbol(g_phase, z, sizeof z);
+    for (int i = 0; i < 8; ++i) out8[i] = (add ? out8[i] : 0ull) + h[i];
+}
+#endif
 
 #if PDD_WIDE_UNIT
 static_assert(TW3 == 128, "the wide unit is built with PDD_P3_WIDE=1");
@@ -1651,18 +1705,27 @@ void launch_queue_order(const TileState &T, const double *key, int n_tiles, int3
 }
 size_t queue_order_scratch_ints() { return 3 * (size_t)QNB + 1 + 4; }
 
-// (re-)seed the work queue after a verification pass: every tile whose residual is >= tol
-// (all tiles clean, admission complete): warp-aggregated reservations of work and ring slots
-__global__ void k_queue_seed(TileState T, QueueArgs Q, int n_tiles, double tol)
+// (re-)seed the work queue (ring zeroed, cursors at 0): first > 0 takes the first `first` tiles of
+// the key order (start of a patchy solve), else every tile among the first `adm` of the order
+// whose residual is >= tol (static start, or the offending tiles of a verification pass);
+// warp-aggregated reservations
+__global__ void k_queue_seed(TileState T, QueueArgs Q, int n_tiles, double tol, int first, int adm)
 {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    const bool take = t < n_tiles && T.tile_free[t] > 0 && T.tile_res[t] >= tol;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    int t = -1;
+    if (first > 0) {
+        if (i < first && i < Q.n_order) t = Q.order[i];
+    } else if (i < n_tiles && T.tile_free[i] > 0 && T.tile_res[i] >= tol && Q.rank[i] < adm) {
+        t = i;   // admitted tiles only: the others enter in key order
+    }
+    const bool take = t >= 0;
     const unsigned m = __ballot_sync(FULL, take);
     if (!m) return;
     const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
     unsigned long long pos = 0;
     if (lane == leader) {
         atomicAdd(&Q.ctl->work, __popc(m));
+        if (first > 0) atomicAdd(&Q.ctl->adm, __popc(m));
         pos = atomicAdd(&Q.ctl->tail, (unsigned long long)__popc(m));
     }
     pos = __shfl_sync(FULL, pos, leader);
@@ -1672,11 +1735,11 @@ __global__ void k_queue_seed(TileState T, QueueArgs Q, int n_tiles, double tol)
     }
 }
 
-void launch_queue_seed(const TileGeom &g, const TileState &T, const QueueArgs &Q, int n_tiles,
-                       double tol, cudaStream_t s)
+void launch_queue_seed(const TileState &T, const QueueArgs &Q, int n_tiles, double tol, int first,
+                       int adm, cudaStream_t s)
 {
-    (void)g;
-    k_queue_seed<<<(n_tiles + 255) / 256, 256, 0, s>>>(T, Q, n_tiles, tol);
+    const int m = first > 0 ? first : n_tiles;
+    k_queue_seed<<<(m + 255) / 256, 256, 0, s>>>(T, Q, n_tiles, tol, first, adm);
 }
 
 void launch_round_begin(RoundCtl *ctl, ActCounters *c, cudaStream_t s) { k_round_begin<<<1, 1, 0, s>>>(ctl, c); }
@@ -1827,3 +1890,14 @@ bool rowtab_build_device(const DProblem &P, int napad, int H, int precision, int
 #endif  // !PDD_WIDE_UNIT
 
 }  // namespace pdd
+
+#if PDD_TIMING && !PDD_WIDE_UNIT
+namespace pdd { namespace wide { void dev_phases(unsigned long long *out8, bool add); } }
+// development builds only: cycles per visit phase summed over all CTAs since the last call
+extern "C" void pdd_dev_phases(unsigned long long *out8)
+{
+    cudaDeviceSynchronize();
+    pdd::dev_phases(out8, false);
+    pdd::wide::dev_phases(out8, true);
+}
+#endif

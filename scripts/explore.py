@@ -43,3 +43,12 @@ for mode in a.modes.split(","):
                   t_sweep=round(st["seconds_sweep"], 3), t_verify=round(st["seconds_verify"], 4),
                   kern_nups=f"{nu / max(st['seconds_sweep'],1e-9):.3e}", res=st["final_residual"], kernel=st["kernel_used"],
                   tiles=st["tiles_processed"], ntiles=st["n_tiles"])), flush=True)
+            L = _native.lib()
+            if hasattr(L, "pdd_dev_phases"):      # PDD_TIMING builds: cycles per visit phase
+                import ctypes
+                ph = (ctypes.c_ulonglong * 8)()
+                L.pdd_dev_phases(ph)
+                tot = float(sum(ph)) or 1.0
+                names = ["fetch/idle", "stage-load", "convert", "sweep", "reduce", "writeback", "queue-ops", "admit"]
+                print("phases: " + ", ".join(f"{nm} {100 * v / tot:.1f}%" for nm, v in zip(names, ph)) +
+                      f"  (total {tot:.3e} CTA-cycles)", flush=True)

@@ -173,10 +173,12 @@ def test_solve_parity_random_general_fp64():
 
 @pytest.mark.parametrize("mode,schedule,policy", [
     ("patchy", "ordered", 0), ("static", "ordered", 0), ("patchy", "rounds", 1),
-    ("patchy", "rounds", 2), ("patchy", "queue", 0), ("static", "queue", 0)])
+    ("patchy", "rounds", 2), ("patchy", "queue", 0), ("static", "queue", 0),
+    ("patchy", "rounds", 0), ("static", "rounds", 0)])
 def test_schedules_reach_the_same_fixed_point(mode, schedule, policy):
-    """Every tile schedule (ordered Gauss-Seidel passes, Delta-stepping buckets, upstream-ready
-    admission) converges to the oracle's fixed point (R29)."""
+    """Every tile schedule (the work queue, ordered Gauss-Seidel passes, rounds with the moving
+    front, Delta-stepping buckets and upstream-ready admission) converges to the oracle's fixed
+    point (R29)."""
     inst = I.make_config("C5", n=513)
     ref = O.jacobi(inst, tol=_tight_tol(inst, 2e-11), max_sweeps=10**6)
     s = _solver(inst, 32)
