@@ -283,6 +283,9 @@ struct SweepLaunch {
 // offending tiles)
 void launch_queue_seed(const TileState &T, const QueueArgs &Q, int n_tiles, double tol, int first,
                        int adm, cudaStream_t s);
+// per-patch activation trace from the per-tile one (work queue: patch_round[p] = max tile_round
+// over the tiles holding nodes of p)
+void launch_patch_rounds(const TileState &T, int n_tiles, cudaStream_t s);
 // order / rank of the tiles with free nodes by key (NULL: tile index order); scratch of
 // queue_order_scratch_ints() ints
 void launch_queue_order(const TileState &T, const double *key, int n_tiles, int32_t *scratch,

@@ -1199,6 +1199,10 @@ static pdd_status queue_loop(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_st
         else if (++stalled >= 8) break;   // below the arithmetic's noise floor: give up
         CK(cudaMemsetAsync(ctx->qstate, 0, sizeof(int) * nt, s));
     }
+    if (ctx->T.n_slots > 0) {
+        launch_patch_rounds(ctx->T, nt, s);
+        ctx->launches++;
+    }
     return PDD_OK;
 }
 

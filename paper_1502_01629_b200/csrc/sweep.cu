@@ -485,16 +485,182 @@ __device__ __forceinline__ void phase_mark(int i, long long &t_prev)
 #define PDD_PHASE(i) ((void)0)
 #endif
 
+// ------------------------------------------------------------------ work-queue schedule
+// Tile states: 0 clean, 1 queued, 2 visiting, 3 visiting and dirtied meanwhile.  A queued or
+// visiting tile holds one unit of ctl->work (an admission in flight reserves one too); the queue
+// is drained for good when work reaches 0 with every tile admitted.
+// The ring is a ticket queue: a consumer takes ticket h = head++ and waits for slot h & (cap - 1)
+// to be filled; a producer takes position p = tail++ and fills slot p & (cap - 1).  No CTA ever
+// polls the cursors, each waits on its own slot (cap > tiles + resident CTAs: two outstanding
+// tickets never share a slot).
+__device__ __forceinline__ int q_ld(const int *p) { return *(volatile const int *)p; }
+
+__device__ __forceinline__ void q_push(const QueueArgs &Q, int t)
+{
+    const unsigned long long pos = atomicAdd(&Q.ctl->tail, 1ull);
+    volatile int32_t *slot = Q.ring + (pos & (unsigned long long)(Q.cap - 1));
+    while (*slot != 0) __nanosleep(32);   // the consumer of the previous lap still reads it
+    *slot = t + 1;
+}
+
+// one unit of work is gone; the last one (with every tile admitted) ends the launch
+__device__ __forceinline__ void q_release(const QueueArgs &Q)
+{
+    if (atomicSub(&Q.ctl->work, 1) == 1 && q_ld(&Q.ctl->adm) >= Q.n_order) atomicExch(&Q.ctl->stop, 1);
+}
+
+// admit the next tile of the key order (lock-free: the reservation of a unit of work comes first,
+// so work cannot reach 0 while an admission is in flight)
+__device__ __forceinline__ void q_admit_one(const QueueArgs &Q)
+{
+    atomicAdd(&Q.ctl->work, 1);
+    const int a = atomicAdd(&Q.ctl->adm, 1);
+    if (a < Q.n_order) {
+        const int t = Q.order[a];
+        if (atomicCAS(Q.state + t, 0, 1) == 0) {   // else a neighbour queued it already
+            q_push(Q, t);
+            return;
+        }
+    }
+    q_release(Q);
+}
+
+// a neighbour dirtied tile t
+__device__ __forceinline__ void q_mark_dirty(const QueueArgs &Q, int t)
+{
+    int st = q_ld(Q.state + t);
+    for (;;) {
+        if (st == 0) {
+            const int o = atomicCAS(Q.state + t, 0, 1);
+            if (o == 0) {
+                atomicAdd(&Q.ctl->work, 1);
+                q_push(Q, t);
+                return;
+            }
+            st = o;
+        } else if (st == 2) {
+            const int o = atomicCAS(Q.state + t, 2, 3);
+            if (o == 2) return;
+            st = o;
+        } else {
+            return;   // already queued, or visiting and already dirty
+        }
+    }
+}
+
+// thread 0: a consumer ticket, and the tile that arrives on it: >= 0, -1 once the queue has
+// stopped, or (block = false) -3 while the slot is still empty -- the ticket stays valid
+__device__ __forceinline__ unsigned long long q_ticket(const QueueArgs &Q)
+{
+    return atomicAdd(&Q.ctl->head, 1ull);
+}
+
+__device__ __forceinline__ int q_take(const QueueArgs &Q, unsigned long long ticket, bool block)
+{
+    volatile int32_t *slot = Q.ring + (ticket & (unsigned long long)(Q.cap - 1));
+    int v;
+    // watchdog: no visit finished anywhere for ~1 s of waiting (a visit takes ~0.1 ms) can only be
+    // a lost unit of work: stop with the non-convergence code instead of hanging the GPU
+    unsigned long long seen = *(volatile unsigned long long *)&Q.ctl->visits;
+    long long t0 = clock64();
+    for (;;) {
+        if (q_ld(&Q.ctl->stop) >= 2) return -1;   // visit cap / verification due: leave the rest queued
+        if ((v = *slot) != 0) break;
+        if (q_ld(&Q.ctl->stop)) return -1;
+        if (!block) return -3;
+        __nanosleep(200);
+        if (clock64() - t0 > (1ll << 31)) {
+            const unsigned long long now = *(volatile unsigned long long *)&Q.ctl->visits;
+            if (now == seen) atomicExch(&Q.ctl->stop, 2);
+            seen = now;
+            t0 = clock64();
+        }
+    }
+    *slot = 0;
+    const int t = v - 1;
+    atomicExch(Q.state + t, 2);   // queued -> visiting (only the consumer changes state 1)
+    __threadfence();              // acquire: the visit's loads of V come after the state change
+    return t;
+}
+
+// after the visit (one thread): back to the queue when dirtied meanwhile or not converged, else
+// clean -- and, patchy, the next tiles of the key order take its place
+__device__ __forceinline__ void q_finish(const QueueArgs &Q, int t, bool self_dirty)
+{
+    if (!self_dirty && atomicCAS(Q.state + t, 2, 0) == 2) {
+#pragma unroll 1
+        for (int k = 0; k < 4; ++k) {
+            if (q_ld(&Q.ctl->adm) >= Q.n_order || q_ld(&Q.ctl->work) > Q.target) break;
+            q_admit_one(Q);
+        }
+        q_release(Q);
+        return;
+    }
+    atomicExch(Q.state + t, 1);   // not converged, or 3: a neighbour changed during the visit
+    q_push(Q, t);
+}
+
+// ------------------------------------------------------------------ tile prefetch (work queue)
+// The work-queue kernel overlaps the staging of its NEXT tile with the end of the current visit:
+// once the sweeps are done, thread 0 takes the next tile off the queue and every thread issues
+// asynchronous 8-byte global -> shared copies (cp.async, LDGSTS in SASS) of that tile + halo of V
+// (fp64) into a staging buffer; the residual reduction, the write-back and the queue bookkeeping
+// of the current tile run meanwhile, and the next visit starts with its values already on chip.
+// Element e of the (TH + 2H) x (TW + 2H) block belongs to thread e % 256 for the copy and for the
+// read, so a thread's cp.async.wait_group is all the synchronisation the buffer needs.
+// (V rows are only 8-byte aligned -- n is odd -- so neither 16-byte cp.async nor a TMA tensor map
+// applies; ordering against other CTAs' writes of V: the consumer's acquire in q_take.)
+struct Pref {
+    double *stage;                // staging buffer, (TH + 2H)(TW + 2H) doubles
+    const QueueArgs *Q;
+    unsigned long long *ticket;   // shared: the consumer ticket taken for the next tile
+    int *next;                    // shared: next tile (>= 0), -1 queue stopped, -3 not there yet
+};
+
+template <int PATH, int WY, int WX>
+struct TileDims {
+    static constexpr int TW = PATH == 2 ? TWOf<WY, WX>::value : PATH == 3 ? TW3 : TW_GENERAL;
+    static constexpr int THt = PATH == 3 ? TH3 : TH;
+    static constexpr int MAXE = ((THt + 16) * (TW + 16) + NW * 32 - 1) / (NW * 32);   // H <= 8
+};
+
+__device__ __forceinline__ void cp_async8(double *dst_shared, const double *src_global)
+{
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst_shared);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src_global) : "memory");
+}
+
+template <typename real, int PATH, int WY, int WX>
+__device__ __forceinline__ void stage_issue(const KP<real> &A, int t, double *stage)
+{
+    constexpr int TW = TileDims<PATH, WY, WX>::TW, THt = TileDims<PATH, WY, WX>::THt;
+    constexpr int MAXE = TileDims<PATH, WY, WX>::MAXE;
+    const int H = A.g.H, n = A.P.n;
+    const int i0 = (t % A.g.tiles_x) * TW, j0 = (t / A.g.tiles_x) * THt;
+    const int W2 = TW + 2 * H, H2 = THt + 2 * H;
+#pragma unroll
+    for (int m = 0; m < MAXE; ++m) {
+        const int e = threadIdx.x + m * NW * 32;
+        if (e < H2 * W2) {
+            const int r = e / W2, c = e - r * W2;
+            const int gj = j0 - H + r, gi = i0 - H + c;
+            if (gj >= 0 && gj < n && gi >= 0 && gi < n) cp_async8(stage + e, A.V + (int64_t)gj * n + gi);
+        }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
 // ------------------------------------------------------------------ one tile visit
 // Stage tile + halo, relax k_inner times, write back.  Global V is read with ld.global.cg (L2):
-// in the ordered (persistent) schedule other CTAs update V during the launch.
-template <typename real, int PATH, int CPL, int WY, int WX, bool CHECK>
+// in the persistent schedules other CTAs update V during the launch.  PREF: the values were
+// prefetched into pf->stage (stage_issue), and the next tile is prefetched before the write-back.
+template <typename real, int PATH, int CPL, int WY, int WX, bool CHECK, bool PREF = false>
 __device__ __forceinline__ void sweep_tile(const KP<real> &A, int t, unsigned char *smem_raw,
-                                           double *res_out, double *chg_out
+                                           double *res_out, double *chg_out,
 #if PDD_TIMING
-                                           , long long &t_phase
+                                           long long &t_phase,
 #endif
-                                           )
+                                           const Pref *pf = nullptr)
 {
     PDD_PHASE(0);
     constexpr int TW = PATH == 2 ? TWOf<WY, WX>::value : PATH == 3 ? TW3 : TW_GENERAL;
@@ -517,6 +683,10 @@ __device__ __forceinline__ void sweep_tile(const KP<real> &A, int t, unsigned ch
     constexpr int MAXE = ((THt + 16) * (TW + 16) + NW * 32 - 1) / (NW * 32);   // (TH + 2H)(TW + 2H), H <= 8
     double vs[MAXE];
     double vmin = INFINITY;
+    __shared__ double s_cref;                       // PREF: the staged tile-centre value
+    const int ci = min(i0 + TW / 2, n - 1), cj = min(j0 + THt / 2, n - 1);
+    const int e_c = (cj - j0 + H) * W2 + (ci - i0 + H);
+    if constexpr (PREF) asm volatile("cp.async.wait_group 0;" ::: "memory");
 #pragma unroll
     for (int m = 0; m < MAXE; ++m) {
         const int e = threadIdx.x + m * (int)blockDim.x;
@@ -525,7 +695,12 @@ __device__ __forceinline__ void sweep_tile(const KP<real> &A, int t, unsigned ch
             const int r = e / W2, c = e - r * W2;
             const int gj = j0 - H + r, gi = i0 - H + c;
             if (gj >= 0 && gj < n && gi >= 0 && gi < n) {
-                vs[m] = __ldcg(A.V + (int64_t)gj * n + gi);
+                if constexpr (PREF) {
+                    vs[m] = pf->stage[e];           // this thread's own cp.async landed it
+                    if (e == e_c) s_cref = vs[m];
+                } else {
+                    vs[m] = __ldcg(A.V + (int64_t)gj * n + gi);
+                }
                 vmin = fmin(vmin, vs[m]);
             }
         }
@@ -548,8 +723,8 @@ __device__ __forceinline__ void sweep_tile(const KP<real> &A, int t, unsigned ch
         // problem's 1e6 start values, or values interpolated from them, next to the front, R39):
         // then the smallest staged value, so that the nodes the front has reached keep full
         // precision next to the placeholders
-        const int ci = min(i0 + TW / 2, n - 1), cj = min(j0 + THt / 2, n - 1);
-        Vref = __ldcg(A.V + (int64_t)cj * n + ci);
+        if constexpr (PREF) Vref = s_cref;          // same snapshot as the staged values
+        else Vref = __ldcg(A.V + (int64_t)cj * n + ci);
         if (PDD_BIGREF) {
             double vminb = s_red[0];
 #pragma unroll
@@ -628,7 +803,20 @@ __device__ __forceinline__ void sweep_tile(const KP<real> &A, int t, unsigned ch
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) res = rmax(res, __shfl_xor_sync(FULL, res, o));
     if (lane == 0) s_red[warp] = (double)res;
+    if constexpr (PREF) {
+        // the sweeps are done: take the next tile off the queue (if one is there already) ...
+        if (threadIdx.x == 0) {
+            *pf->ticket = q_ticket(*pf->Q);
+            *pf->next = q_take(*pf->Q, *pf->ticket, false);
+        }
+    }
     __syncthreads();
+    if constexpr (PREF) {
+        // ... and start its copies: they overlap the reduction, the write-back and the queue
+        // bookkeeping of this visit (every thread has read its staged values long ago)
+        const int tn = *pf->next;
+        if (tn >= 0) stage_issue<real, PATH, WY, WX>(A, tn, pf->stage);
+    }
     double rmaxv = 0.0;
     for (int w = 0; w < NW; ++w) rmaxv = fmax(rmaxv, s_red[w]);
     if (threadIdx.x == 0) A.tile_res[t] = rmaxv;
@@ -866,138 +1054,49 @@ __global__ void __launch_bounds__(NW * 32, min_blocks<PATH>()) k_sweep_ordered(K
     }
 }
 
-// ------------------------------------------------------------------ work-queue schedule
-// Tile states: 0 clean, 1 queued, 2 visiting, 3 visiting and dirtied meanwhile.  A queued or
-// visiting tile holds one unit of ctl->work (an admission in flight reserves one too); the queue
-// is drained for good when work reaches 0 with every tile admitted.
-// The ring is a ticket queue: a consumer takes ticket h = head++ and waits for slot h & (cap - 1)
-// to be filled; a producer takes position p = tail++ and fills slot p & (cap - 1).  No CTA ever
-// polls the cursors, each waits on its own slot (cap > tiles + resident CTAs: two outstanding
-// tickets never share a slot).
-__device__ __forceinline__ int q_ld(const int *p) { return *(volatile const int *)p; }
-
-__device__ __forceinline__ void q_push(const QueueArgs &Q, int t)
+// bytes of dynamic shared memory of a sweep CTA before the prefetch staging buffer
+template <typename real, int PATH>
+__host__ __device__ constexpr size_t sweep_smem_base(int H, int pitch, int cstride)
 {
-    const unsigned long long pos = atomicAdd(&Q.ctl->tail, 1ull);
-    volatile int32_t *slot = Q.ring + (pos & (unsigned long long)(Q.cap - 1));
-    while (*slot != 0) __nanosleep(32);   // the consumer of the previous lap still reads it
-    *slot = t + 1;
+    return NW * sizeof(double) + TH * sizeof(int) + 256 * sizeof(real) +
+           (PATH == 3 ? (size_t)4 * cstride : (size_t)(TH + 2 * H) * pitch) * sizeof(real);
 }
-
-// one unit of work is gone; the last one (with every tile admitted) ends the launch
-__device__ __forceinline__ void q_release(const QueueArgs &Q)
-{
-    if (atomicSub(&Q.ctl->work, 1) == 1 && q_ld(&Q.ctl->adm) >= Q.n_order) atomicExch(&Q.ctl->stop, 1);
-}
-
-// admit the next tile of the key order (lock-free: the reservation of a unit of work comes first,
-// so work cannot reach 0 while an admission is in flight)
-__device__ __forceinline__ void q_admit_one(const QueueArgs &Q)
-{
-    atomicAdd(&Q.ctl->work, 1);
-    const int a = atomicAdd(&Q.ctl->adm, 1);
-    if (a < Q.n_order) {
-        const int t = Q.order[a];
-        if (atomicCAS(Q.state + t, 0, 1) == 0) {   // else a neighbour queued it already
-            q_push(Q, t);
-            return;
-        }
-    }
-    q_release(Q);
-}
-
-// a neighbour dirtied tile t
-__device__ __forceinline__ void q_mark_dirty(const QueueArgs &Q, int t)
-{
-    int st = q_ld(Q.state + t);
-    for (;;) {
-        if (st == 0) {
-            const int o = atomicCAS(Q.state + t, 0, 1);
-            if (o == 0) {
-                atomicAdd(&Q.ctl->work, 1);
-                q_push(Q, t);
-                return;
-            }
-            st = o;
-        } else if (st == 2) {
-            const int o = atomicCAS(Q.state + t, 2, 3);
-            if (o == 2) return;
-            st = o;
-        } else {
-            return;   // already queued, or visiting and already dirty
-        }
-    }
-}
-
-// thread 0: wait for the next tile (>= 0), or -1 once the queue has stopped
-__device__ __forceinline__ int q_pop(const QueueArgs &Q)
-{
-    const unsigned long long h = atomicAdd(&Q.ctl->head, 1ull);
-    volatile int32_t *slot = Q.ring + (h & (unsigned long long)(Q.cap - 1));
-    int v;
-    // watchdog: no visit finished anywhere for ~1 s of waiting (a visit takes ~0.1 ms) can only be
-    // a lost unit of work: stop with the non-convergence code instead of hanging the GPU
-    unsigned long long seen = *(volatile unsigned long long *)&Q.ctl->visits;
-    long long t0 = clock64();
-    while ((v = *slot) == 0) {
-        if (q_ld(&Q.ctl->stop)) return -1;
-        __nanosleep(200);
-        if (clock64() - t0 > (1ll << 31)) {
-            const unsigned long long now = *(volatile unsigned long long *)&Q.ctl->visits;
-            if (now == seen) atomicExch(&Q.ctl->stop, 2);
-            seen = now;
-            t0 = clock64();
-        }
-    }
-    *slot = 0;
-    const int t = v - 1;
-    atomicExch(Q.state + t, 2);   // queued -> visiting (only the consumer changes state 1)
-    __threadfence();              // the visit's loads come after the state change
-    return t;
-}
-
-// after the visit (one thread): back to the queue when dirtied meanwhile or not converged, else
-// clean -- and, patchy, the next tiles of the key order take its place
-__device__ __forceinline__ void q_finish(const QueueArgs &Q, int t, bool self_dirty)
-{
-    if (!self_dirty && atomicCAS(Q.state + t, 2, 0) == 2) {
-#pragma unroll 1
-        for (int k = 0; k < 4; ++k) {
-            if (q_ld(&Q.ctl->adm) >= Q.n_order || q_ld(&Q.ctl->work) > Q.target) break;
-            q_admit_one(Q);
-        }
-        q_release(Q);
-        return;
-    }
-    atomicExch(Q.state + t, 1);   // not converged, or 3: a neighbour changed during the visit
-    q_push(Q, t);
-}
+// the 16 x 128 path-3 tile leaves no room for the staging buffer at 3 CTAs / SM (its visits do
+// several sweeps, so staging is a small share anyway): no prefetch there
+template <int PATH>
+__host__ __device__ constexpr bool queue_prefetch() { return !(PATH == 3 && TW3 == 128); }
 
 template <typename real, int PATH, int CPL, int WY, int WX>
 __global__ void __launch_bounds__(NW * 32, min_blocks<PATH>()) k_sweep_queue(KP<real> A, QueueArgs Q)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ int s_t;
+    constexpr bool PREF = queue_prefetch<PATH>();
+    __shared__ int s_t, s_next;
+    __shared__ unsigned long long s_ticket;
     const int tid = threadIdx.x;
+    Pref pf;
+    pf.stage = reinterpret_cast<double *>(
+        smem_raw + ((sweep_smem_base<real, PATH>(A.g.H, A.g.pitch, A.g.cstride) + 15) & ~(size_t)15));
+    pf.Q = &Q;
+    pf.ticket = &s_ticket;
+    pf.next = &s_next;
 #if PDD_TIMING
     long long t_phase = clock64();
 #endif
     // nothing seeded and nothing left to admit: no producer would ever end the wait
     if (tid == 0 && q_ld(&Q.ctl->work) == 0 && q_ld(&Q.ctl->adm) >= Q.n_order) atomicExch(&Q.ctl->stop, 1);
+    if (tid == 0) s_t = q_take(Q, q_ticket(Q), true);
+    __syncthreads();
+    int t = s_t;
+    if (t < 0) return;
+    if constexpr (PREF) stage_issue<real, PATH, WY, WX>(A, t, pf.stage);
     for (;;) {
-        PDD_PHASE(6);
-        if (tid == 0) s_t = q_pop(Q);
-        __syncthreads();
-        const int t = s_t;
-        if (t < 0) {
-            PDD_PHASE(0);
-            return;
-        }
         double r = 0.0, c = 0.0;
+        if (tid == 0) s_next = -3;
 #if PDD_TIMING
-        sweep_tile<real, PATH, CPL, WY, WX, false>(A, t, smem_raw, &r, &c, t_phase);
+        sweep_tile<real, PATH, CPL, WY, WX, false, PREF>(A, t, smem_raw, &r, &c, t_phase, &pf);
 #else
-        sweep_tile<real, PATH, CPL, WY, WX, false>(A, t, smem_raw, &r, &c);   // ends with a barrier
+        sweep_tile<real, PATH, CPL, WY, WX, false, PREF>(A, t, smem_raw, &r, &c, &pf);   // ends with a barrier
 #endif
         if (tid < 32) {
             if (tid < 9 && tid != 4 && c >= Q.tol_act) {
@@ -1013,17 +1112,32 @@ __global__ void __launch_bounds__(NW * 32, min_blocks<PATH>()) k_sweep_queue(KP<
             __syncwarp();          // the neighbours hold their units of work before t gives up its own
             if (tid == 4) {
                 const unsigned long long seq = atomicAdd(&Q.ctl->visits, 1ull) + 1;
-                atomicMax(&Q.ctl->max_res, (unsigned long long)__double_as_longlong(r));
-                if (Q.tile_round) {
-                    Q.tile_round[t] = (int32_t)seq;
-                    for (int k = Q.lab_off[t]; k < Q.lab_off[t + 1]; ++k)
-                        atomicMax(&Q.patch_round[Q.lab_ids[k]], (int32_t)seq);
-                }
+                if (r >= Q.tol) atomicMax(&Q.ctl->max_res, (unsigned long long)__double_as_longlong(r));
+                if (Q.tile_round) Q.tile_round[t] = (int32_t)seq;   // per-patch rounds: k_patch_rounds
                 if (seq >= Q.ctl->max_visits) atomicExch(&Q.ctl->stop, 2);
                 else if (seq >= Q.ctl->verify_at) atomicCAS(&Q.ctl->stop, 0, 3);
                 q_finish(Q, t, r >= Q.tol);
             }
         }
+        PDD_PHASE(6);
+        // the next tile: prefetched during the visit, or wait for it now
+        if (tid == 0) {
+            int tn = s_next;
+            const bool waited = tn == -3;
+            if (waited) tn = q_take(Q, PREF ? s_ticket : q_ticket(Q), true);
+            s_t = tn;
+            s_next = waited ? -3 : tn;
+        }
+        __syncthreads();
+        t = s_t;
+        if (t < 0) {
+            PDD_PHASE(0);
+            return;
+        }
+        if constexpr (PREF) {
+            if (s_next == -3) stage_issue<real, PATH, WY, WX>(A, t, pf.stage);
+        }
+        __syncthreads();           // s_next is reset at the top of the loop
     }
 }
 
@@ -1057,9 +1171,14 @@ static cudaError_t launch_one(const SweepLaunch &L, cudaStream_t s)
     A.labels = L.labels;
     A.patch_res = CHECK ? L.patch_res : nullptr;
     A.n_slots = L.n_slots;
-    const size_t smem = NW * sizeof(double) + TH * sizeof(int) + 256 * sizeof(real) +
-                        (PATH == 3 ? (size_t)4 * L.g.cstride
-                                   : (size_t)(TH + 2 * L.g.H) * L.g.pitch) * sizeof(real);
+    const size_t smem_base = sweep_smem_base<real, PATH>(L.g.H, L.g.pitch, L.g.cstride);
+    const int tw_ = PATH == 2 ? TWOf<WY, WX>::value : PATH == 3 ? TW3 : TW_GENERAL;
+    const int th_ = PATH == 3 ? TH3 : TH;
+    // the work-queue kernel adds the staging buffer of its tile prefetch
+    const size_t smem = (L.queued && !CHECK && queue_prefetch<PATH>())
+                            ? ((smem_base + 15) & ~(size_t)15) +
+                                  sizeof(double) * (size_t)(th_ + 2 * L.g.H) * (tw_ + 2 * L.g.H)
+                            : smem_base;
     if (L.ordered && !CHECK) {
         auto kern = k_sweep_ordered<real, PATH, CPL, WY, WX>;
         if (smem > 48 * 1024) {
@@ -1740,6 +1859,22 @@ void launch_queue_seed(const TileState &T, const QueueArgs &Q, int n_tiles, doub
 {
     const int m = first > 0 ? first : n_tiles;
     k_queue_seed<<<(m + 255) / 256, 256, 0, s>>>(T, Q, n_tiles, tol, first, adm);
+}
+
+// per-patch activation trace of the work-queue schedule: the last visit of any tile holding nodes
+// of the patch (the tile label CSR of k_tile_labels)
+__global__ void k_patch_rounds(const int32_t *tile_round, const int32_t *lab_off, const int16_t *lab_ids,
+                               int32_t *patch_round, int n_tiles)
+{
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n_tiles || tile_round[t] < 0) return;
+    for (int k = lab_off[t]; k < lab_off[t + 1]; ++k) atomicMax(&patch_round[lab_ids[k]], tile_round[t]);
+}
+
+void launch_patch_rounds(const TileState &T, int n_tiles, cudaStream_t s)
+{
+    k_patch_rounds<<<(n_tiles + 255) / 256, 256, 0, s>>>(T.tile_round, T.tile_lab_off, T.tile_lab_ids,
+                                                         T.patch_round, n_tiles);
 }
 
 void launch_round_begin(RoundCtl *ctl, ActCounters *c, cudaStream_t s) { k_round_begin<<<1, 1, 0, s>>>(ctl, c); }

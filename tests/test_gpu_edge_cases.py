@@ -18,7 +18,9 @@ def _solve_both(inst, precision, kernel=0, k_inner=4):
     s = Solver(inst, precision=precision)
     s.build_static(1, 1)
     if precision == 64:
-        st = s.solve("static", tol=tol_o, k_inner=k_inner, kernel=kernel)
+        # a-posteriori bound (R29): ||V - V*|| <= r / (1 - beta) = 1e-11, a tenth of the 1e-10 bar;
+        # (a residual of 1e-12 (1 - beta) is below one ulp of the values for a weak discount)
+        st = s.solve("static", tol=10.0 * tol_o, k_inner=k_inner, kernel=kernel)
         assert st["converged"] == 1
     else:
         # fp32: a single-tile grid's noise floor (~1 ulp of the tile-relative values) can sit
