@@ -1061,10 +1061,21 @@ __host__ __device__ constexpr size_t sweep_smem_base(int H, int pitch, int cstri
     return NW * sizeof(double) + TH * sizeof(int) + 256 * sizeof(real) +
            (PATH == 3 ? (size_t)4 * cstride : (size_t)(TH + 2 * H) * pitch) * sizeof(real);
 }
-// the 16 x 128 path-3 tile leaves no room for the staging buffer at 3 CTAs / SM (its visits do
-// several sweeps, so staging is a small share anyway): no prefetch there
+// Measured (profiles/r2g_prefetch_ab.txt): the prefetch pays on the general-stencil kernel (C3:
+// fine solve -5 %), whose CTAs use little shared memory; on the fp32 row-table kernel (path 3) the
+// staging buffer takes the three resident CTAs to 220 KB of the SM's 228 KB (the L1 that serves
+// the row-table and node-kind reads shrinks to the minimum) and the other two CTAs already cover
+// a CTA's staging latency: C5 +6 %, C4 +3 % slower.  So path 3 stages with plain loads
+// (PDD_PREFETCH3=1 builds the prefetch there too, for A/B runs; never on the 16 x 128 tile, where
+// three CTAs would not fit).
+#ifndef PDD_PREFETCH3
+#define PDD_PREFETCH3 0
+#endif
 template <int PATH>
-__host__ __device__ constexpr bool queue_prefetch() { return !(PATH == 3 && TW3 == 128); }
+__host__ __device__ constexpr bool queue_prefetch()
+{
+    return PATH != 3 || (PDD_PREFETCH3 != 0 && TW3 != 128);
+}
 
 template <typename real, int PATH, int CPL, int WY, int WX>
 __global__ void __launch_bounds__(NW * 32, min_blocks<PATH>()) k_sweep_queue(KP<real> A, QueueArgs Q)
