@@ -97,6 +97,11 @@ def lib():
         L.orc_fuzzy_phi.argtypes = [P, C.POINTER(C.c_uint8), C.POINTER(C.c_int32), C.c_int,
                                     C.c_double, C.c_int64, dp, dp]
         L.orc_fuzzy_phi.restype = C.c_int64
+        L.orc_fuzzy_sparse.argtypes = [P, C.POINTER(C.c_uint8), C.POINTER(C.c_int32), C.c_int, C.c_int,
+                                       C.c_double, C.c_int64, C.POINTER(C.c_int16), dp, dp]
+        L.orc_fuzzy_sparse.restype = C.c_int64
+        L.orc_fuzzy_sparse_assign.argtypes = [P, C.POINTER(C.c_int16), dp, C.c_int, C.c_int, C.c_double,
+                                              C.POINTER(C.c_int16), C.POINTER(C.c_uint8)]
         L.orc_fuzzy_assign.argtypes = [P, dp, C.c_int, C.c_double, C.POINTER(C.c_int16),
                                        C.POINTER(C.c_uint8)]
         _lib = L
@@ -383,3 +388,27 @@ def fuzzy_assign(inst, phi: np.ndarray, tau_P: float):
     lib().orc_fuzzy_assign(P.ref, _ptr(phi.reshape(-1), C.c_double), int(npatch), float(tau_P),
                            _ptr(lab, C.c_int16), _ptr(mem, C.c_uint8))
     return lab, mem
+
+
+def fuzzy_sparse(inst, astar: np.ndarray, n_patches: int, K: int, eps_P: float, tau_P: float = 0.5,
+                 max_sweeps: int = 10**6):
+    """Sparse top-K form of the fuzzy patches (per node the K largest (patch, phi_p) pairs; reading
+    R40).  Returns dict(lab (N, K) int16, mass (N, K), sweeps, residual, labels, members)."""
+    P = Problem(inst)
+    N = inst.n * inst.n
+    a = np.ascontiguousarray(astar, dtype=np.uint8)
+    sec = np.ascontiguousarray(inst.sector, dtype=np.int32)
+    lab = np.empty(N * K, dtype=np.int16)
+    mass = np.empty(N * K, dtype=np.float64)
+    res = C.c_double(0.0)
+    sw = lib().orc_fuzzy_sparse(P.ref, _ptr(a, C.c_uint8), _ptr(sec, C.c_int32), int(n_patches), int(K),
+                                float(eps_P), int(max_sweeps), _ptr(lab, C.c_int16),
+                                _ptr(mass, C.c_double), C.byref(res))
+    if sw < 0:
+        raise ValueError("K must be in 1..16")
+    own = np.empty(N, dtype=np.int16)
+    mem = np.empty(N, dtype=np.uint8)
+    lib().orc_fuzzy_sparse_assign(P.ref, _ptr(lab, C.c_int16), _ptr(mass, C.c_double), int(K),
+                                  int(n_patches), float(tau_P), _ptr(own, C.c_int16), _ptr(mem, C.c_uint8))
+    return {"lab": lab.reshape(N, K), "mass": mass.reshape(N, K), "sweeps": int(sw),
+            "residual": res.value, "labels": own, "members": mem}

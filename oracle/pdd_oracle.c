@@ -672,3 +672,139 @@ void orc_fuzzy_assign(const orc_problem *P, const double *phi, int n_patches, do
         if (members) members[k] = (uint8_t)(cnt > 255 ? 255 : cnt);
     }
 }
+
+/* Sparse form of the fuzzy patches ("per-node top-K (label, mass)"; the
+ * paper's construction P:777-803 with hundreds of patches, reading R40).  Every node keeps at most
+ * K pairs (p, phi_p): the K largest phi_p of the node (ties: lower p first), stored in that order;
+ * a patch that is not listed has phi_p = 0 there.  One Jacobi sweep of the same advection scheme
+ *     phi_p(x_i) = w00 phi_p(c00) + w10 phi_p(c10) + w01 phi_p(c01) + w11 phi_p(c11)
+ * merges the lists of the four corners IN THE ORDER 00, 10, 01, 11 (a label's partial sums are
+ * added in corner order, exactly the dense expression with its zero terms left out), drops the
+ * labels whose sum is 0 and keeps the K largest.  With K >= the number of patches that reach a
+ * node this IS the dense iteration (same bits); a smaller K truncates the smallest memberships
+ * (the dropped mass is reported by orc_fuzzy_sparse_assign).  The sweep change is the largest
+ * |new phi_p - old phi_p| over the labels listed before or after; iteration stops at the first
+ * sweep with change < eps_P.  lab / mass: N * K (node-major; empty slot: label -1, mass 0). */
+static void sparse_insert_topk(int K, int16_t *ol, double *om, int *cnt, int16_t l, double m)
+{
+    /* insertion into a list sorted by (mass descending, label ascending), capacity K */
+    int pos = *cnt;
+    while (pos > 0 && (om[pos - 1] < m || (om[pos - 1] == m && ol[pos - 1] > l))) --pos;
+    if (pos >= K) return;
+    const int last = *cnt < K ? *cnt : K - 1;
+    for (int s = last; s > pos; --s) { ol[s] = ol[s - 1]; om[s] = om[s - 1]; }
+    ol[pos] = l;
+    om[pos] = m;
+    if (*cnt < K) ++*cnt;
+}
+
+int64_t orc_fuzzy_sparse(const orc_problem *P, const uint8_t *astar, const int32_t *sector,
+                         int n_patches, int K, double eps_P, int64_t max_sweeps, int16_t *lab,
+                         double *mass, double *residual_out)
+{
+    const int n = P->n;
+    const int64_t N = (int64_t)n * n;
+    const double q = P->h / P->dx;
+    if (K < 1 || K > 16) return -1;
+    int16_t *clab = lab, *nlab = (int16_t *)malloc(sizeof(int16_t) * (size_t)N * K);
+    double *cm = mass, *nm = (double *)malloc(sizeof(double) * (size_t)N * K);
+    for (int64_t k = 0; k < N; ++k)
+        for (int s = 0; s < K; ++s) {
+            const int on = s == 0 && P->kind[k] == 1 && sector[k] >= 0 && sector[k] < n_patches;
+            clab[k * K + s] = on ? (int16_t)sector[k] : (int16_t)-1;
+            cm[k * K + s] = on ? 1.0 : 0.0;
+        }
+    int64_t sw = 0;
+    double res = INFINITY;
+    while (sw < max_sweeps) {
+        res = 0.0;
+#pragma omp parallel for schedule(static) reduction(max : res)
+        for (int j = 0; j < n; ++j)
+            for (int i = 0; i < n; ++i) {
+                const int64_t k = (int64_t)j * n + i;
+                if (P->kind[k] != 0) {
+                    for (int s = 0; s < K; ++s) { nlab[k * K + s] = clab[k * K + s]; nm[k * K + s] = cm[k * K + s]; }
+                    continue;
+                }
+                const int a = astar[k];
+                const double c = coef_at(&P->speed, i, j, n);
+                const double f1 = c * P->ctrl[2 * a] + coef_at(&P->drift[0], i, j, n);
+                const double f2 = c * P->ctrl[2 * a + 1] + coef_at(&P->drift[1], i, j, n);
+                int64_t cr[4];
+                double wg[4];
+                bilinear_stencil(n, (double)i + q * f1, (double)j + q * f2, cr, wg);
+                int16_t al[64];
+                double am[64];
+                int na = 0;
+                for (int t = 0; t < 4; ++t)            /* corner order 00, 10, 01, 11 */
+                    for (int s = 0; s < K; ++s) {
+                        const int16_t l = clab[cr[t] * K + s];
+                        if (l < 0) continue;
+                        const double term = wg[t] * cm[cr[t] * K + s];
+                        int idx = 0;
+                        while (idx < na && al[idx] != l) ++idx;
+                        if (idx < na) am[idx] = am[idx] + term;
+                        else { al[na] = l; am[na] = term; ++na; }
+                    }
+                int16_t ol[16];
+                double om[16];
+                int cnt = 0;
+                for (int idx = 0; idx < na; ++idx)
+                    if (am[idx] > 0.0) sparse_insert_topk(K, ol, om, &cnt, al[idx], am[idx]);
+                /* change of the sweep over the labels listed before or after */
+                for (int s = 0; s < cnt; ++s) {
+                    double old = 0.0;
+                    for (int u = 0; u < K; ++u)
+                        if (clab[k * K + u] == ol[s]) old = cm[k * K + u];
+                    const double d = fabs(om[s] - old);
+                    if (d > res) res = d;
+                }
+                for (int u = 0; u < K; ++u) {
+                    const int16_t l = clab[k * K + u];
+                    if (l < 0) continue;
+                    int found = 0;
+                    for (int s = 0; s < cnt; ++s) found |= ol[s] == l;
+                    if (!found && cm[k * K + u] > res) res = cm[k * K + u];
+                }
+                for (int s = 0; s < K; ++s) {
+                    nlab[k * K + s] = s < cnt ? ol[s] : (int16_t)-1;
+                    nm[k * K + s] = s < cnt ? om[s] : 0.0;
+                }
+            }
+        { int16_t *t = clab; clab = nlab; nlab = t; }
+        { double *t = cm; cm = nm; nm = t; }
+        ++sw;
+        if (res < eps_P) break;
+    }
+    if (clab != lab) {
+        memcpy(lab, clab, sizeof(int16_t) * (size_t)N * K);
+        memcpy(mass, cm, sizeof(double) * (size_t)N * K);
+        nlab = clab;
+        nm = cm;
+    }
+    free(nlab);
+    free(nm);
+    if (residual_out) *residual_out = res;
+    return sw;
+}
+
+/* Ownership from the sparse lists (same rule as orc_fuzzy_assign): owner = the first listed patch
+ * (largest phi_p, lowest p on ties), orphan n_patches when the list is empty; members = listed
+ * patches with phi_p >= tau_P. */
+void orc_fuzzy_sparse_assign(const orc_problem *P, const int16_t *lab, const double *mass, int K,
+                             int n_patches, double tau_P, int16_t *labels, uint8_t *members)
+{
+    const int64_t N = (int64_t)P->n * P->n;
+    for (int64_t k = 0; k < N; ++k) {
+        if (P->kind[k] != 0) {
+            labels[k] = P->kind[k] == 1 ? -1 : -2;
+            if (members) members[k] = 0;
+            continue;
+        }
+        int cnt = 0;
+        for (int s = 0; s < K; ++s)
+            if (lab[k * K + s] >= 0 && mass[k * K + s] >= tau_P) ++cnt;
+        labels[k] = (int16_t)(lab[k * K] >= 0 ? lab[k * K] : n_patches);
+        if (members) members[k] = (uint8_t)cnt;
+    }
+}

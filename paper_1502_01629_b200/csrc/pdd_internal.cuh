@@ -254,7 +254,8 @@ struct SweepLaunch {
     const void *rowtab;      // RowEntry array [n][na_pad]
     int na_pad;
     int Hx;                  // nodes with i < Hx or i > n-1-Hx use the general stencil
-    int path;                // 1 general, 2 row-table, 3 row-table fp32 G=4
+    int path;                // 1 general, 2 row-table, 3 row-table fp32 G=4, 4 lean general
+                             // (WY = branches, WX = 1: drift planes staged)
     int WY, WX;              // row-table window
     int check;               // 1: pure Jacobi residual, no update
     int precision;           // 32 | 64
@@ -320,6 +321,7 @@ int sweep_tile_rows();
 // compile-time shared-memory geometry of the path-3 kernel (rows pitch, copy stride, max halo)
 void p3_geometry(int &pitch, int &cstride, int &hmax);
 void p3_tile(int &tw, int &th);   // path-3 tile columns / rows
+void gf_geometry(int &pitch);      // compile-time shared-memory pitch of path 4 (sweep_gf.cuh)
 // the 16 x 128 path-3 tile (sweep.cu built with PDD_WIDE_UNIT=1)
 cudaError_t launch_sweep_wide(const SweepLaunch &L, cudaStream_t s);
 void p3_geometry_wide(int &pitch, int &cstride, int &hmax);

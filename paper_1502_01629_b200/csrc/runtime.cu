@@ -145,6 +145,7 @@ struct pdd_ctx {
     TileState T{};
     int max_tiles = 0;
     // work-queue schedule (schedule 2)
+    bool prepared_queue_ok = false;
     QueueCtl *qctl = nullptr;
     int32_t *qring = nullptr;
     unsigned qcap = 0;
@@ -837,11 +838,26 @@ static bool p3_use_wide(const pdd_problem *p, bool patchy, int force_cols)
     return !patchy && 128.0 * dx <= 0.125 + 1e-12;
 }
 
-static pdd_status prepare(pdd_ctx *ctx, int kernel_req, bool patchy)
+// The lean general-stencil kernel (path 4, sweep_gf.cuh) covers f = c(x) a + d(x) with any speed /
+// drift coefficients, row-uniform sigma and cost, lambda > 0 and 2 or 4 branches.
+static bool fast_general_ok(const pdd_problem *p)
+{
+    auto row_ok = [](const pdd_coef &c) { return c.kind == PDD_COEF_CONST || c.kind == PDD_COEF_ROW; };
+    if (!(p->lambda > 0.0) || p->sigma_mode != 0 || (p->p != 1 && p->p != 2) || !row_ok(p->cost)) return false;
+    for (int k = 0; k < p->p; ++k)
+        for (int c = 0; c < 2; ++c)
+            if (!row_ok(p->sigma[k][c])) return false;
+    return p->n_controls <= 128;
+}
+
+// queue_ok: the launch is a work-queue solve or a check pass (the only forms path 4 is built in)
+static pdd_status prepare(pdd_ctx *ctx, int kernel_req, bool patchy, bool queue_ok)
 {
     const pdd_problem *p = &ctx->fine;   // sizes only: its host arrays are gone (pdd_create)
     const bool want_wide = p3_use_wide(p, patchy, ctx->force_tile_cols);
-    if (ctx->prepared_kernel == kernel_req && ctx->prepared_wide == want_wide) return PDD_OK;
+    if (ctx->prepared_kernel == kernel_req && ctx->prepared_wide == want_wide &&
+        ctx->prepared_queue_ok == queue_ok)
+        return PDD_OK;
     const DProblem &d = ctx->F.d;
     const int H = ctx->fine_halo;
     if (H > 8) return fail(ctx, PDD_E_STENCIL, "foot points reach %.2f cells; tile halo limited to 8",
@@ -849,7 +865,7 @@ static pdd_status prepare(pdd_ctx *ctx, int kernel_req, bool patchy)
     int WY = 0, WX = 0, oxmin = 0, oxmax = 0;
     int path = 1;
     const int napad = na_pad_of(p->n_controls);
-    if (kernel_req != 1 && napad && ctx->fine_row_uniform_all) {
+    if (kernel_req != 1 && kernel_req != 4 && napad && ctx->fine_row_uniform_all) {
         // the compact row stencils are built on the device (k_rowtab_extent / k_rowtab_fill)
         if (rowtab_build_device(d, napad, H, ctx->precision, ctx->dev_int + 2, ctx->rowtab,
                                 ctx->rowtab_bytes, WY, WX, oxmin, oxmax, ctx->stream) &&
@@ -865,6 +881,18 @@ static pdd_status prepare(pdd_ctx *ctx, int kernel_req, bool patchy)
     p3_geometry(p3_pitch, p3_cstride, p3_hmax);
     const bool g4 = path == 2 && ctx->precision == 32 && kernel_req != 3 && H <= p3_hmax;
     ctx->path = g4 ? 3 : path;
+    // general stencil: the lean kernel where it applies (kernel 4 insists on it, kernel 1 on the
+    // fully general one)
+    const bool fast = path == 1 && kernel_req != 1 && queue_ok && fast_general_ok(p);
+    if (kernel_req == 4 && !fast)
+        return fail(ctx, PDD_E_INVALID, "kernel 4 needs the work-queue schedule and a problem with row-uniform "
+                                        "sigma and cost, lambda > 0, p = 1 or 2");
+    if (fast) {
+        auto xvar = [](const pdd_coef &c) { return c.kind == PDD_COEF_COL || c.kind == PDD_COEF_FIELD; };
+        ctx->path = 4;
+        WY = 2 * p->p;                                            // branches
+        WX = (xvar(p->drift[0]) || xvar(p->drift[1])) ? 1 : 0;    // drift planes staged
+    }
     ctx->WY = WY;
     ctx->WX = WX;
     ctx->Hx = H;
@@ -891,6 +919,11 @@ static pdd_status prepare(pdd_ctx *ctx, int kernel_req, bool patchy)
         g.cstride = p3_cstride;
         if (pitch < g.TW + 2 * H || p3_cstride < (g.TH + 2 * H) * pitch + 4)
             return fail(ctx, PDD_E_STENCIL, "path-3 shared-memory geometry too small for halo %d", H);
+    } else if (fast) {
+        int gp = 0;
+        gf_geometry(gp);
+        pitch = gp;                                               // compile-time pitch of path 4
+        g.cstride = (1 + 2 * WX) * g.TH * g.TW;                   // reals of the coefficient planes
     } else {
         while (pitch % banks != mod % banks) ++pitch;
         g.cstride = 0;
@@ -904,6 +937,7 @@ static pdd_status prepare(pdd_ctx *ctx, int kernel_req, bool patchy)
     CK(cudaMemcpy(ctx->T.all_list, all.data(), sizeof(int32_t) * all.size(), cudaMemcpyHostToDevice));
     ctx->prepared_kernel = kernel_req;
     ctx->prepared_wide = want_wide;
+    ctx->prepared_queue_ok = queue_ok;
     return PDD_OK;
 }
 
@@ -1116,8 +1150,13 @@ static pdd_status queue_loop(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_st
     Q.rank = ctx->qrank;
     Q.n_order = tiles_free;
     // patchy: about two waves of resident CTAs queued or visiting at any time (A/B: PDD_QW)
+    // (measured, profiles/r2e_queue_scan.txt, r2j_c3_target.txt: C5 / C4 want 2 - 3 waves -- fewer
+    // and tiles are revisited before their upstream neighbours moved -- but never more than about a
+    // fifth of the grid's tiles: C3's 2145 tiles against 592 resident CTAs want 0.75 waves)
     const char *qe = dev_env("PDD_QW");
-    Q.target = o->queue_target > 0 ? o->queue_target : std::max(1, (int)((qe ? std::atof(qe) : 2.0) * resident));
+    const int auto_target = std::min(2 * resident, std::max(tiles_free / 5, resident / 2));
+    Q.target = o->queue_target > 0 ? o->queue_target
+                                   : std::max(1, qe ? (int)(std::atof(qe) * resident) : auto_target);
     Q.state = ctx->qstate;
     Q.tol = o->tol;
     const char *te = dev_env("PDD_TACT");   // A/B: neighbour-change activation threshold / tol
@@ -1222,7 +1261,8 @@ pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
         return fail(ctx, PDD_E_STATE, "patchy solve needs pdd_synthesize and pdd_build_patches");
     if (o->mode == 1 && ctx->labels_mode != 2)
         return fail(ctx, PDD_E_STATE, "static solve needs pdd_build_static");
-    pdd_status ps = prepare(ctx, o->kernel, o->mode == 0);
+    if (o->kernel < 0 || o->kernel > 4) return fail(ctx, PDD_E_INVALID, "kernel must be 0..4");
+    pdd_status ps = prepare(ctx, o->kernel, o->mode == 0, (o->schedule == 0 ? 2 : o->schedule) == 2);
     if (ps != PDD_OK) return ps;
     cudaStream_t s = ctx->stream;
     const DProblem &d = ctx->F.d;
@@ -1264,6 +1304,8 @@ pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
         SweepLaunch Q = make_launch(ctx, nullptr, 0, 1, 0, nullptr);
         int per_sm = 1;
         Q.occupancy_out = &per_sm;
+        Q.queued = sched == 2 ? 1 : 0;   // the kernel that will run (the queue kernel's prefetch
+                                         // buffer can lower its occupancy)
         CK(launch_sweep(Q, s));
         resident *= std::max(1, per_sm);
     }
@@ -1285,7 +1327,7 @@ pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
     // 800^2: 49.7 vs 117 sweep-equivalents -- the row-table kernels 1: C2 10 ms vs 16 ms,
     // eikonal 800^2 16 ms vs 34 ms)
     const int k_inner = o->k_inner > 0 ? o->k_inner
-                        : (o->mode == 1 ? 4 : (one_wave && ctx->path == 1 ? 4 : 1));
+                        : (o->mode == 1 ? 4 : (one_wave && (ctx->path == 1 || ctx->path == 4) ? 4 : 1));
     if (o->mode == 0 && o->delta == 0.0 && one_wave && o->bucket_policy != 2) {
         delta = -1.0;
         thr = INFINITY;
@@ -1470,8 +1512,8 @@ pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
 pdd_status pdd_apply_operator(pdd_ctx *ctx, double *out, int32_t kernel, double *residual)
 {
     if (!ctx) return fail(nullptr, PDD_E_INVALID, "ctx is NULL");
-    if (kernel < 0 || kernel > 3) return fail(ctx, PDD_E_INVALID, "kernel must be 0..3");
-    pdd_status ps = prepare(ctx, kernel, false);
+    if (kernel < 0 || kernel > 4) return fail(ctx, PDD_E_INVALID, "kernel must be 0..4");
+    pdd_status ps = prepare(ctx, kernel, false, true);
     if (ps != PDD_OK) return ps;
     cudaStream_t s = ctx->stream;
     const size_t N = (size_t)ctx->fine.n * ctx->fine.n;

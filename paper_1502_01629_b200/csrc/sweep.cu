@@ -59,11 +59,14 @@ namespace wide {
 #define PDD_MIN_BLOCKS1 2   // path 1 (general stencil) CTAs per SM bound (measured: C3 patchy
                             // 0.124 -> 0.106 s, static 0.29 -> 0.22 s against 1 CTA/SM)
 #endif
+#ifndef PDD_MIN_BLOCKS4
+#define PDD_MIN_BLOCKS4 4   // path 4 (lean general stencil): 64 registers at 8 warps, 32 warps / SM
+#endif
 #ifndef PDD_MIN_BLOCKS3
 #define PDD_MIN_BLOCKS3 3   // path 3 (row-table GS) CTAs per SM bound: 80 registers at 8 warps
 #endif
 template <int PATH>
-constexpr int min_blocks() { return PDD_MIN_BLOCKS > 0 ? PDD_MIN_BLOCKS : (PATH == 3 ? PDD_MIN_BLOCKS3 : PATH == 1 ? PDD_MIN_BLOCKS1 : 1); }
+constexpr int min_blocks() { return PDD_MIN_BLOCKS > 0 ? PDD_MIN_BLOCKS : (PATH == 3 ? PDD_MIN_BLOCKS3 : PATH == 1 ? PDD_MIN_BLOCKS1 : PATH == 4 ? PDD_MIN_BLOCKS4 : 1); }
 #ifndef PDD_TH
 #define PDD_TH 32           // tile rows (multiple of NW)
 #endif
@@ -76,8 +79,11 @@ constexpr int RPW = TH / NW;    // rows per warp
 constexpr int TW_GENERAL = 64;
 constexpr unsigned FULL = 0xffffffffu;
 
+// path 4 in fp64 needs twice the registers: 2 CTAs / SM
+template <typename real, int PATH>
+constexpr int min_blocks_r() { return (PATH == 4 && sizeof(real) == 8) ? 2 : min_blocks<PATH>(); }
 template <int WY, int WX>
-struct TWOf { static constexpr int value = WX * (64 / WX); };   // multiple of WX, <= 64
+struct TWOf { static constexpr int value = WX > 0 ? WX * (64 / (WX > 0 ? WX : 1)) : 64; };   // multiple of WX, <= 64
 
 int rowtab_tw(int WY, int WX) { (void)WY; return WX * (64 / WX); }
 void p3_geometry(int &pitch, int &cstride, int &hmax);
@@ -461,6 +467,7 @@ __device__ __forceinline__ void row_table(const KP<real> &A, real *s_u, const re
 #define PDD_GSG 1    // path 1 (general stencil) uses the Gauss-Seidel tile sweeps of sweep_gs.cuh
 #endif
 #include "sweep_gs.cuh"
+#include "sweep_gf.cuh"
 
 constexpr bool kRawMinRef = PDD_RAWMIN != 0;   // fp32 path 3: V_ref = staged min (sweep_gs.cuh)
 
@@ -746,7 +753,25 @@ __device__ __forceinline__ void sweep_tile(const KP<real> &A, int t, unsigned ch
             for (int q = 0; q < NCOPY; ++q) s_u[q * A.g.cstride + q + r * pitch + c] = v;
         }
     }
-    for (int e = threadIdx.x; e < 2 * A.P.na; e += blockDim.x) s_ctrl[e] = (real)A.P.ctrl[e];
+    if constexpr (PATH == 4) {
+        // q a_k, h m(a_k) and the tile's x-varying coefficient planes: c, then q d1, q d2 (WX)
+        real *s_cf = s_u + (TH + 2 * H) * GF_PITCH;
+        real *s_hm = s_cf + A.g.cstride;
+        for (int e = threadIdx.x; e < 2 * A.P.na; e += blockDim.x) s_ctrl[e] = (real)(A.P.q * A.P.ctrl[e]);
+        for (int e = threadIdx.x; e < A.P.na; e += blockDim.x)
+            s_hm[e] = A.P.cost_ctrl ? (real)(A.P.h * A.P.cost_ctrl[e]) : (real)0;
+        for (int e = threadIdx.x; e < TH * TW; e += blockDim.x) {
+            const int ly = e / TW, lx = e - ly * TW;
+            const int gi = min(i0 + lx, n - 1), gj = min(j0 + ly, n - 1);
+            s_cf[e] = (real)coef_at(A.P.speed, gi, gj, n);
+            if constexpr (WX != 0) {
+                s_cf[TH * TW + e] = (real)(A.P.q * coef_at(A.P.drift[0], gi, gj, n));
+                s_cf[2 * TH * TW + e] = (real)(A.P.q * coef_at(A.P.drift[1], gi, gj, n));
+            }
+        }
+    } else {
+        for (int e = threadIdx.x; e < 2 * A.P.na; e += blockDim.x) s_ctrl[e] = (real)A.P.ctrl[e];
+    }
     if (threadIdx.x < THt) s_prog[threadIdx.x] = 0;
     if constexpr (CHECK) {
         if (A.patch_res)
@@ -773,6 +798,16 @@ __device__ __forceinline__ void sweep_tile(const KP<real> &A, int t, unsigned ch
         done_sweeps = tile_gs4<CPL, WY, WX, CHECK>(A, s_u, s_ctrl, s_prog, s_red, pitch,
                                                    A.g.cstride, H, i0, j0, D, kin, res, Vref, ot & 3,
                                                    sbase, edge4);
+    } else if constexpr (PATH == 4) {
+        // lean general stencil (sweep_gf.cuh): CPL unused, WY = branches NB, WX = 1 when the drift
+        // varies along x; coefficient planes behind the V tile, h m(a) behind them
+        const real *s_cf = s_u + (TH + 2 * H) * GF_PITCH;
+        const real *s_hm = s_cf + A.g.cstride;
+        const int ot = A.tile_orient ? A.tile_orient[t] : 0;
+        const int kin = (ot & 4) ? min(A.k_inner, A.k_coherent) : A.k_inner;
+        const int sbase = (A.tile_sweeps && !(ot & 4)) ? A.tile_sweeps[t] : 0;
+        done_sweeps = tile_gsf<real, WY, WX != 0, CHECK>(A, s_u, s_ctrl, s_hm, s_cf, s_prog, s_red, H, i0,
+                                                        j0, kin, res, Vref, ot & 3, sbase);
     } else if constexpr (PATH == 1 && PDD_GSG) {
         const int ot = A.tile_orient ? A.tile_orient[t] : 0;
         const int kin = (ot & 4) ? min(A.k_inner, A.k_coherent) : A.k_inner;
@@ -898,7 +933,7 @@ __device__ __forceinline__ void sweep_tile(const KP<real> &A, int t, unsigned ch
 
 // Round schedule: one CTA per listed tile (chaotic relaxation across the tiles of a launch).
 template <typename real, int PATH, int CPL, int WY, int WX, bool CHECK>
-__global__ void __launch_bounds__(NW * 32, min_blocks<PATH>()) k_sweep(KP<real> A)
+__global__ void __launch_bounds__(NW * 32, min_blocks_r<real, PATH>()) k_sweep(KP<real> A)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     #if PDD_TIMING
@@ -912,7 +947,7 @@ __global__ void __launch_bounds__(NW * 32, min_blocks<PATH>()) k_sweep(KP<real> 
 // Device-driven round: persistent CTAs take the activated tiles one at a time (dynamic fetch),
 // the count is the activation's -- no host round trip between activation and sweep.
 template <typename real, int PATH, int CPL, int WY, int WX>
-__global__ void __launch_bounds__(NW * 32, min_blocks<PATH>()) k_sweep_dyn(KP<real> A)
+__global__ void __launch_bounds__(NW * 32, min_blocks_r<real, PATH>()) k_sweep_dyn(KP<real> A)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ int s_t;
@@ -988,7 +1023,7 @@ __global__ void __launch_bounds__(NW * 32, min_blocks<PATH>()) k_sweep_dyn(KP<re
 // A tile is skipped (but still marked done) when its last residual is < tol and no neighbour
 // changed by >= tol after its last visit (visit stamps).
 template <typename real, int PATH, int CPL, int WY, int WX>
-__global__ void __launch_bounds__(NW * 32, min_blocks<PATH>()) k_sweep_ordered(KP<real> A, OrderArgs O)
+__global__ void __launch_bounds__(NW * 32, min_blocks_r<real, PATH>()) k_sweep_ordered(KP<real> A, OrderArgs O)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ int s_idx;
@@ -1058,8 +1093,10 @@ __global__ void __launch_bounds__(NW * 32, min_blocks<PATH>()) k_sweep_ordered(K
 template <typename real, int PATH>
 __host__ __device__ constexpr size_t sweep_smem_base(int H, int pitch, int cstride)
 {
+    // path 4: cstride carries the size of the coefficient planes, 128 reals of h m(a) follow
     return NW * sizeof(double) + TH * sizeof(int) + 256 * sizeof(real) +
-           (PATH == 3 ? (size_t)4 * cstride : (size_t)(TH + 2 * H) * pitch) * sizeof(real);
+           (PATH == 3 ? (size_t)4 * cstride
+                      : (size_t)(TH + 2 * H) * pitch + (PATH == 4 ? (size_t)cstride + 128 : 0)) * sizeof(real);
 }
 // Measured (profiles/r2g_prefetch_ab.txt): the prefetch pays on the general-stencil kernel (C3:
 // fine solve -5 %), whose CTAs use little shared memory; on the fp32 row-table kernel (path 3) the
@@ -1078,7 +1115,7 @@ __host__ __device__ constexpr bool queue_prefetch()
 }
 
 template <typename real, int PATH, int CPL, int WY, int WX>
-__global__ void __launch_bounds__(NW * 32, min_blocks<PATH>()) k_sweep_queue(KP<real> A, QueueArgs Q)
+__global__ void __launch_bounds__(NW * 32, min_blocks_r<real, PATH>()) k_sweep_queue(KP<real> A, QueueArgs Q)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr bool PREF = queue_prefetch<PATH>();
@@ -1190,7 +1227,11 @@ static cudaError_t launch_one(const SweepLaunch &L, cudaStream_t s)
                             ? ((smem_base + 15) & ~(size_t)15) +
                                   sizeof(double) * (size_t)(th_ + 2 * L.g.H) * (tw_ + 2 * L.g.H)
                             : smem_base;
-    if (L.ordered && !CHECK) {
+    // path 4 is built for the work queue and for check launches only
+    if constexpr (PATH == 4 && !CHECK) {
+        if (!L.queued) return cudaErrorInvalidValue;
+    }
+    if constexpr (PATH != 4) if (L.ordered && !CHECK) {
         auto kern = k_sweep_ordered<real, PATH, CPL, WY, WX>;
         if (smem > 48 * 1024) {
             cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1219,13 +1260,17 @@ static cudaError_t launch_one(const SweepLaunch &L, cudaStream_t s)
         int per_sm = 0, dev = 0, sms = 148;
         cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NW * 32, smem);
         if (e != cudaSuccess) return e;
+        if (L.occupancy_out) {
+            *L.occupancy_out = std::max(1, per_sm);
+            return cudaSuccess;
+        }
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         // every CTA must be resident at once: idle CTAs spin on the queue
         kern<<<std::max(1, per_sm) * sms, NW * 32, smem, s>>>(A, L.queue);
         return cudaGetLastError();
     }
-    if ((L.ctl || L.occupancy_out) && !CHECK) {
+    if constexpr (PATH != 4) if ((L.ctl || L.occupancy_out) && !CHECK) {
         auto kern = k_sweep_dyn<real, PATH, CPL, WY, WX>;
         // occupancy and the shared-memory attribute are per device: cached per device ordinal
         constexpr int kMaxDev = 64;
@@ -1258,21 +1303,32 @@ static cudaError_t launch_one(const SweepLaunch &L, cudaStream_t s)
         kern<<<grid, NW * 32, smem, s>>>(A);
         return cudaGetLastError();
     }
-    auto kern = k_sweep<real, PATH, CPL, WY, WX, CHECK>;
-    if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
-        if (e != cudaSuccess) return e;
+    if constexpr (PATH != 4 || CHECK) {
+        auto kern = k_sweep<real, PATH, CPL, WY, WX, CHECK>;
+        if (smem > 48 * 1024) {
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)smem);
+            if (e != cudaSuccess) return e;
+        }
+        if (L.n_list <= 0) return cudaSuccess;
+        kern<<<L.n_list, NW * 32, smem, s>>>(A);
+        return cudaGetLastError();
     }
-    if (L.n_list <= 0) return cudaSuccess;
-    kern<<<L.n_list, NW * 32, smem, s>>>(A);
-    return cudaGetLastError();
+    return cudaErrorInvalidValue;
 }
 
 template <typename real, bool CHECK>
 static cudaError_t dispatch(const SweepLaunch &L, cudaStream_t s)
 {
     if (L.path == 1) return launch_one<real, 1, 1, 1, 1, CHECK>(L, s);
+    if (L.path == 4) {
+        // lean general stencil: WY = branches (2 or 4), WX = drift varies along x; only the
+        // work queue and check launches are built for it (runtime.cu prepare())
+        if (L.ordered || (L.ctl && !CHECK)) return cudaErrorInvalidValue;
+        if (L.WY == 2) return L.WX ? launch_one<real, 4, 1, 2, 1, CHECK>(L, s) : launch_one<real, 4, 1, 2, 0, CHECK>(L, s);
+        if (L.WY == 4) return L.WX ? launch_one<real, 4, 1, 4, 1, CHECK>(L, s) : launch_one<real, 4, 1, 4, 0, CHECK>(L, s);
+        return cudaErrorInvalidValue;
+    }
     const int cpl = L.na_pad / 32;
     if constexpr (sizeof(real) == 4) {
         if (L.path == 3) {
@@ -1306,6 +1362,10 @@ void p3_geometry(int &pitch, int &cstride, int &hmax)
     cstride = P3_CSTRIDE;
     hmax = P3_HMAX;
 }
+
+#if !PDD_WIDE_UNIT
+void gf_geometry(int &pitch) { pitch = GF_PITCH; }
+#endif
 
 void p3_tile(int &tw, int &th)
 {

@@ -14,7 +14,7 @@ ap.add_argument("--general", default=None, help="cost:sigma:n:eps:n_coarse (gene
 ap.add_argument("--prec", type=int, default=32); ap.add_argument("--k", default="0")
 ap.add_argument("--modes", default="patchy,static"); ap.add_argument("--tol", type=float, default=1e-6)
 ap.add_argument("--kernel", type=int, default=0); ap.add_argument("--delta", default="0")
-ap.add_argument("--max_rounds", type=int, default=200000); ap.add_argument("--schedule", default="rounds"); ap.add_argument("--policy", type=int, default=0)
+ap.add_argument("--max_rounds", type=int, default=200000); ap.add_argument("--schedule", default="rounds"); ap.add_argument("--policy", type=int, default=0); ap.add_argument("--qt", type=int, default=0)
 a = ap.parse_args()
 t = time.time()
 if a.paper:
@@ -35,7 +35,7 @@ for mode in a.modes.split(","):
     for k in map(int, a.k.split(",")):
         for d in map(float, a.delta.split(",")):
             t = time.time()
-            st = s.solve(mode, tol=a.tol, k_inner=k, kernel=a.kernel, delta=d, max_rounds=a.max_rounds, schedule=a.schedule, bucket_policy=a.policy, raise_on_noconverge=False)
+            st = s.solve(mode, tol=a.tol, k_inner=k, kernel=a.kernel, delta=d, max_rounds=a.max_rounds, schedule=a.schedule, bucket_policy=a.policy, queue_target=a.qt, raise_on_noconverge=False)
             wall = time.time() - t
             nu = st["node_updates"]
             print(json.dumps(dict(mode=mode, k=k, delta=d, wall=round(wall, 3), rounds=st["rounds"], conv=st["converged"],
