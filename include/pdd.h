@@ -224,12 +224,31 @@ typedef struct {
     double seconds;
     int32_t converged;
     int32_t overlap_nodes; /* free nodes in >= 2 patches Omega_p (phi_p >= tau_P)              */
-    int64_t phi_offset;    /* byte offset of the final phi fields inside scratch               */
+    int64_t phi_offset;    /* byte offset of the final phi fields (sparse: the masses, n*n*K
+                              doubles) inside scratch                                          */
+    int64_t lab_offset;    /* sparse form: byte offset of the final patch lists (n*n*K int16)  */
+    int32_t max_list;      /* sparse form: longest per-node list (== K: memberships may have
+                              been truncated)                                                  */
+    int32_t reserved;
 } pdd_fuzzy_stats;
 pdd_status pdd_fuzzy_scratch_bytes(int32_t n, int32_t n_patches, size_t *bytes);
 pdd_status pdd_build_fuzzy_patches(pdd_ctx *ctx, int32_t n_patches, double eps_P, double tau_P,
                                    int64_t max_sweeps, void *scratch, size_t scratch_bytes,
                                    pdd_fuzzy_stats *st);
+
+/* The same construction in sparse form for decompositions with hundreds of patches (SURVEY.md
+ * 8(f) NEXT #2, reading R40): every node keeps its K largest (patch, phi_p) pairs, sorted by
+ * (phi_p descending, patch ascending), node-major, empty slots (-1, 0) last; a Jacobi sweep merges
+ * the lists of the foot's four corners in the order 00, 10, 01, 11 and keeps the K largest sums.
+ * With K >= the number of patches that reach a node the lists hold the dense phi bit for bit; a
+ * smaller K drops the smallest memberships (st->max_list == K flags that this may have happened).
+ * Owner = first listed patch, orphan n_patches for an empty list; overlap_nodes counts free nodes
+ * with >= 2 listed patches of phi_p >= tau_P.  K in {1, 2, 3, 4, 6, 8, 16}.  scratch: DEVICE
+ * memory of >= pdd_fuzzy_sparse_scratch_bytes(n, K) bytes (20 K n^2 + 512). */
+pdd_status pdd_fuzzy_sparse_scratch_bytes(int32_t n, int32_t K, size_t *bytes);
+pdd_status pdd_build_fuzzy_patches_sparse(pdd_ctx *ctx, int32_t n_patches, int32_t K, double eps_P,
+                                          double tau_P, int64_t max_sweeps, void *scratch,
+                                          size_t scratch_bytes, pdd_fuzzy_stats *st);
 
 /* Static equal squares: px columns x py rows, boundaries floor(k n / P) (R19). */
 pdd_status pdd_build_static(pdd_ctx *ctx, int32_t px, int32_t py);

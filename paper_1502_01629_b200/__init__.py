@@ -190,6 +190,29 @@ class Solver:
         del scratch
         return out
 
+    def build_fuzzy_patches_sparse(self, n_patches: int, K: int = 4, eps_P: float = 1e-3,
+                                   tau_P: float = 0.5, max_sweeps: int = 1 << 20,
+                                   return_lists: bool = False) -> dict:
+        """Fuzzy patches in sparse form: per node the K largest (patch, phi_p) pairs (hundreds of
+        patches; 20 K n^2 bytes of device scratch, a torch tensor owned here)."""
+        import torch
+        nb = C.c_size_t(0)
+        _check(N.lib().pdd_fuzzy_sparse_scratch_bytes(int(self.n), int(K), C.byref(nb)), None)
+        scratch = torch.empty(int(nb.value), dtype=torch.uint8, device=self.device)
+        st = N.pdd_fuzzy_stats()
+        self._ck(N.lib().pdd_build_fuzzy_patches_sparse(self._ctx, int(n_patches), int(K), float(eps_P),
+                                                        float(tau_P), int(max_sweeps),
+                                                        C.c_void_p(scratch.data_ptr()), int(nb.value),
+                                                        C.byref(st)))
+        out = st.as_dict()
+        if return_lists:
+            nk = self.n * self.n * int(K)
+            po, lo = int(st.phi_offset), int(st.lab_offset)
+            out["mass"] = scratch[po:po + 8 * nk].view(torch.float64).reshape(-1, int(K)).cpu().numpy()
+            out["lab"] = scratch[lo:lo + 2 * nk].view(torch.int16).reshape(-1, int(K)).cpu().numpy()
+        del scratch
+        return out
+
     def build_static(self, px: int, py: int) -> None:
         self._ck(N.lib().pdd_build_static(self._ctx, int(px), int(py)))
 

@@ -32,7 +32,8 @@ EXPORTS = ["pdd_version", "pdd_workspace_bytes", "pdd_create", "pdd_coarse_solve
            "pdd_get_coarse_values", "pdd_get_controls", "pdd_get_labels", "pdd_get_successors",
            "pdd_get_patch_rounds", "pdd_get_patch_residuals", "pdd_get_tile_rounds",
            "pdd_set_tile_cols", "pdd_kernel_launches", "pdd_last_error", "pdd_destroy",
-           "pdd_regime_analyse", "pdd_fuzzy_scratch_bytes", "pdd_build_fuzzy_patches"]
+           "pdd_regime_analyse", "pdd_fuzzy_scratch_bytes", "pdd_build_fuzzy_patches",
+           "pdd_fuzzy_sparse_scratch_bytes", "pdd_build_fuzzy_patches_sparse"]
 
 
 class pdd_coef(C.Structure):
@@ -82,10 +83,11 @@ class pdd_regime(C.Structure):
 
 class pdd_fuzzy_stats(C.Structure):
     _fields_ = [("sweeps", C.c_int64), ("residual", C.c_double), ("seconds", C.c_double),
-                ("converged", C.c_int32), ("overlap_nodes", C.c_int32), ("phi_offset", C.c_int64)]
+                ("converged", C.c_int32), ("overlap_nodes", C.c_int32), ("phi_offset", C.c_int64),
+                ("lab_offset", C.c_int64), ("max_list", C.c_int32), ("reserved", C.c_int32)]
 
     def as_dict(self):
-        return {k: getattr(self, k) for k, _ in self._fields_}
+        return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
 
 
 class pdd_coarse_stats(C.Structure):
@@ -132,6 +134,9 @@ def lib():
     L.pdd_fuzzy_scratch_bytes.argtypes = [C.c_int32, C.c_int32, C.POINTER(C.c_size_t)]
     L.pdd_build_fuzzy_patches.argtypes = [ctx, C.c_int32, C.c_double, C.c_double, C.c_int64, vp,
                                           C.c_size_t, C.POINTER(pdd_fuzzy_stats)]
+    L.pdd_fuzzy_sparse_scratch_bytes.argtypes = [C.c_int32, C.c_int32, C.POINTER(C.c_size_t)]
+    L.pdd_build_fuzzy_patches_sparse.argtypes = [ctx, C.c_int32, C.c_int32, C.c_double, C.c_double,
+                                                 C.c_int64, vp, C.c_size_t, C.POINTER(pdd_fuzzy_stats)]
     L.pdd_regime_analyse.argtypes = [C.c_double, C.c_double, C.c_double, C.c_double,
                                      C.POINTER(pdd_regime)]
     L.pdd_destroy.argtypes = [ctx]

@@ -485,6 +485,141 @@ __global__ void k_fuzzy_assign(DProblem P, const double *__restrict__ phi, int n
     if ((threadIdx.x & 31) == 0 && ov) atomicAdd(overlap, ov);
 }
 
+// ------------------------------------------------------------------ sparse fuzzy patches
+// Per node the K largest (patch, phi_p) pairs, sorted by (phi_p descending, patch ascending),
+// empty slots (-1, 0) last (reading R40; the dense fields above need 16 N_P n^2 bytes, this form
+// 20 K n^2).  One Jacobi sweep merges the four corner lists in the order 00, 10, 01, 11 -- a
+// label's partial sums are added in corner order: the dense expression with its zero terms left
+// out, so with K >= the number of patches reaching a node the result has the dense bits.
+template <int K>
+__device__ __forceinline__ void sparse_topk_insert(int16_t *ol, double *om, int &cnt, int16_t l, double m)
+{
+    int pos = cnt;
+    while (pos > 0 && (om[pos - 1] < m || (om[pos - 1] == m && ol[pos - 1] > l))) --pos;
+    if (pos >= K) return;
+    const int last = cnt < K ? cnt : K - 1;
+    for (int s = last; s > pos; --s) { ol[s] = ol[s - 1]; om[s] = om[s - 1]; }
+    ol[pos] = l;
+    om[pos] = m;
+    if (cnt < K) ++cnt;
+}
+
+__global__ void k_fuzzy_sparse_init(DProblem P, const int16_t *__restrict__ sector, int np, int K,
+                                    int16_t *lab, double *mass)
+{
+    const int64_t N = (int64_t)P.n * P.n;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < N;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const int sp = P.kind[k] == 1 ? sector[k] : -1;
+        const bool on = sp >= 0 && sp < np;
+        for (int s = 0; s < K; ++s) {
+            lab[k * K + s] = (s == 0 && on) ? (int16_t)sp : (int16_t)-1;
+            mass[k * K + s] = (s == 0 && on) ? 1.0 : 0.0;
+        }
+    }
+}
+
+template <int K>
+__global__ void k_fuzzy_sparse_sweep(DProblem P, const uint8_t *__restrict__ astar,
+                                     const int16_t *__restrict__ clab, const double *__restrict__ cm,
+                                     int16_t *__restrict__ nlab, double *__restrict__ nm, double eps,
+                                     unsigned long long *res_hist, int sweep, int *sweeps_done)
+{
+    if (sweep > 0 && __longlong_as_double((long long)res_hist[sweep - 1]) < eps) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(sweeps_done, 1);
+    const int n = P.n;
+    const int64_t N = (int64_t)n * n;
+    double res = 0.0;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < N;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        if (P.kind[k] != 0) {
+#pragma unroll
+            for (int s = 0; s < K; ++s) { nlab[k * K + s] = clab[k * K + s]; nm[k * K + s] = cm[k * K + s]; }
+            continue;
+        }
+        const int i = (int)(k % n), j = (int)(k / n);
+        const int a = astar[k];
+        const double c = coef_at(P.speed, i, j, n);
+        const double f1 = DADD(DMUL(c, P.ctrl[2 * a]), coef_at(P.drift[0], i, j, n));
+        const double f2 = DADD(DMUL(c, P.ctrl[2 * a + 1]), coef_at(P.drift[1], i, j, n));
+        int64_t cr[4];
+        double wg[4];
+        canon_stencil(n, DADD((double)i, DMUL(P.q, f1)), DADD((double)j, DMUL(P.q, f2)), cr, wg);
+        int16_t al[4 * K];
+        double am[4 * K];
+        int na = 0;
+        for (int t = 0; t < 4; ++t)
+            for (int s = 0; s < K; ++s) {
+                const int16_t l = clab[cr[t] * K + s];
+                if (l < 0) continue;
+                const double term = DMUL(wg[t], cm[cr[t] * K + s]);
+                int idx = 0;
+                while (idx < na && al[idx] != l) ++idx;
+                if (idx < na) am[idx] = DADD(am[idx], term);
+                else { al[na] = l; am[na] = term; ++na; }
+            }
+        int16_t ol[K], oldl[K];
+        double om[K], oldm[K];
+        int cnt = 0;
+        for (int idx = 0; idx < na; ++idx)
+            if (am[idx] > 0.0) sparse_topk_insert<K>(ol, om, cnt, al[idx], am[idx]);
+#pragma unroll
+        for (int u = 0; u < K; ++u) { oldl[u] = clab[k * K + u]; oldm[u] = cm[k * K + u]; }
+        for (int s = 0; s < cnt; ++s) {
+            double old = 0.0;
+            for (int u = 0; u < K; ++u)
+                if (oldl[u] == ol[s]) old = oldm[u];
+            res = fmax(res, fabs(DSUB(om[s], old)));
+        }
+        for (int u = 0; u < K; ++u) {
+            if (oldl[u] < 0) continue;
+            bool found = false;
+            for (int s = 0; s < cnt; ++s) found |= ol[s] == oldl[u];
+            if (!found) res = fmax(res, oldm[u]);
+        }
+        for (int s = 0; s < K; ++s) {
+            nlab[k * K + s] = s < cnt ? ol[s] : (int16_t)-1;
+            nm[k * K + s] = s < cnt ? om[s] : 0.0;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) res = fmax(res, __shfl_xor_sync(0xffffffffu, res, o));
+    if ((threadIdx.x & 31) == 0 && res > 0.0)
+        atomicMax(&res_hist[sweep], (unsigned long long)__double_as_longlong(res));
+}
+
+// owner = first listed patch (largest phi_p, lowest p on ties), orphan np when the list is empty;
+// overlap: free nodes with >= 2 listed patches of phi_p >= tau; maxlist: the longest list found
+// (== K means some node may have lost memberships to the truncation)
+__global__ void k_fuzzy_sparse_assign(DProblem P, const int16_t *__restrict__ lab,
+                                      const double *__restrict__ mass, int K, int np, double tau,
+                                      int16_t *__restrict__ labels, int *overlap, int *maxlist)
+{
+    const int64_t N = (int64_t)P.n * P.n;
+    int ov = 0, ml = 0;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < N;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const uint8_t kd = P.kind[k];
+        if (kd != 0) { labels[k] = kd == 1 ? -1 : -2; continue; }
+        int cnt = 0, len = 0;
+        for (int s = 0; s < K; ++s) {
+            if (lab[k * K + s] < 0) continue;
+            ++len;
+            if (mass[k * K + s] >= tau) ++cnt;
+        }
+        labels[k] = lab[k * K] >= 0 ? lab[k * K] : (int16_t)np;
+        ov += cnt >= 2;
+        ml = max(ml, len);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        ov += __shfl_xor_sync(0xffffffffu, ov, o);
+        ml = max(ml, __shfl_xor_sync(0xffffffffu, ml, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (ov) atomicAdd(overlap, ov);
+        atomicMax(maxlist, ml);
+    }
+}
+
 // k_synthesize with the row-invariant table of k_coarse_rowtab built on the fine grid (row-uniform
 // coefficients): the same operations per (node, control), the row-dependent ones hoisted
 __global__ void k_synthesize_rt(DProblem P, const double *__restrict__ uhat,
@@ -704,6 +839,38 @@ void launch_fuzzy_sweep(const DProblem &P, const uint8_t *astar, int np, const d
     const int64_t N = (int64_t)P.n * P.n;
     k_fuzzy_sweep<<<grid_for(N, 128), 128, 0, s>>>(P, astar, np, cur, nxt, eps, res_hist, sweep,
                                                     sweeps_done);
+}
+
+void launch_fuzzy_sparse_init(const DProblem &P, const int16_t *sector, int np, int K, int16_t *lab,
+                              double *mass, cudaStream_t s)
+{
+    const int64_t N = (int64_t)P.n * P.n;
+    k_fuzzy_sparse_init<<<grid_for(N, 256), 256, 0, s>>>(P, sector, np, K, lab, mass);
+}
+
+bool launch_fuzzy_sparse_sweep(const DProblem &P, const uint8_t *astar, int K, const int16_t *clab,
+                               const double *cm, int16_t *nlab, double *nm, double eps,
+                               unsigned long long *res_hist, int sweep, int *sweeps_done, cudaStream_t s)
+{
+    const int64_t N = (int64_t)P.n * P.n;
+    const int g = grid_for(N, 128);
+#define PDD_FS(K_)                                                                                     \
+    case K_:                                                                                           \
+        k_fuzzy_sparse_sweep<K_><<<g, 128, 0, s>>>(P, astar, clab, cm, nlab, nm, eps, res_hist, sweep, \
+                                                   sweeps_done);                                       \
+        return true;
+    switch (K) {
+        PDD_FS(1) PDD_FS(2) PDD_FS(3) PDD_FS(4) PDD_FS(6) PDD_FS(8) PDD_FS(16)
+    default: return false;
+    }
+#undef PDD_FS
+}
+
+void launch_fuzzy_sparse_assign(const DProblem &P, const int16_t *lab, const double *mass, int K, int np,
+                                double tau, int16_t *labels, int *overlap, int *maxlist, cudaStream_t s)
+{
+    const int64_t N = (int64_t)P.n * P.n;
+    k_fuzzy_sparse_assign<<<grid_for(N, 256), 256, 0, s>>>(P, lab, mass, K, np, tau, labels, overlap, maxlist);
 }
 
 void launch_fuzzy_assign(const DProblem &P, const double *phi, int np, double tau, int16_t *labels,

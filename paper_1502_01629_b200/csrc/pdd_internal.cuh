@@ -93,6 +93,14 @@ void launch_fuzzy_sweep(const DProblem &P, const uint8_t *astar, int np, const d
                         int *sweeps_done, cudaStream_t s);
 void launch_fuzzy_assign(const DProblem &P, const double *phi, int np, double tau, int16_t *labels,
                          int *overlap, cudaStream_t s);
+// sparse top-K form (per node K (patch, phi_p) pairs, node-major); K in {1,2,3,4,6,8,16}
+void launch_fuzzy_sparse_init(const DProblem &P, const int16_t *sector, int np, int K, int16_t *lab,
+                              double *mass, cudaStream_t s);
+bool launch_fuzzy_sparse_sweep(const DProblem &P, const uint8_t *astar, int K, const int16_t *clab,
+                               const double *cm, int16_t *nlab, double *nm, double eps,
+                               unsigned long long *res_hist, int sweep, int *sweeps_done, cudaStream_t s);
+void launch_fuzzy_sparse_assign(const DProblem &P, const int16_t *lab, const double *mass, int K, int np,
+                                double tau, int16_t *labels, int *overlap, int *maxlist, cudaStream_t s);
 void launch_prolong(int nc, const double *uc, int n, double *out, cudaStream_t s);
 void launch_synthesize(const DProblem &P, const double *uhat, uint8_t *astar, cudaStream_t s);
 void launch_successor(const DProblem &P, double M, const uint8_t *astar, int32_t *succ,

@@ -784,8 +784,106 @@ pdd_status pdd_build_fuzzy_patches(pdd_ctx *ctx, int32_t n_patches, double eps_P
         st->converged = converged ? 1 : 0;
         st->overlap_nodes = ctx->h_int[1];
         st->phi_offset = (int64_t)((const char *)fin - (const char *)scratch);
+        st->lab_offset = 0;
+        st->max_list = 0;
+        st->reserved = 0;
     }
     return converged ? PDD_OK : fail(ctx, PDD_E_NOCONVERGE, "fuzzy patches: %lld sweeps without reaching eps_P",
+                                     (long long)done);
+}
+
+pdd_status pdd_fuzzy_sparse_scratch_bytes(int32_t n, int32_t K, size_t *bytes)
+{
+    if (!bytes) return fail(nullptr, PDD_E_INVALID, "bytes is NULL");
+    if (n < 3 || K < 1 || K > 16)
+        return fail(nullptr, PDD_E_INVALID, "sparse fuzzy scratch: n >= 3 and 1 <= K <= 16");
+    const size_t NK = (size_t)n * (size_t)n * (size_t)K;
+    *bytes = 2 * (sizeof(double) + sizeof(int16_t)) * NK + 512;
+    return PDD_OK;
+}
+
+pdd_status pdd_build_fuzzy_patches_sparse(pdd_ctx *ctx, int32_t n_patches, int32_t K, double eps_P,
+                                          double tau_P, int64_t max_sweeps, void *scratch,
+                                          size_t scratch_bytes, pdd_fuzzy_stats *st)
+{
+    if (!ctx) return fail(nullptr, PDD_E_INVALID, "ctx is NULL");
+    if (!ctx->synth_done) return fail(ctx, PDD_E_STATE, "pdd_build_fuzzy_patches_sparse needs pdd_synthesize first");
+    if (n_patches < 1 || n_patches >= kMaxPatches)
+        return fail(ctx, PDD_E_INVALID, "n_patches must be in 1..%d", kMaxPatches - 1);
+    if (!ctx->F.sector) return fail(ctx, PDD_E_INVALID, "the fine problem has no sector table");
+    if (!(eps_P > 0.0) || !(tau_P > 0.0 && tau_P < 1.0))
+        return fail(ctx, PDD_E_INVALID, "need eps_P > 0 and 0 < tau_P < 1");
+    if (max_sweeps <= 0 || max_sweeps > kMaxCoarseSweeps)
+        return fail(ctx, PDD_E_INVALID, "max_sweeps must be in 1..%lld", (long long)kMaxCoarseSweeps);
+    if (!(K == 1 || K == 2 || K == 3 || K == 4 || K == 6 || K == 8 || K == 16))
+        return fail(ctx, PDD_E_INVALID, "K must be one of 1, 2, 3, 4, 6, 8, 16");
+    size_t need = 0;
+    pdd_status ps = pdd_fuzzy_sparse_scratch_bytes(ctx->fine.n, K, &need);
+    if (ps != PDD_OK) return ps;
+    if (!scratch || scratch_bytes < need)
+        return fail(ctx, PDD_E_NOMEM, "sparse fuzzy scratch needs %zu bytes", need);
+    cudaStream_t s = ctx->stream;
+    const size_t NK = (size_t)ctx->fine.n * ctx->fine.n * (size_t)K;
+    char *b = (char *)scratch;
+    const size_t mis = (size_t)((uintptr_t)b % 256);
+    if (mis) b += 256 - mis;
+    double *mass[2] = {reinterpret_cast<double *>(b), reinterpret_cast<double *>(b) + NK};
+    int16_t *lab[2] = {reinterpret_cast<int16_t *>(mass[1] + NK), reinterpret_cast<int16_t *>(mass[1] + NK) + NK};
+    CK(cudaEventRecord(ctx->ev[0], s));
+    launch_fuzzy_sparse_init(ctx->F.d, ctx->F.sector, n_patches, K, lab[0], mass[0], s);
+    CK(cudaMemsetAsync(ctx->res_hist, 0, sizeof(unsigned long long) * max_sweeps, s));
+    CK(cudaMemsetAsync(ctx->dev_int, 0, 3 * sizeof(int), s));
+    ctx->launches++;
+    int64_t issued = 0, batch = 8;
+    int done = 0;
+    bool converged = false;
+    while (issued < max_sweeps) {
+        const int64_t nb = std::min<int64_t>(batch, max_sweeps - issued);
+        for (int64_t q = 0; q < nb; ++q, ++issued)
+            launch_fuzzy_sparse_sweep(ctx->F.d, ctx->astar, K, lab[issued & 1], mass[issued & 1],
+                                      lab[(issued + 1) & 1], mass[(issued + 1) & 1], eps_P, ctx->res_hist,
+                                      (int)issued, ctx->dev_int, s);
+        ctx->launches += nb;
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(ctx->h_int, ctx->dev_int, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        done = ctx->h_int[0];
+        if (done < issued) { converged = true; break; }
+        unsigned long long last = 0;
+        CK(cudaMemcpy(&last, ctx->res_hist + (issued - 1), sizeof last, cudaMemcpyDeviceToHost));
+        double lr;
+        std::memcpy(&lr, &last, sizeof lr);
+        if (lr < eps_P) { converged = true; break; }
+        batch = std::min<int64_t>(batch * 2, 256);
+    }
+    const int fin = done & 1;
+    launch_fuzzy_sparse_assign(ctx->F.d, lab[fin], mass[fin], K, n_patches, tau_P, ctx->labels,
+                               ctx->dev_int + 1, ctx->dev_int + 2, s);
+    ctx->launches++;
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(ctx->ev[1], s));
+    CK(cudaMemcpyAsync(ctx->h_int + 1, ctx->dev_int + 1, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    ctx->labels_mode = 1;
+    ctx->n_patches = n_patches;
+    ctx->prepared_kernel = -1;
+    if (st) {
+        unsigned long long lastbits = 0;
+        if (done > 0)
+            CK(cudaMemcpy(&lastbits, ctx->res_hist + (done - 1), sizeof lastbits, cudaMemcpyDeviceToHost));
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]);
+        st->sweeps = done;
+        std::memcpy(&st->residual, &lastbits, sizeof(double));
+        st->seconds = ms * 1e-3;
+        st->converged = converged ? 1 : 0;
+        st->overlap_nodes = ctx->h_int[1];
+        st->max_list = ctx->h_int[2];
+        st->reserved = 0;
+        st->phi_offset = (int64_t)((const char *)mass[fin] - (const char *)scratch);
+        st->lab_offset = (int64_t)((const char *)lab[fin] - (const char *)scratch);
+    }
+    return converged ? PDD_OK : fail(ctx, PDD_E_NOCONVERGE, "sparse fuzzy patches: %lld sweeps without reaching eps_P",
                                      (long long)done);
 }
 
