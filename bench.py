@@ -69,6 +69,9 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-others", action="store_true",
                     help="skip the time-to-converge report of the other BASELINE configs")
+    ap.add_argument("--oracle-ttc", default="C1,C2",
+                    help="configs whose oracle (plain fp64 Jacobi, host cores) time-to-converge is MEASURED "
+                         "(cfg or cfg@n, comma separated; C3@1025 takes minutes; '' = none)")
     return ap.parse_args()
 
 
@@ -222,6 +225,34 @@ def run_reference(args, world, rank):
     print(json.dumps(out), flush=True)
 
 
+def oracle_time_to_converge(spec: str):
+    """Measured wall time of the oracle's plain Jacobi value iteration to the config's tolerance
+    (fp64, all host cores): the CPU side of the paper's time-to-converge comparison."""
+    import pdd_inputs as I
+    import oracle as O
+    out = {}
+    for item in [x for x in spec.split(",") if x]:
+        cfg, _, nn = item.partition("@")
+        inst = I.make_config(cfg, n=int(nn) if nn else None)
+        t = time.perf_counter()
+        r = O.jacobi(inst, tol=inst.tol, max_sweeps=10**6)
+        dt = time.perf_counter() - t
+        out[item] = {"grid": inst.n, "tol": inst.tol, "sweeps": int(r["sweeps"]), "seconds": dt,
+                     "threads": O.num_threads(), "kind": "measured",
+                     "node_updates_per_s": inst.free_count() * int(r["sweeps"]) / dt}
+    return out
+
+
+def decomposition_quality(s, inst):
+    """Orphan fraction and non-empty patch count of the patch labels held by the solver."""
+    import numpy as np
+    import pdd_inputs as I
+    lab = s.get_labels()
+    own = lab[inst.kind == I.KIND_FREE]
+    return {"patches": int(inst.n_patches), "orphan_fraction": float((own == inst.n_patches).mean()),
+            "patches_nonempty": int(np.unique(own[(own >= 0) & (own < inst.n_patches)]).size)}
+
+
 # ----------------------------------------------------------------------------- our arm
 def pipeline_step(s, inst, args, mode="patchy"):
     """One pass of the hot path on a resident context; returns the fine-solve stats."""
@@ -245,7 +276,7 @@ def main():
     import torch
     import torch.distributed as dist
     import pdd_inputs as I
-    from paper_1502_01629_b200 import Solver
+    from paper_1502_01629_b200 import Solver, measure_alu_peaks
 
     torch.cuda.set_device(local)
     inst = I.make_config(args.config, n=args.n)
@@ -265,7 +296,7 @@ def main():
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0 = s.kernel_launches()
     ev0.record(stream)
-    nu, t_sweep, t_verify, rounds, t_solve = 0, 0.0, 0.0, 0, 0.0
+    nu, t_sweep, t_verify, rounds, t_solve, sweep_launches = 0, 0.0, 0.0, 0, 0.0, 0
     for _ in range(args.steps):
         st = pipeline_step(s, inst, args)
         assert st["converged"] == 1
@@ -274,6 +305,7 @@ def main():
         t_verify += st["seconds_verify"]
         t_solve += st["seconds_total"]
         rounds += st["rounds"]
+        sweep_launches += st["rounds"] - st["verify_passes"]
     ev1.record(stream)
     torch.cuda.synchronize()
     barrier(world)
@@ -282,6 +314,9 @@ def main():
     t_local = ev0.elapsed_time(ev1) * 1e-3
     nu_all, t_max, value = aggregate(nu, t_local, world)
     last = st
+    decomp = decomposition_quality(s, inst) if rank == 0 else None
+    # roofline denominators measured on this box (FFMA and LDS.128 micro-benchmarks of libpdd)
+    alu = measure_alu_peaks(5)
 
     # static decomposition on the same kernels (time-to-converge comparison)
     static = None
@@ -329,7 +364,8 @@ def main():
     flop_per_update = inst.n_controls * (15 * nbr + 10)
     flop_bilinear = inst.n_controls * nbr * 4 * 2
     achieved = flop_per_update * nu / max(t_sweep, 1e-12) / 1e12
-    peak = FP32_PEAK_TFLOPS if args.precision == 32 else FP64_PEAK_TFLOPS
+    peak32 = alu["fp32_tflops"] if alu["fp32_tflops"] > 0 else FP32_PEAK_TFLOPS
+    peak = peak32 if args.precision == 32 else peak32 / 2.0
     roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
             "frac": achieved / peak, "traffic": None,
             "flop_basis": "SURVEY.md 8(d): F = N_A (15 * 2p + 10) per node-update",
@@ -337,12 +373,20 @@ def main():
             "frac_bilinear_only": flop_bilinear * nu / max(t_sweep, 1e-12) / 1e12 / peak,
             "kernel": {1: "k_sweep path 1 (general stencil)",
                        2: "k_sweep path 2 (row-table stencil, one node per warp step)",
-                       3: "k_sweep path 3 (row-table stencil, in-tile Gauss-Seidel, 4 nodes per step)"}
+                       3: "k_sweep_queue path 3 (row-table stencil, in-tile Gauss-Seidel, 4 nodes per "
+                          "step; persistent CTAs on the tile work queue)",
+                       4: "k_sweep_queue path 4 (lean general stencil)"}
                       .get(last["kernel_used"], "k_sweep"),
             "flop_per_node_update": flop_per_update,
             "kernel_node_updates_per_s": nu / max(t_sweep, 1e-12),
             "kernel_seconds_share_of_step": t_sweep / max(t_local, 1e-12),
-            "peak_basis": "derived: 148 SM x 128 FP32 lanes x 2 x 1965 MHz (guide unit counts)"}
+            "peak_basis": ("measured on this GPU: FFMA micro-benchmark of libpdd (pdd_measure_alu_peaks, best "
+                           "of 5; fp64 = half of it); derived figure 148 SM x 128 lanes x 2 x 1.965 GHz = "
+                           "%.1f TFLOP/s" % FP32_PEAK_TFLOPS),
+            "peak_derived": FP32_PEAK_TFLOPS if args.precision == 32 else FP64_PEAK_TFLOPS,
+            "frac_of_derived_peak": achieved / (FP32_PEAK_TFLOPS if args.precision == 32 else FP64_PEAK_TFLOPS),
+            "smem_peak_tbs_measured": alu["smem_tbs"],
+            "sweep_launches_per_step": sweep_launches / args.steps}
     if static:
         # the same kernel in the static solve's full rounds (16 x 128 path-3 tiles at C4/C5,
         # runtime.cu p3_use_wide; the patchy step above runs 32 x 64 tiles)
@@ -351,11 +395,13 @@ def main():
     if os.path.exists(prof):
         try:
             pj = json.load(open(prof))
-            per_launch_updates = nu / max(1, rounds)
+            per_launch_updates = nu / max(1, sweep_launches)
             roof["traffic"] = pj["dram_bytes_per_node_update"] * per_launch_updates
+            roof["algorithmic_bytes_per_launch"] = pj.get("algorithmic_bytes_per_node_update", 18.4) * per_launch_updates
             roof["traffic_basis"] = ("dram bytes per node-update from ncu --set full (%s) x the "
                                      "average node-updates per sweep launch of this run; "
-                                     "algorithmic bytes per node-update ~18.4 at k_inner 1" % pj["source"])
+                                     "algorithmic bytes per node-update ~18.4 at one sweep per visit "
+                                     "(tile + halo fp64 read, fp64 write, kinds)" % pj["source"])
         except Exception:
             pass
 
@@ -371,6 +417,8 @@ def main():
             prec = 64 if cfg == "C1" else args.precision
             so = Solver(ci, precision=prec, device=str(dev))
             rec = {"grid": ci.n, "precision": prec, "tol": ci.tol}
+            flop_o = ci.n_controls * (15 * (2 * ci.p if ci.p > 0 else 1) + 10)
+            peak_o = peak32 if prec == 32 else peak32 / 2.0
             for mode in (("static",) if ci.coarse is None else ("patchy", "static")):
                 pipeline_step(so, ci, args, mode=mode)                       # warm-up
                 torch.cuda.synchronize()
@@ -390,14 +438,19 @@ def main():
                              "sweep_equivalents": sto["node_updates"] / ci.free_count(),
                              "kernel_node_updates_per_s": sto["node_updates"] / max(sto["seconds_sweep"], 1e-12),
                              "kernel": sto["kernel_used"], "converged": sto["converged"]}
+                rec[mode]["kernel_alu_frac"] = rec[mode]["kernel_node_updates_per_s"] * flop_o / 1e12 / peak_o
+                if mode == "patchy":
+                    rec["decomposition"] = decomposition_quality(so, ci)
             so.close()
             del so
             others[cfg] = rec
 
     cpu = None
+    ottc = None
     if not args.no_cpu and rank == 0 and world == 1:
         v, desc, thr, _ = oracle_sample(inst, args.cpu_seconds)
         cpu = {"value": v, "unit": UNIT, "cores": thr, "kind": "oracle", "sample": desc}
+        ottc = oracle_time_to_converge(args.oracle_ttc)
 
     if rank == 0:
         out = {
@@ -410,6 +463,7 @@ def main():
                                    f"tol {args.tol:g}) on {inst.n}^2",
                        "grid": inst.n, "controls": inst.n_controls, "branches": 2 * inst.p,
                        "patches": inst.n_patches, "k_inner": args.k_inner if args.k_inner is not None else {"patchy": "auto (1)", "static": "auto (4)"},
+                       "schedule": "work queue (persistent sweep CTAs, key-order admission), then full-grid verification",
                        "path3_tile": {"patchy": "32x64", "static": "16x128" if 128 * inst.dx <= 0.125 + 1e-12 else "32x64"},
                        "l2": "inputs larger than L2 (V fp64 %d MB)" % (inst.n * inst.n * 8 >> 20),
                        "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
@@ -419,7 +473,9 @@ def main():
                                  "rounds_patchy": rounds // args.steps,
                                  "sweep_equivalents_patchy": nu / args.steps / inst.free_count()},
             "static": static,
+            "decomposition": decomp,
             "other_configs": others,
+            "oracle_time_to_converge": ottc,
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -427,8 +483,9 @@ def main():
             "clocks": clk,
         }
         if cpu:
-            # plain-Jacobi oracle time-to-converge estimate: sweeps ~ 0.71 n
-            out["time_to_converge"]["oracle_jacobi_estimate_s"] = (
+            # EXTRAPOLATED (not measured): plain-Jacobi oracle sweeps ~ 0.71 n (
+            # the measured oracle solves of the smaller configs are in oracle_time_to_converge)
+            out["time_to_converge"]["oracle_jacobi_extrapolated_s"] = (
                 inst.free_count() * 0.71 * inst.n / cpu["value"])
         print(json.dumps(out), flush=True)
     barrier(world)

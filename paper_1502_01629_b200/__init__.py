@@ -326,3 +326,11 @@ def regime_analyse(f_min: float, f_max: float, sigma_norm: float, dx: float) -> 
     d = r.as_dict()
     d["hyperbolic"] = bool(d["hyperbolic"])
     return d
+
+
+def measure_alu_peaks(reps: int = 5) -> dict:
+    """FP32 FFMA and shared-memory (LDS.128) throughput of the current device, measured by the
+    library's micro-benchmarks (pdd_measure_alu_peaks): the roofline denominators of bench.py."""
+    f, m = C.c_double(0.0), C.c_double(0.0)
+    _check(N.lib().pdd_measure_alu_peaks(None, int(reps), C.byref(f), C.byref(m)), None)
+    return {"fp32_tflops": f.value, "smem_tbs": m.value}

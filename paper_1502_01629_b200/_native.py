@@ -33,7 +33,7 @@ EXPORTS = ["pdd_version", "pdd_workspace_bytes", "pdd_create", "pdd_coarse_solve
            "pdd_get_patch_rounds", "pdd_get_patch_residuals", "pdd_get_tile_rounds",
            "pdd_set_tile_cols", "pdd_kernel_launches", "pdd_last_error", "pdd_destroy",
            "pdd_regime_analyse", "pdd_fuzzy_scratch_bytes", "pdd_build_fuzzy_patches",
-           "pdd_fuzzy_sparse_scratch_bytes", "pdd_build_fuzzy_patches_sparse"]
+           "pdd_fuzzy_sparse_scratch_bytes", "pdd_build_fuzzy_patches_sparse", "pdd_measure_alu_peaks"]
 
 
 class pdd_coef(C.Structure):
@@ -134,6 +134,7 @@ def lib():
     L.pdd_fuzzy_scratch_bytes.argtypes = [C.c_int32, C.c_int32, C.POINTER(C.c_size_t)]
     L.pdd_build_fuzzy_patches.argtypes = [ctx, C.c_int32, C.c_double, C.c_double, C.c_int64, vp,
                                           C.c_size_t, C.POINTER(pdd_fuzzy_stats)]
+    L.pdd_measure_alu_peaks.argtypes = [vp, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double)]
     L.pdd_fuzzy_sparse_scratch_bytes.argtypes = [C.c_int32, C.c_int32, C.POINTER(C.c_size_t)]
     L.pdd_build_fuzzy_patches_sparse.argtypes = [ctx, C.c_int32, C.c_int32, C.c_double, C.c_double,
                                                  C.c_int64, vp, C.c_size_t, C.POINTER(pdd_fuzzy_stats)]

@@ -197,6 +197,14 @@ static pdd_status fail(pdd_ctx *c, pdd_status s, const char *fmt, ...)
                         cudaGetErrorString(e_), __FILE__, __LINE__);                         \
     } while (0)
 
+#define CK0(call)                                                                            \
+    do {                                                                                     \
+        cudaError_t e_ = (call);                                                             \
+        if (e_ != cudaSuccess)                                                               \
+            return fail(nullptr, PDD_E_CUDA, "%s failed: %s (%s:%d)", #call,                 \
+                        cudaGetErrorString(e_), __FILE__, __LINE__);                         \
+    } while (0)
+
 static pdd_status validate(const pdd_problem *p, const char *what)
 {
     if (!p) return fail(nullptr, PDD_E_INVALID, "%s problem is NULL", what);
@@ -790,6 +798,89 @@ pdd_status pdd_build_fuzzy_patches(pdd_ctx *ctx, int32_t n_patches, double eps_P
     }
     return converged ? PDD_OK : fail(ctx, PDD_E_NOCONVERGE, "fuzzy patches: %lld sweeps without reaching eps_P",
                                      (long long)done);
+}
+
+}  // extern "C"
+
+// ---- machine-peak micro-benchmarks (pdd_measure_alu_peaks)
+__global__ void __launch_bounds__(512) k_peak_ffma(float *sink, int iters, float b, float c)
+{
+    float a0 = threadIdx.x, a1 = a0 + 1.f, a2 = a0 + 2.f, a3 = a0 + 3.f, a4 = a0 + 4.f, a5 = a0 + 5.f,
+          a6 = a0 + 6.f, a7 = a0 + 7.f;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            a0 = fmaf(a0, b, c); a1 = fmaf(a1, b, c); a2 = fmaf(a2, b, c); a3 = fmaf(a3, b, c);
+            a4 = fmaf(a4, b, c); a5 = fmaf(a5, b, c); a6 = fmaf(a6, b, c); a7 = fmaf(a7, b, c);
+        }
+    }
+    const float r = ((a0 + a1) + (a2 + a3)) + ((a4 + a5) + (a6 + a7));
+    if (r == 12345.678f) sink[0] = r;   // never true: keeps the chains alive
+}
+
+__global__ void __launch_bounds__(512) k_peak_lds(float *sink, int iters)
+{
+    __shared__ float4 buf[1024];
+    for (int e = threadIdx.x; e < 1024; e += blockDim.x) buf[e] = make_float4(1.f, 2.f, 3.f, (float)e);
+    __syncthreads();
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    int idx = threadIdx.x;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            // a warp reads 512 contiguous bytes; volatile asm: every load is issued
+            float4 v;
+            const unsigned a = (unsigned)__cvta_generic_to_shared(&buf[(idx + 32 * u) & 1023]);
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+            acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        }
+        idx = (idx + 64) & 1023;
+    }
+    if (acc.x + acc.y + acc.z + acc.w == 12345.678f) sink[0] = acc.x;
+}
+
+extern "C" {
+
+pdd_status pdd_measure_alu_peaks(void *stream, int32_t reps, double *fp32_tflops, double *smem_tbs)
+{
+    if (reps < 1 || reps > 1000) return fail(nullptr, PDD_E_INVALID, "reps must be in 1..1000");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int dev = 0, sms = 0;
+    CK0(cudaGetDevice(&dev));
+    CK0(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    float *sink = nullptr;
+    CK0(cudaMalloc(&sink, sizeof(float)));
+    cudaEvent_t e0, e1;
+    CK0(cudaEventCreate(&e0));
+    CK0(cudaEventCreate(&e1));
+    const int grid = sms * 4, block = 512;
+    double best_f = 0.0, best_l = 0.0;
+    for (int r = 0; r < reps + 1; ++r) {        // the first launch warms up
+        const int it_f = 4096, it_l = 2048;
+        cudaEventRecord(e0, s);
+        k_peak_ffma<<<grid, block, 0, s>>>(sink, it_f, 1.0000001f, 1e-7f);
+        cudaEventRecord(e1, s);
+        cudaEventSynchronize(e1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        const double fl = 2.0 * 64.0 * it_f * (double)grid * block;
+        if (r > 0 && ms > 0.f) best_f = std::max(best_f, fl / (ms * 1e-3) * 1e-12);
+        cudaEventRecord(e0, s);
+        k_peak_lds<<<grid, block, 0, s>>>(sink, it_l);
+        cudaEventRecord(e1, s);
+        cudaEventSynchronize(e1);
+        cudaEventElapsedTime(&ms, e0, e1);
+        const double by = 16.0 * 8.0 * it_l * (double)grid * block;
+        if (r > 0 && ms > 0.f) best_l = std::max(best_l, by / (ms * 1e-3) * 1e-12);
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(sink);
+    CK0(cudaGetLastError());
+    if (fp32_tflops) *fp32_tflops = best_f;
+    if (smem_tbs) *smem_tbs = best_l;
+    return PDD_OK;
 }
 
 pdd_status pdd_fuzzy_sparse_scratch_bytes(int32_t n, int32_t K, size_t *bytes)

@@ -1,6 +1,6 @@
 """Full-size parity at BASELINE.json's own grids (C3 2049^2, C4 4097^2, C5 8193^2), element by
-element, in the launch configuration bench.py times (patchy pipeline, fp32, rounds schedule,
-automatic k_inner: one in-tile sweep per visit).
+element, in the launch configuration bench.py times (patchy pipeline, fp32, the default work-queue
+schedule, automatic k_inner: one in-tile sweep per visit).
 
 north_star: labels bit-exact and V within tolerance on all five configs (the outputs of the
 paper's pipeline).  At these sizes the oracle computes every
