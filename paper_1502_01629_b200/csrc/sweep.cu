@@ -82,6 +82,35 @@ constexpr unsigned FULL = 0xffffffffu;
 // path 4 in fp64 needs twice the registers: 2 CTAs / SM
 template <typename real, int PATH>
 constexpr int min_blocks_r() { return (PATH == 4 && sizeof(real) == 8) ? 2 : min_blocks<PATH>(); }
+// PDD_CHECKED (development builds; compute-sanitizer is not available on the GPU pool): bounds
+// checks of the kernels' own making on every shared-memory address the sweeps form (window loads,
+// corner gathers, commits, staging stores) and on tile indices; violations are counted in g_fault
+// (read by pdd_dev_faults) instead of trapping.  scripts/run_checked.sh runs the GPU tests on it.
+#ifndef PDD_CHECKED
+#define PDD_CHECKED 0
+#endif
+#if PDD_CHECKED
+__device__ unsigned long long g_fault[2];   // [0] violations, [1] code of the first one
+__device__ __forceinline__ void chk_fail(int code)
+{
+    atomicAdd(&g_fault[0], 1ull);
+    atomicCAS(&g_fault[1], 0ull, (unsigned long long)code);
+}
+struct ChkBounds { const char *lo, *hi; };
+__device__ __forceinline__ ChkBounds &chk_bounds()
+{
+    __shared__ ChkBounds b;
+    return b;
+}
+#define PDD_CHK(cond, code) do { if (!(cond)) chk_fail(code); } while (0)
+// the bytes [p, p + n reals) lie inside the staged V tile (+ halo, all shifted copies)
+#define PDD_CHK_TILE(p, n, code)                                                              \
+    PDD_CHK((const char *)(p) >= chk_bounds().lo && (const char *)((p) + (n)) <= chk_bounds().hi, code)
+#else
+#define PDD_CHK(cond, code) ((void)0)
+#define PDD_CHK_TILE(p, n, code) ((void)0)
+#endif
+
 template <int WY, int WX>
 struct TWOf { static constexpr int value = WX > 0 ? WX * (64 / (WX > 0 ? WX : 1)) : 64; };   // multiple of WX, <= 64
 
@@ -271,6 +300,8 @@ __device__ __forceinline__ real general_node_c(const DProblem &P, const real *__
             const real fy = rmin(rfloor(yr), cym);
             const real tx = xr - fx, ty = yr - fy;
             const real *pc = base + (int)fy * pitch + (int)fx;
+            PDD_CHK_TILE(pc, 2, 3);
+            PDD_CHK_TILE(pc + pitch, 2, 3);
             const real ws = rmax((real)0, (real)1 - rabs(xr)) * rmax((real)0, (real)1 - rabs(yr));
             if (big_self) {
                 // the node's own corner enters with value 0 (its weight goes to Lambda0,
@@ -350,7 +381,10 @@ __device__ __forceinline__ void commit_node(real *p, real best, bool last, real 
         if (last) res = rmax(res, rabs(best - old));
         if constexpr (!CHECK) {
 #pragma unroll
-            for (int q = 0; q < NCOPY; ++q) p[q * cstride + q] = best;
+            for (int q = 0; q < NCOPY; ++q) {
+                PDD_CHK_TILE(p + q * cstride + q, 1, 4);
+                p[q * cstride + q] = best;
+            }
         } else {
             if (out) out[gidx] = Vref + (double)best;
             if (A && A->patch_res) patch_acc(*A, gidx, (double)rabs(best - old));
@@ -585,6 +619,7 @@ __device__ __forceinline__ int q_take(const QueueArgs &Q, unsigned long long tic
     }
     *slot = 0;
     const int t = v - 1;
+    PDD_CHK(t >= 0 && Q.rank[t] < Q.n_order, 6);
     atomicExch(Q.state + t, 2);   // queued -> visiting (only the consumer changes state 1)
     __threadfence();              // acquire: the visit's loads of V come after the state change
     return t;
@@ -681,6 +716,14 @@ __device__ __forceinline__ void sweep_tile(const KP<real> &A, int t, unsigned ch
     const int n = A.P.n;
     const int i0 = (t % A.g.tiles_x) * TW;
     const int j0 = (t / A.g.tiles_x) * THt;
+#if PDD_CHECKED
+    PDD_CHK(t >= 0 && t < A.g.tiles_x * A.g.tiles_y, 1);
+    if (threadIdx.x == 0) {
+        chk_bounds().lo = (const char *)s_u;
+        chk_bounds().hi = (const char *)(s_u + (PATH == 3 ? 4 * A.g.cstride : (THt + 2 * H) * pitch));
+    }
+    __syncthreads();
+#endif
     // stage tile + halo (coalesced fp64 row reads, held in registers: one consistent snapshot
     // even while neighbouring CTAs of the same round write their tiles), converted relative to
     // V_ref = the tile-centre value (|u| at most half the tile's value range), or with PDD_RAWMIN
@@ -750,7 +793,10 @@ __device__ __forceinline__ void sweep_tile(const KP<real> &A, int t, unsigned ch
             const int r = e / W2, c = e - r * W2;
             const real v = vs[m] < INFINITY ? (real)(vs[m] - Vref) : (real)0;
 #pragma unroll
-            for (int q = 0; q < NCOPY; ++q) s_u[q * A.g.cstride + q + r * pitch + c] = v;
+            for (int q = 0; q < NCOPY; ++q) {
+                PDD_CHK_TILE(s_u + q * A.g.cstride + q + r * pitch + c, 1, 2);
+                s_u[q * A.g.cstride + q + r * pitch + c] = v;
+            }
         }
     }
     if constexpr (PATH == 4) {
@@ -891,6 +937,7 @@ __device__ __forceinline__ void sweep_tile(const KP<real> &A, int t, unsigned ch
             const int e = threadIdx.x + m * NW * 32;
             if (kd[m] != 0) continue;
             const int ly = e / TW, lx = e - ly * TW;
+            PDD_CHK(j0 + ly < n && i0 + lx < n, 5);
             A.V[(int64_t)(j0 + ly) * n + i0 + lx] = Vref + (double)s_u[(ly + H) * pitch + lx + H];
         }
         chg = rmaxv;
@@ -1381,6 +1428,17 @@ cudaError_t launch_sweep(const SweepLaunch &L, cudaStream_t s)
     if (L.precision == 32) return L.check ? dispatch<float, true>(L, s) : dispatch<float, false>(L, s);
     return L.check ? dispatch<double, true>(L, s) : dispatch<double, false>(L, s);
 }
+
+#if PDD_CHECKED
+void dev_faults(unsigned long long *out2, bool add)
+{
+    unsigned long long h[2], z[2] = {};
+    cudaMemcpyFromSymbol(h, g_fault, sizeof h);
+    cudaMemcpyToSymbol(g_fault, z, sizeof z);
+    out2[0] = (add ? out2[0] : 0ull) + h[0];
+    if (!add || out2[1] == 0ull) out2[1] = h[1];
+}
+#endif
 
 #if PDD_TIMING
 void dev_phases(unsigned long long *out8, bool add)
@@ -2096,6 +2154,17 @@ bool rowtab_build_device(const DProblem &P, int napad, int H, int precision, int
 #endif  // !PDD_WIDE_UNIT
 
 }  // namespace pdd
+
+#if PDD_CHECKED && !PDD_WIDE_UNIT
+namespace pdd { namespace wide { void dev_faults(unsigned long long *out2, bool add); } }
+// checked builds only: bounds violations counted by the sweep kernels since the last call
+extern "C" void pdd_dev_faults(unsigned long long *out2)
+{
+    cudaDeviceSynchronize();
+    pdd::dev_faults(out2, false);
+    pdd::wide::dev_faults(out2, true);
+}
+#endif
 
 #if PDD_TIMING && !PDD_WIDE_UNIT
 namespace pdd { namespace wide { void dev_phases(unsigned long long *out8, bool add); } }

@@ -68,6 +68,8 @@ __device__ __forceinline__ real gf_node(const DProblem &P, const real *__restric
             }
             const real tx = x - (real)ix, ty = y - (real)iy;
             const real *pc = base + iy * pitch + ix;
+            PDD_CHK_TILE(pc, 2, 20);
+            PDD_CHK_TILE(pc + pitch, 2, 20);
             const real u00 = pc[0], u10 = pc[1], u01 = pc[pitch], u11 = pc[pitch + 1];
             const real a0 = fma(tx, u10 - u00, u00);
             const real a1 = fma(tx, u11 - u01, u01);

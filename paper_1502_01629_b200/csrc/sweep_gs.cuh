@@ -218,6 +218,8 @@ __device__ __forceinline__ void row_gs4(const KP<float> &A, float *s_u, const fl
 #pragma unroll
             for (int r = 0; r < WY; ++r) {
                 const float *p = src[c] + r * pitch + g;
+                PDD_CHK_TILE(p, NWC > 6 ? 8 : NWC > 4 ? 6 : 4, 10);
+                PDD_CHK(((size_t)p & 15) == 0, 11);
                 const float4 v = *reinterpret_cast<const float4 *>(p);
                 win[r][0] = v.x; win[r][1] = v.y; win[r][2] = v.z; win[r][3] = v.w;
                 if constexpr (NWC > 6) {
@@ -240,6 +242,7 @@ __device__ __forceinline__ void row_gs4(const KP<float> &A, float *s_u, const fl
             }
         }
         const unsigned sk4 = (unsigned)(skip[g >> 6] >> (g & 63)) & 0xfu;   // special nodes of this group
+        PDD_CHK_TILE(oldp + g, 4, 12);
         const float4 o4 = *reinterpret_cast<const float4 *>(oldp + g);
         const float old[4] = {o4.x, o4.y, o4.z, o4.w};
         float nv[4], dlt[4], rd[4];
@@ -294,7 +297,10 @@ __device__ __forceinline__ void row_gs4(const KP<float> &A, float *s_u, const fl
             x = nd == 3 ? nv[3] : x;
             if (!((skip16 >> G) & 1u)) {
                 if (!CHECK) {
-                    if (lane < 16) cptr[g] = x;
+                    if (lane < 16) {
+                        PDD_CHK_TILE(cptr + g, 1, 13);
+                        cptr[g] = x;
+                    }
                 } else if (A.out && lane < 4) {
                     A.out[(int64_t)gj * n + i0 + g + nd] = Vref + (double)x;
                 }
