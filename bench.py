@@ -69,6 +69,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-others", action="store_true",
                     help="skip the time-to-converge report of the other BASELINE configs")
+    ap.add_argument("--no-accuracy-run", action="store_true",
+                    help="skip the fp64 accuracy run of the same pipeline (BASELINE config C5: fp32 with an fp64 accuracy run)")
     ap.add_argument("--oracle-ttc", default="C1,C2",
                     help="configs whose oracle (plain fp64 Jacobi, host cores) time-to-converge is MEASURED "
                          "(cfg or cfg@n, comma separated; C3@1025 takes minutes; '' = none)")
@@ -318,6 +320,32 @@ def main():
     # roofline denominators measured on this box (FFMA and LDS.128 micro-benchmarks of libpdd)
     alu = measure_alu_peaks(5)
 
+    # fp64 accuracy run (BASELINE.json C5: "fp32 with an fp64 accuracy run"): the same pipeline in
+    # fp64 arithmetic on a second context, compared with the fp32 V on the device
+    accuracy = None
+    if not args.no_accuracy_run and rank == 0 and args.precision == 32:
+        N = inst.n * inst.n
+        V32 = torch.empty(N, dtype=torch.float64, device=dev)
+        s.get_values_into(V32, on_device=True)
+        s64 = Solver(inst, precision=64, device=str(dev))
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        st64 = pipeline_step(s64, inst, args)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        V64 = torch.empty(N, dtype=torch.float64, device=dev)
+        s64.get_values_into(V64, on_device=True)
+        vmax = float(V64.abs().max().item())
+        accuracy = {"fp64_pipeline_s": a0.elapsed_time(a1) * 1e-3, "fp64_solve_s": st64["seconds_total"],
+                    "fp64_converged": st64["converged"], "fp64_final_residual": st64["final_residual"],
+                    "fp64_apost_bound": st64["apost_bound"], "fp64_kernel": st64["kernel_used"],
+                    "max_abs_fp32_minus_fp64": float((V32 - V64).abs().max().item()),
+                    "max_abs_V": vmax,
+                    "rel_to_max_V": float((V32 - V64).abs().max().item()) / vmax,
+                    "bar": "north_star: fp32 within 5e-5 max|V| (the fp64 V is within apost_bound of the fixed point)"}
+        s64.close()
+        del s64, V32, V64
+
     # static decomposition on the same kernels (time-to-converge comparison)
     static = None
     if not args.no_static:
@@ -474,6 +502,7 @@ def main():
                                  "sweep_equivalents_patchy": nu / args.steps / inst.free_count()},
             "static": static,
             "decomposition": decomp,
+            "accuracy_run": accuracy,
             "other_configs": others,
             "oracle_time_to_converge": ottc,
             "roofline": roof,

@@ -1343,13 +1343,17 @@ static pdd_status queue_loop(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_st
     // and tiles are revisited before their upstream neighbours moved -- but never more than about a
     // fifth of the grid's tiles: C3's 2145 tiles against 592 resident CTAs want 0.75 waves)
     const char *qe = dev_env("PDD_QW");
-    const int auto_target = std::min(2 * resident, std::max(tiles_free / 5, resident / 2));
+    const int auto_target = dev_env("PDD_QT25")
+        ? std::min(3 * resident, std::max(tiles_free / 25, 3 * resident / 4))
+        : std::min(2 * resident, std::max(tiles_free / 5, resident / 2));
     Q.target = o->queue_target > 0 ? o->queue_target
                                    : std::max(1, qe ? (int)(std::atof(qe) * resident) : auto_target);
     Q.state = ctx->qstate;
-    Q.tol = o->tol;
+    const char *qte = dev_env("PDD_QTOL");  // A/B: queue tolerances / tol (re-queue and activation)
+    const double qtf = qte ? std::atof(qte) : 1.0;
+    Q.tol = o->tol * qtf;
     const char *te = dev_env("PDD_TACT");   // A/B: neighbour-change activation threshold / tol
-    Q.tol_act = o->tol * (te ? std::atof(te) : 1.0);
+    Q.tol_act = o->tol * qtf * (te ? std::atof(te) : 1.0);
     Q.tile_round = ctx->T.tile_round;
     Q.lab_off = ctx->T.tile_lab_off;
     Q.lab_ids = ctx->T.tile_lab_ids;
