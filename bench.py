@@ -339,6 +339,8 @@ def main():
         accuracy = {"fp64_pipeline_s": a0.elapsed_time(a1) * 1e-3, "fp64_solve_s": st64["seconds_total"],
                     "fp64_converged": st64["converged"], "fp64_final_residual": st64["final_residual"],
                     "fp64_apost_bound": st64["apost_bound"], "fp64_kernel": st64["kernel_used"],
+                    "fp64_kernel_node_updates_per_s": st64["node_updates"] / max(st64["seconds_sweep"], 1e-12),
+                    "fp64_sweep_equivalents": st64["node_updates"] / inst.free_count(),
                     "max_abs_fp32_minus_fp64": float((V32 - V64).abs().max().item()),
                     "max_abs_V": vmax,
                     "rel_to_max_V": float((V32 - V64).abs().max().item()) / vmax,
@@ -393,7 +395,8 @@ def main():
     flop_bilinear = inst.n_controls * nbr * 4 * 2
     achieved = flop_per_update * nu / max(t_sweep, 1e-12) / 1e12
     peak32 = alu["fp32_tflops"] if alu["fp32_tflops"] > 0 else FP32_PEAK_TFLOPS
-    peak = peak32 if args.precision == 32 else peak32 / 2.0
+    peak64 = alu["fp64_tflops"] if alu.get("fp64_tflops", 0) > 0 else peak32 / 2.0
+    peak = peak32 if args.precision == 32 else peak64
     roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
             "frac": achieved / peak, "traffic": None,
             "flop_basis": "SURVEY.md 8(d): F = N_A (15 * 2p + 10) per node-update",
@@ -409,12 +412,18 @@ def main():
             "kernel_node_updates_per_s": nu / max(t_sweep, 1e-12),
             "kernel_seconds_share_of_step": t_sweep / max(t_local, 1e-12),
             "peak_basis": ("measured on this GPU: FFMA micro-benchmark of libpdd (pdd_measure_alu_peaks, best "
-                           "of 5; fp64 = half of it); derived figure 148 SM x 128 lanes x 2 x 1.965 GHz = "
+                           "of 5; fp64: its DFMA twin); derived figure 148 SM x 128 lanes x 2 x 1.965 GHz = "
                            "%.1f TFLOP/s" % FP32_PEAK_TFLOPS),
             "peak_derived": FP32_PEAK_TFLOPS if args.precision == 32 else FP64_PEAK_TFLOPS,
             "frac_of_derived_peak": achieved / (FP32_PEAK_TFLOPS if args.precision == 32 else FP64_PEAK_TFLOPS),
-            "smem_peak_tbs_measured": alu["smem_tbs"],
+            "smem_peak_tbs_measured": alu["smem_tbs"], "fp64_peak_tflops_measured": alu.get("fp64_tflops"),
+            "step": {"patchy_fine_solve_s": t_solve / args.steps, "patchy_pipeline_s": t_max / args.steps,
+                     "static_solve_s": static["time_to_converge_s"] if static else None,
+                     "static_over_patchy_pipeline": (static["time_to_converge_s"] / (t_max / args.steps)) if static else None},
             "sweep_launches_per_step": sweep_launches / args.steps}
+    if accuracy:
+        accuracy["fp64_kernel_alu_frac"] = accuracy["fp64_kernel_node_updates_per_s"] * flop_per_update / 1e12 / peak64
+        accuracy["fp64_peak_tflops_measured"] = peak64
     if static:
         # the same kernel in the static solve's full rounds (16 x 128 path-3 tiles at C4/C5,
         # runtime.cu p3_use_wide; the patchy step above runs 32 x 64 tiles)
@@ -446,7 +455,7 @@ def main():
             so = Solver(ci, precision=prec, device=str(dev))
             rec = {"grid": ci.n, "precision": prec, "tol": ci.tol}
             flop_o = ci.n_controls * (15 * (2 * ci.p if ci.p > 0 else 1) + 10)
-            peak_o = peak32 if prec == 32 else peak32 / 2.0
+            peak_o = peak32 if prec == 32 else peak64
             for mode in (("static",) if ci.coarse is None else ("patchy", "static")):
                 pipeline_step(so, ci, args, mode=mode)                       # warm-up
                 torch.cuda.synchronize()

@@ -320,9 +320,12 @@ pdd_status pdd_regime_analyse(double f_min, double f_max, double sigma_norm, dou
 /* Measurement aid (the roofline denominators are measured on the box, not taken
  * from a data sheet).  Runs two micro-benchmarks on the current device and `stream`:
  *   fp32_tflops: dependent-free FFMA chains (8 per thread, every SM full): 2 flop per FFMA lane;
- *   smem_tbs:    conflict-free 16-byte shared-memory loads (LDS.128) from every warp of every SM.
- * Each is the best of `reps` launches timed with CUDA events.  Not part of the hot path. */
-pdd_status pdd_measure_alu_peaks(void *stream, int32_t reps, double *fp32_tflops, double *smem_tbs);
+ *   smem_tbs:    conflict-free 16-byte shared-memory loads (LDS.128) from every warp of every SM;
+ *   fp64_tflops: the same chains with DFMA.
+ * Each is the best of `reps` launches timed with CUDA events (any output may be NULL).  Not part
+ * of the hot path. */
+pdd_status pdd_measure_alu_peaks(void *stream, int32_t reps, double *fp32_tflops, double *smem_tbs,
+                                 double *fp64_tflops);
 
 /* Number of kernels this context has enqueued since pdd_create (all calls). */
 long long pdd_kernel_launches(const pdd_ctx *ctx);

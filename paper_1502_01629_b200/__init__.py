@@ -331,6 +331,6 @@ def regime_analyse(f_min: float, f_max: float, sigma_norm: float, dx: float) -> 
 def measure_alu_peaks(reps: int = 5) -> dict:
     """FP32 FFMA and shared-memory (LDS.128) throughput of the current device, measured by the
     library's micro-benchmarks (pdd_measure_alu_peaks): the roofline denominators of bench.py."""
-    f, m = C.c_double(0.0), C.c_double(0.0)
-    _check(N.lib().pdd_measure_alu_peaks(None, int(reps), C.byref(f), C.byref(m)), None)
-    return {"fp32_tflops": f.value, "smem_tbs": m.value}
+    f, m, d = C.c_double(0.0), C.c_double(0.0), C.c_double(0.0)
+    _check(N.lib().pdd_measure_alu_peaks(None, int(reps), C.byref(f), C.byref(m), C.byref(d)), None)
+    return {"fp32_tflops": f.value, "smem_tbs": m.value, "fp64_tflops": d.value}

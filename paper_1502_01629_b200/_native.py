@@ -134,7 +134,8 @@ def lib():
     L.pdd_fuzzy_scratch_bytes.argtypes = [C.c_int32, C.c_int32, C.POINTER(C.c_size_t)]
     L.pdd_build_fuzzy_patches.argtypes = [ctx, C.c_int32, C.c_double, C.c_double, C.c_int64, vp,
                                           C.c_size_t, C.POINTER(pdd_fuzzy_stats)]
-    L.pdd_measure_alu_peaks.argtypes = [vp, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    L.pdd_measure_alu_peaks.argtypes = [vp, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                        C.POINTER(C.c_double)]
     L.pdd_fuzzy_sparse_scratch_bytes.argtypes = [C.c_int32, C.c_int32, C.POINTER(C.c_size_t)]
     L.pdd_build_fuzzy_patches_sparse.argtypes = [ctx, C.c_int32, C.c_int32, C.c_double, C.c_double,
                                                  C.c_int64, vp, C.c_size_t, C.POINTER(pdd_fuzzy_stats)]

@@ -818,6 +818,21 @@ __global__ void __launch_bounds__(512) k_peak_ffma(float *sink, int iters, float
     if (r == 12345.678f) sink[0] = r;   // never true: keeps the chains alive
 }
 
+__global__ void __launch_bounds__(512) k_peak_dfma(float *sink, int iters, double b, double c)
+{
+    double a0 = threadIdx.x, a1 = a0 + 1., a2 = a0 + 2., a3 = a0 + 3., a4 = a0 + 4., a5 = a0 + 5.,
+           a6 = a0 + 6., a7 = a0 + 7.;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            a0 = fma(a0, b, c); a1 = fma(a1, b, c); a2 = fma(a2, b, c); a3 = fma(a3, b, c);
+            a4 = fma(a4, b, c); a5 = fma(a5, b, c); a6 = fma(a6, b, c); a7 = fma(a7, b, c);
+        }
+    }
+    const double r = ((a0 + a1) + (a2 + a3)) + ((a4 + a5) + (a6 + a7));
+    if (r == 12345.678) sink[0] = (float)r;
+}
+
 __global__ void __launch_bounds__(512) k_peak_lds(float *sink, int iters)
 {
     __shared__ float4 buf[1024];
@@ -842,7 +857,8 @@ __global__ void __launch_bounds__(512) k_peak_lds(float *sink, int iters)
 
 extern "C" {
 
-pdd_status pdd_measure_alu_peaks(void *stream, int32_t reps, double *fp32_tflops, double *smem_tbs)
+pdd_status pdd_measure_alu_peaks(void *stream, int32_t reps, double *fp32_tflops, double *smem_tbs,
+                                 double *fp64_tflops)
 {
     if (reps < 1 || reps > 1000) return fail(nullptr, PDD_E_INVALID, "reps must be in 1..1000");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -855,9 +871,9 @@ pdd_status pdd_measure_alu_peaks(void *stream, int32_t reps, double *fp32_tflops
     CK0(cudaEventCreate(&e0));
     CK0(cudaEventCreate(&e1));
     const int grid = sms * 4, block = 512;
-    double best_f = 0.0, best_l = 0.0;
+    double best_f = 0.0, best_l = 0.0, best_d = 0.0;
     for (int r = 0; r < reps + 1; ++r) {        // the first launch warms up
-        const int it_f = 4096, it_l = 2048;
+        const int it_f = 4096, it_l = 2048, it_d = 1024;
         cudaEventRecord(e0, s);
         k_peak_ffma<<<grid, block, 0, s>>>(sink, it_f, 1.0000001f, 1e-7f);
         cudaEventRecord(e1, s);
@@ -873,6 +889,13 @@ pdd_status pdd_measure_alu_peaks(void *stream, int32_t reps, double *fp32_tflops
         cudaEventElapsedTime(&ms, e0, e1);
         const double by = 16.0 * 8.0 * it_l * (double)grid * block;
         if (r > 0 && ms > 0.f) best_l = std::max(best_l, by / (ms * 1e-3) * 1e-12);
+        cudaEventRecord(e0, s);
+        k_peak_dfma<<<grid, block, 0, s>>>(sink, it_d, 1.0000001, 1e-7);
+        cudaEventRecord(e1, s);
+        cudaEventSynchronize(e1);
+        cudaEventElapsedTime(&ms, e0, e1);
+        const double fd = 2.0 * 64.0 * it_d * (double)grid * block;
+        if (r > 0 && ms > 0.f) best_d = std::max(best_d, fd / (ms * 1e-3) * 1e-12);
     }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
@@ -880,6 +903,7 @@ pdd_status pdd_measure_alu_peaks(void *stream, int32_t reps, double *fp32_tflops
     CK0(cudaGetLastError());
     if (fp32_tflops) *fp32_tflops = best_f;
     if (smem_tbs) *smem_tbs = best_l;
+    if (fp64_tflops) *fp64_tflops = best_d;
     return PDD_OK;
 }
 
@@ -1339,13 +1363,12 @@ static pdd_status queue_loop(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_st
     Q.rank = ctx->qrank;
     Q.n_order = tiles_free;
     // patchy: about two waves of resident CTAs queued or visiting at any time (A/B: PDD_QW)
-    // (measured, profiles/r2e_queue_scan.txt, r2j_c3_target.txt: C5 / C4 want 2 - 3 waves -- fewer
-    // and tiles are revisited before their upstream neighbours moved -- but never more than about a
-    // fifth of the grid's tiles: C3's 2145 tiles against 592 resident CTAs want 0.75 waves)
+    // (measured, profiles/r2e_queue_scan.txt, r2j_c3_target.txt, r2o_target_scan.txt: the best
+    // window is about 1/20 of the grid's tiles -- C5's 33 k tiles want 2.5 - 3 waves of resident
+    // CTAs (with fewer, tiles are revisited before their upstream neighbours moved), C4's 8.4 k
+    // one wave, C3's 2.1 k tiles against 592 CTAs 0.75 waves)
     const char *qe = dev_env("PDD_QW");
-    const int auto_target = dev_env("PDD_QT25")
-        ? std::min(3 * resident, std::max(tiles_free / 25, 3 * resident / 4))
-        : std::min(2 * resident, std::max(tiles_free / 5, resident / 2));
+    const int auto_target = std::min(3 * resident, std::max(tiles_free / 19, 3 * resident / 4));
     Q.target = o->queue_target > 0 ? o->queue_target
                                    : std::max(1, qe ? (int)(std::atof(qe) * resident) : auto_target);
     Q.state = ctx->qstate;
