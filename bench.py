@@ -198,6 +198,20 @@ def oracle_sample(inst, seconds: float):
     return idx.size / dt, desc, O.num_threads(), dt
 
 
+def workload_config(inst, args, world):
+    """The workload both arms are quoted on (BASELINE.json configs[4] by default)."""
+    return {"workload": f"{inst.name}: patchy pipeline (coarse {inst.coarse.n}^2 solve,"
+                        f" synthesis, {inst.n_patches} patch labels, fine solve to "
+                        f"tol {args.tol:g}) on {inst.n}^2",
+            "grid": inst.n, "controls": inst.n_controls, "branches": 2 * inst.p,
+            "patches": inst.n_patches,
+            "k_inner": args.k_inner if args.k_inner is not None else {"patchy": "auto (1)", "static": "auto (4)"},
+            "schedule": "work queue (persistent sweep CTAs, key-order admission), then full-grid verification",
+            "path3_tile": {"patchy": "32x64", "static": "16x128" if 128 * inst.dx <= 0.125 + 1e-12 else "32x64"},
+            "l2": "inputs larger than L2 (V fp64 %d MB)" % (inst.n * inst.n * 8 >> 20),
+            "parallelism": f"replicas x{world}" if world > 1 else "single GPU"}
+
+
 def run_reference(args, world, rank):
     import pdd_inputs as I
     import oracle as O
@@ -218,8 +232,9 @@ def run_reference(args, world, rank):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{inst.name}: oracle operator application on a row band",
-                   "grid": inst.n, "controls": inst.n_controls, "branches": 2 * inst.p},
+        # the same workload as our arm; each step is a bounded sample of it (cpu_baseline.sample):
+        # the oracle's node-update rate on the fine grid of that config
+        "config": workload_config(inst, args, world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": thr, "kind": "oracle",
                          "sample": desc},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -495,15 +510,7 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32" if args.precision == 32 else "f64", "data": "synthetic",
-            "config": {"workload": f"{inst.name}: patchy pipeline (coarse {inst.coarse.n}^2 solve,"
-                                   f" synthesis, {inst.n_patches} patch labels, fine solve to "
-                                   f"tol {args.tol:g}) on {inst.n}^2",
-                       "grid": inst.n, "controls": inst.n_controls, "branches": 2 * inst.p,
-                       "patches": inst.n_patches, "k_inner": args.k_inner if args.k_inner is not None else {"patchy": "auto (1)", "static": "auto (4)"},
-                       "schedule": "work queue (persistent sweep CTAs, key-order admission), then full-grid verification",
-                       "path3_tile": {"patchy": "32x64", "static": "16x128" if 128 * inst.dx <= 0.125 + 1e-12 else "32x64"},
-                       "l2": "inputs larger than L2 (V fp64 %d MB)" % (inst.n * inst.n * 8 >> 20),
-                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+            "config": workload_config(inst, args, world),
             "time_to_converge": {"patchy_s": t_solve / args.steps,
                                  "patchy_pipeline_s": t_max / args.steps,
                                  "static_s": static["time_to_converge_s"] if static else None,
