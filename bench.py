@@ -207,7 +207,8 @@ def workload_config(inst, args, world):
             "patches": inst.n_patches,
             "k_inner": args.k_inner if args.k_inner is not None else {"patchy": "auto (1)", "static": "auto (4)"},
             "schedule": "work queue (persistent sweep CTAs, key-order admission), then full-grid verification",
-            "path3_tile": {"patchy": "32x64", "static": "16x128" if 128 * inst.dx <= 0.125 + 1e-12 else "32x64"},
+            "path3_tile": {"patchy": "16x64" if ((inst.n + 63) // 64) * ((inst.n + 31) // 32) <= 16384 else "32x64",
+                           "static": "16x128" if 128 * inst.dx <= 0.125 + 1e-12 else "32x64"},
             "l2": "inputs larger than L2 (V fp64 %d MB)" % (inst.n * inst.n * 8 >> 20),
             "parallelism": f"replicas x{world}" if world > 1 else "single GPU"}
 

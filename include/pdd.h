@@ -118,10 +118,11 @@ typedef struct {
                             per tile with free nodes)                                      */
     double delta;        /* patchy bucket width in value units; 0 = automatic; < 0 = off      */
     int32_t kernel;      /* 0 auto, 1 general stencil, 2 row-table stencil, 3 row-table one
-                            node per warp step (A/B only).  The fp32 row-table kernel's tile
-                            is 32 x 64 nodes, or 16 x 128 for static solves on grids where
-                            128 dx <= 1/8 (pdd_set_tile_cols forces one
-                            geometry)                                                        */
+                            node per warp step (A/B only), 4 lean general stencil.  The
+                            fp32 row-table kernel's tile is 32 x 64 nodes, 16 x 64 for patchy
+                            solves on grids of up to 16 k tiles, 16 x 128 for static solves
+                            where 128 dx <= 1/8 (pdd_set_tile_shape
+                            forces one geometry)                                             */
     int32_t schedule;    /* 0 automatic (= 2);
                             1 ordered: Gauss-Seidel passes over the tiles in key order (u_hat
                             for patchy, block-lexicographic for static), each tile waiting for
@@ -289,8 +290,11 @@ pdd_status pdd_get_patch_residuals(pdd_ctx *ctx, double *dst, int32_t count);
 pdd_status pdd_get_tile_rounds(pdd_ctx *ctx, int32_t *dst, int32_t count);
 
 /* Force the fp32 row-table kernel's tile geometry for the following solves / operator
- * applications: 0 automatic, 64 (32 x 64 tiles) or 128 (16 x 128).  For A/B
- * measurements and the forced-geometry parity tests; PDD_E_INVALID for any other value. */
+ * applications: rows x cols = 0 x 0 automatic (16 x 64 for patchy solves on
+ * grids of up to 16 k tiles, 16 x 128 for static solves where 128 dx <= 1/8, else 32 x 64), or
+ * 32 x 64, 16 x 128, 16 x 64.  For A/B measurements and the forced-geometry parity tests;
+ * PDD_E_INVALID for any other value.  pdd_set_tile_cols(cols): 0, 64 (32 x 64) or 128 (16 x 128). */
+pdd_status pdd_set_tile_shape(pdd_ctx *ctx, int32_t rows, int32_t cols);
 pdd_status pdd_set_tile_cols(pdd_ctx *ctx, int32_t cols);
 
 /* The upwind diffusion ball analysis of P:528-697 (host arithmetic, no context, no GPU).

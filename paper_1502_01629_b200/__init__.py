@@ -303,6 +303,10 @@ class Solver:
         """Force the fp32 row-table tile geometry (0 auto, 64 or 128; A/B and tests)."""
         self._ck(N.lib().pdd_set_tile_cols(self._ctx, int(cols)))
 
+    def set_tile_shape(self, rows: int, cols: int) -> None:
+        """Force the fp32 row-table kernel's tile: (0, 0) automatic, (32, 64), (16, 128), (16, 64)."""
+        self._ck(N.lib().pdd_set_tile_shape(self._ctx, int(rows), int(cols)))
+
     def kernel_launches(self) -> int:
         return int(N.lib().pdd_kernel_launches(self._ctx))
 

@@ -19,12 +19,14 @@ LIB = os.path.join(HERE, "libpdd.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",
           "-I", os.path.join(ROOT, "include"), "-Xptxas", "-v"]
-# (object, source, extra flags): sweep.cu is compiled twice, the second time as the 16 x 128
-# path-3 tile in namespace pdd::wide (runtime.cu picks the geometry per problem)
+# (object, source, extra flags): sweep.cu is compiled three times: the 32 x 64 path-3 tile, the
+# 16 x 128 one in namespace pdd::wide and the 16 x 64 one in pdd::low (runtime.cu picks the geometry
+# per problem)
 UNITS = [
     ("canonical.o", "canonical.cu", ["--fmad=false"]),
     ("sweep.o", "sweep.cu", []),
     ("sweep_wide.o", "sweep.cu", ["-DPDD_P3_WIDE=1", "-DPDD_WIDE_UNIT=1"]),
+    ("sweep_low.o", "sweep.cu", ["-DPDD_P3_TH=16", "-DPDD_LOW_UNIT=1"]),
     ("runtime.o", "runtime.cu", []),
 ]
 

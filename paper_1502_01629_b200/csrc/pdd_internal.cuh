@@ -334,6 +334,10 @@ void gf_geometry(int &pitch);      // compile-time shared-memory pitch of path 4
 cudaError_t launch_sweep_wide(const SweepLaunch &L, cudaStream_t s);
 void p3_geometry_wide(int &pitch, int &cstride, int &hmax);
 void p3_tile_wide(int &tw, int &th);
+// the 16 x 64 path-3 tile (sweep.cu built with PDD_LOW_UNIT=1, PDD_P3_TH=16)
+cudaError_t launch_sweep_low(const SweepLaunch &L, cudaStream_t s);
+void p3_geometry_low(int &pitch, int &cstride, int &hmax);
+void p3_tile_low(int &tw, int &th);
 // Build the row-stencil table on the device; false if no supported window fits.
 bool rowtab_build_device(const DProblem &P, int napad, int H, int precision, int *scratch,
                          void *tab, size_t tab_bytes, int &WY, int &WX, int &oxmin, int &oxmax,

@@ -169,7 +169,8 @@ struct pdd_ctx {
     TileGeom g{};
     int n_tiles = 0;
     int prepared_kernel = -1;
-    bool prepared_wide = false;      // path-3 tile of the prepared geometry (p3_use_wide)
+    int prepared_geo = -1;           // path-3 tile of the prepared geometry (p3_geometry_choice)
+    int force_tile_rows = 0;         // pdd_set_tile_shape: 0 auto, 16 or 32
     int force_tile_cols = 0;         // pdd_set_tile_cols: 0 auto, 64 or 128
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     cudaEvent_t evp[2][64] = {};  // per-round sweep-kernel timing inside a batch (lazy)
@@ -1043,12 +1044,19 @@ static bool row_uniform(const pdd_problem *p)
 // the u_hat front do fewer wasted updates on the finer 32 x 64 tiles (measured C5 pipeline
 // 182 vs 188 ms, C4 the same), the static rounds gain the kernel's throughput (C5 0.78 vs
 // 1.07 s).  PDD_P3_TILE=64|128 in the environment forces one geometry (A/B measurements).
-static bool p3_use_wide(const pdd_problem *p, bool patchy, int force_cols)
+// geometry codes: 0 = 32 x 64, 1 = 16 x 128 (wide), 2 = 16 x 64 (low)
+static int p3_geometry_choice(const pdd_problem *p, bool patchy, int force_cols, int force_rows)
 {
-    if (force_cols == 64) return false;    // pdd_set_tile_cols (A/B runs, forced-geometry tests)
-    if (force_cols == 128) return true;
+    if (force_cols == 64) return force_rows == 16 ? 2 : 0;   // pdd_set_tile_shape (A/B runs, tests)
+    if (force_cols == 128) return 1;
     const double dx = (p->hi - p->lo) / (p->n - 1);
-    return !patchy && 128.0 * dx <= 0.125 + 1e-12;
+    if (!patchy) return 128.0 * dx <= 0.125 + 1e-12 ? 1 : 0;
+    // patchy: 16 x 64 tiles waste fewer updates along the u_hat front (a tile stays in the window
+    // until the front has crossed it) at a lower kernel rate (2 rows per warp: the row pipeline
+    // fills and drains in 46 steps for 32 of work).  Measured (profiles/r2t_tile16_ab.txt): C4
+    // fine solve 0.063 -> 0.051 s, C2 5 -> 3 ms, C5 0.097 -> 0.101 s: taken up to 16 k tiles.
+    const int64_t tiles = (int64_t)((p->n + 63) / 64) * ((p->n + 31) / 32);
+    return tiles <= 16384 ? 2 : 0;
 }
 
 // The lean general-stencil kernel (path 4, sweep_gf.cuh) covers f = c(x) a + d(x) with any speed /
@@ -1067,8 +1075,9 @@ static bool fast_general_ok(const pdd_problem *p)
 static pdd_status prepare(pdd_ctx *ctx, int kernel_req, bool patchy, bool queue_ok)
 {
     const pdd_problem *p = &ctx->fine;   // sizes only: its host arrays are gone (pdd_create)
-    const bool want_wide = p3_use_wide(p, patchy, ctx->force_tile_cols);
-    if (ctx->prepared_kernel == kernel_req && ctx->prepared_wide == want_wide &&
+    const int want_geo = p3_geometry_choice(p, patchy, ctx->force_tile_cols, ctx->force_tile_rows);
+    const bool want_wide = want_geo == 1;
+    if (ctx->prepared_kernel == kernel_req && ctx->prepared_geo == want_geo &&
         ctx->prepared_queue_ok == queue_ok)
         return PDD_OK;
     const DProblem &d = ctx->F.d;
@@ -1116,6 +1125,10 @@ static pdd_status prepare(pdd_ctx *ctx, int kernel_req, bool patchy, bool queue_
         p3_tile_wide(tw3, th3);
         p3_geometry_wide(p3_pitch, p3_cstride, p3_hmax);
         if (H > p3_hmax) return fail(ctx, PDD_E_STENCIL, "wide path-3 tile: halo %d too large", H);
+    } else if (g4 && want_geo == 2) {
+        p3_tile_low(tw3, th3);
+        p3_geometry_low(p3_pitch, p3_cstride, p3_hmax);
+        if (H > p3_hmax) return fail(ctx, PDD_E_STENCIL, "16 x 64 path-3 tile: halo %d too large", H);
     }
     g.TW = (path == 2 && !g4) ? rowtab_tw(WY, WX) : (g4 ? tw3 : 64);
     g.TH = g4 ? th3 : sweep_tile_rows();
@@ -1149,7 +1162,7 @@ static pdd_status prepare(pdd_ctx *ctx, int kernel_req, bool patchy, bool queue_
     for (int t = 0; t < ctx->n_tiles; ++t) all[t] = t;
     CK(cudaMemcpy(ctx->T.all_list, all.data(), sizeof(int32_t) * all.size(), cudaMemcpyHostToDevice));
     ctx->prepared_kernel = kernel_req;
-    ctx->prepared_wide = want_wide;
+    ctx->prepared_geo = want_geo;
     ctx->prepared_queue_ok = queue_ok;
     return PDD_OK;
 }
@@ -1796,12 +1809,22 @@ pdd_status pdd_get_tile_rounds(pdd_ctx *ctx, int32_t *dst, int32_t count)
     return PDD_OK;
 }
 
+pdd_status pdd_set_tile_shape(pdd_ctx *ctx, int32_t rows, int32_t cols)
+{
+    if (!ctx) return fail(nullptr, PDD_E_INVALID, "ctx is NULL");
+    const bool ok = (rows == 0 && cols == 0) || (rows == 32 && cols == 64) || (rows == 16 && cols == 128) ||
+                    (rows == 16 && cols == 64);
+    if (!ok) return fail(ctx, PDD_E_INVALID, "tile shape must be 0 x 0 (automatic), 32 x 64, 16 x 128 or 16 x 64");
+    ctx->force_tile_cols = cols;
+    ctx->force_tile_rows = rows;
+    return PDD_OK;
+}
+
 pdd_status pdd_set_tile_cols(pdd_ctx *ctx, int32_t cols)
 {
     if (!ctx) return fail(nullptr, PDD_E_INVALID, "ctx is NULL");
     if (cols != 0 && cols != 64 && cols != 128) return fail(ctx, PDD_E_INVALID, "tile cols must be 0, 64 or 128");
-    ctx->force_tile_cols = cols;
-    return PDD_OK;
+    return pdd_set_tile_shape(ctx, cols == 64 ? 32 : cols == 128 ? 16 : 0, cols);
 }
 
 static pdd_status fetch(pdd_ctx *ctx, void *dst, const void *src, size_t bytes, int on_device)

@@ -43,10 +43,18 @@
 #ifndef PDD_WIDE_UNIT
 #define PDD_WIDE_UNIT 0
 #endif
+// PDD_LOW_UNIT: a third build with PDD_P3_TH=16 gives the 16 x 64 path-3 tile in namespace pdd::low
+// (patchy solves on grids of up to ~16 k tiles: fewer wasted updates along the u_hat front)
+#ifndef PDD_LOW_UNIT
+#define PDD_LOW_UNIT 0
+#endif
+#define PDD_ALT_UNIT (PDD_WIDE_UNIT || PDD_LOW_UNIT)
 
 namespace pdd {
 #if PDD_WIDE_UNIT
 namespace wide {
+#elif PDD_LOW_UNIT
+namespace low {
 #endif
 
 #ifndef PDD_MIN_BLOCKS
@@ -1410,7 +1418,7 @@ void p3_geometry(int &pitch, int &cstride, int &hmax)
     hmax = P3_HMAX;
 }
 
-#if !PDD_WIDE_UNIT
+#if !PDD_ALT_UNIT
 void gf_geometry(int &pitch) { pitch = GF_PITCH; }
 #endif
 
@@ -1422,8 +1430,9 @@ void p3_tile(int &tw, int &th)
 
 cudaError_t launch_sweep(const SweepLaunch &L, cudaStream_t s)
 {
-#if !PDD_WIDE_UNIT
+#if !PDD_ALT_UNIT
     if (L.path == 3 && L.g.TW == 128) return launch_sweep_wide(L, s);
+    if (L.path == 3 && L.g.TH == 16) return launch_sweep_low(L, s);
 #endif
     if (L.precision == 32) return L.check ? dispatch<float, true>(L, s) : dispatch<float, false>(L, s);
     return L.check ? dispatch<double, true>(L, s) : dispatch<double, false>(L, s);
@@ -1457,6 +1466,13 @@ static_assert(TW3 == 128, "the wide unit is built with PDD_P3_WIDE=1");
 cudaError_t launch_sweep_wide(const SweepLaunch &L, cudaStream_t s) { return wide::launch_sweep(L, s); }
 void p3_geometry_wide(int &pitch, int &cstride, int &hmax) { wide::p3_geometry(pitch, cstride, hmax); }
 void p3_tile_wide(int &tw, int &th) { wide::p3_tile(tw, th); }
+#elif PDD_LOW_UNIT
+static_assert(TW3 == 64 && TH3 == 16, "the low unit is built with PDD_P3_TH=16");
+}  // namespace low
+
+cudaError_t launch_sweep_low(const SweepLaunch &L, cudaStream_t s) { return low::launch_sweep(L, s); }
+void p3_geometry_low(int &pitch, int &cstride, int &hmax) { low::p3_geometry(pitch, cstride, hmax); }
+void p3_tile_low(int &tw, int &th) { low::p3_tile(tw, th); }
 #else
 // ------------------------------------------------------------------ tile bookkeeping
 __global__ void k_tile_init(DProblem P, TileGeom g, const double *uhat, const int16_t *labels,
@@ -2151,28 +2167,32 @@ bool rowtab_build_device(const DProblem &P, int napad, int H, int precision, int
     return true;
 }
 
-#endif  // !PDD_WIDE_UNIT
+#endif  // !PDD_ALT_UNIT
 
 }  // namespace pdd
 
-#if PDD_CHECKED && !PDD_WIDE_UNIT
+#if PDD_CHECKED && !PDD_ALT_UNIT
 namespace pdd { namespace wide { void dev_faults(unsigned long long *out2, bool add); } }
+namespace pdd { namespace low { void dev_faults(unsigned long long *out2, bool add); } }
 // checked builds only: bounds violations counted by the sweep kernels since the last call
 extern "C" void pdd_dev_faults(unsigned long long *out2)
 {
     cudaDeviceSynchronize();
     pdd::dev_faults(out2, false);
     pdd::wide::dev_faults(out2, true);
+    pdd::low::dev_faults(out2, true);
 }
 #endif
 
-#if PDD_TIMING && !PDD_WIDE_UNIT
+#if PDD_TIMING && !PDD_ALT_UNIT
 namespace pdd { namespace wide { void dev_phases(unsigned long long *out8, bool add); } }
+namespace pdd { namespace low { void dev_phases(unsigned long long *out8, bool add); } }
 // development builds only: cycles per visit phase summed over all CTAs since the last call
 extern "C" void pdd_dev_phases(unsigned long long *out8)
 {
     cudaDeviceSynchronize();
     pdd::dev_phases(out8, false);
     pdd::wide::dev_phases(out8, true);
+    pdd::low::dev_phases(out8, true);
 }
 #endif

@@ -14,7 +14,7 @@ ap.add_argument("--general", default=None, help="cost:sigma:n:eps:n_coarse (gene
 ap.add_argument("--prec", type=int, default=32); ap.add_argument("--k", default="0")
 ap.add_argument("--modes", default="patchy,static"); ap.add_argument("--tol", type=float, default=1e-6)
 ap.add_argument("--kernel", type=int, default=0); ap.add_argument("--delta", default="0")
-ap.add_argument("--max_rounds", type=int, default=200000); ap.add_argument("--schedule", default="rounds"); ap.add_argument("--policy", type=int, default=0); ap.add_argument("--qt", type=int, default=0)
+ap.add_argument("--max_rounds", type=int, default=200000); ap.add_argument("--schedule", default="rounds"); ap.add_argument("--policy", type=int, default=0); ap.add_argument("--qt", type=int, default=0); ap.add_argument("--cols", type=int, default=0)
 a = ap.parse_args()
 t = time.time()
 if a.paper:
@@ -28,6 +28,7 @@ else:
 print("gen", time.time() - t, flush=True)
 t = time.time(); s = Solver(inst, precision=a.prec); torch.cuda.synchronize(); print("create", time.time() - t, flush=True)
 cs = s.coarse_solve(inst.tol_coarse); print("coarse", cs, flush=True)
+if a.cols: s.set_tile_cols(a.cols)
 t = time.time(); s.synthesize(); s.build_patches(inst.n_patches); print("synth+patches", time.time() - t, flush=True)
 for mode in a.modes.split(","):
     if mode == "static": s.build_static(*inst.static_blocks)

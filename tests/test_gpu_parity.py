@@ -193,29 +193,36 @@ def test_schedules_reach_the_same_fixed_point(mode, schedule, policy):
     assert np.abs(s.get_values() - ref["V"]).max() <= 5e-5 * np.abs(ref["V"]).max()
 
 
-# The 16 x 128 path-3 tile (sweep.cu's second build, pdd::wide) is chosen automatically only on
-# fine grids (runtime.cu p3_use_wide: C4, C5 full size, covered by test_gpu_fullsize.py); here
-# pdd_set_tile_cols(128) forces it on small grids with ragged tails in both directions.
+# The fp32 row-table kernel comes in three tile geometries (sweep.cu is built three times: 32 x 64,
+# 16 x 128 in pdd::wide, 16 x 64 in pdd::low); the automatic choice (runtime.cu
+# p3_geometry_choice) takes 16 x 64 for patchy solves up to 16 k tiles, 16 x 128 for static solves
+# on fine grids (C4, C5 full size, covered by test_gpu_fullsize.py), else 32 x 64.  Here
+# pdd_set_tile_shape forces each of them on small grids with ragged tails in both directions.
+SHAPES = [(16, 128), (16, 64), (32, 64)]
+
+
 @pytest.mark.parametrize("cfg,n", [("C2", 201), ("C4", 257), ("C5", 257), ("C5", 300)])
 @pytest.mark.parametrize("kernel", [0, 2])
-def test_wide_tile_operator_parity(cfg, n, kernel):
+@pytest.mark.parametrize("shape", SHAPES)
+def test_forced_tile_operator_parity(cfg, n, kernel, shape):
     inst = I.make_config(cfg, n=n)
     V = _random_field(inst, 5)
     ref, _ = O.apply(inst, V)
     s = _solver(inst, 32)
-    s.set_tile_cols(128)
+    s.set_tile_shape(*shape)
     out, res = s.apply_operator(V, kernel=kernel)
     assert np.abs(out - ref).max() < 2e-6 * np.abs(V).max()
     assert abs(res - np.abs(ref - V)[inst.kind == 0].max()) < 4e-6
 
 
 @pytest.mark.parametrize("mode", ["patchy", "static"])
-def test_wide_tile_solve_parity(mode):
+@pytest.mark.parametrize("shape", SHAPES)
+def test_forced_tile_solve_parity(mode, shape):
     # tol 1e-6: on a 513^2 grid the wide tile spans 1 in x and its fp32 noise floor sits near 1e-7
     inst = I.make_config("C5", n=513)
     ref = O.jacobi(inst, tol=_tight_tol(inst, 2e-11), max_sweeps=10**6)
     s = _solver(inst, 32)
-    s.set_tile_cols(128)
+    s.set_tile_shape(*shape)
     if mode == "patchy":
         s.coarse_solve(inst.tol_coarse)
         s.synthesize()
@@ -224,8 +231,23 @@ def test_wide_tile_solve_parity(mode):
         s.build_static(*inst.static_blocks)
     st = s.solve(mode, tol=1e-6, k_inner=4)
     assert st["converged"] == 1
+    assert (st["tile_rows"], st["tile_cols"]) == shape
     V = s.get_values()
     assert np.abs(V - ref["V"]).max() <= 5e-5 * np.abs(ref["V"]).max()
+
+
+def test_automatic_tile_shapes():
+    """16 x 64 for a patchy solve on a small grid, 32 x 64 for its static solve (128 dx > 1/8)."""
+    inst = I.make_config("C2")
+    s = _solver(inst, 32)
+    s.coarse_solve(inst.tol_coarse)
+    s.synthesize()
+    s.build_patches(inst.n_patches)
+    st = s.solve("patchy", tol=1e-7)
+    assert (st["tile_rows"], st["tile_cols"]) == (16, 64)
+    s.build_static(*inst.static_blocks)
+    st = s.solve("static", tol=1e-7)
+    assert (st["tile_rows"], st["tile_cols"]) == (32, 64)
 
 
 def test_ordered_static_with_tiles_without_free_nodes():
