@@ -76,9 +76,15 @@ namespace low {
 template <int PATH>
 constexpr int min_blocks() { return PDD_MIN_BLOCKS > 0 ? PDD_MIN_BLOCKS : (PATH == 3 ? PDD_MIN_BLOCKS3 : PATH == 1 ? PDD_MIN_BLOCKS1 : PATH == 4 ? PDD_MIN_BLOCKS4 : 1); }
 #ifndef PDD_TH
-#define PDD_TH 32           // tile rows (multiple of NW)
+#define PDD_TH 16           // tile rows of the general / fp64 kernels (paths 1, 2, 4; multiple of NW).
+                            // 16 since round 2: under the work queue smaller tiles waste fewer
+                            // updates along the front and fill the GPU on mid-size grids (measured,
+                            // profiles/r2w_general_tile16_ab.txt: C3 patchy fine solve 49 -> 35 ms,
+                            // static 141 -> 118 ms; C5@2049 fp64 patchy 0.249 -> 0.165 s; the
+                            // paper's 800^2 workloads within 2 %)
 #endif
 constexpr int TH = PDD_TH;      // tile rows
+constexpr int PROG_N = 32;      // row-pipeline progress counters per CTA: the tallest tile (32 x 64)
 #ifndef PDD_NW
 #define PDD_NW 8
 #endif
@@ -717,8 +723,8 @@ __device__ __forceinline__ void sweep_tile(const KP<real> &A, int t, unsigned ch
     constexpr int THt = PATH == 3 ? TH3 : TH;      // tile rows of this path
     constexpr int NCOPY = PATH == 3 ? 4 : 1;
     double *s_red = reinterpret_cast<double *>(smem_raw);            // NW
-    volatile int *s_prog = reinterpret_cast<volatile int *>(s_red + NW);   // TH progress counters
-    real *s_ctrl = reinterpret_cast<real *>(s_red + NW + TH / 2);     // 2 * 128
+    volatile int *s_prog = reinterpret_cast<volatile int *>(s_red + NW);   // PROG_N progress counters
+    real *s_ctrl = reinterpret_cast<real *>(s_red + NW + PROG_N / 2);   // 2 * 128
     real *s_u = s_ctrl + 256;
     const int H = A.g.H, pitch = A.g.pitch;
     const int n = A.P.n;
@@ -1149,7 +1155,7 @@ template <typename real, int PATH>
 __host__ __device__ constexpr size_t sweep_smem_base(int H, int pitch, int cstride)
 {
     // path 4: cstride carries the size of the coefficient planes, 128 reals of h m(a) follow
-    return NW * sizeof(double) + TH * sizeof(int) + 256 * sizeof(real) +
+    return NW * sizeof(double) + PROG_N * sizeof(int) + 256 * sizeof(real) +
            (PATH == 3 ? (size_t)4 * cstride
                       : (size_t)(TH + 2 * H) * pitch + (PATH == 4 ? (size_t)cstride + 128 : 0)) * sizeof(real);
 }

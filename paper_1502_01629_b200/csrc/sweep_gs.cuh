@@ -106,6 +106,7 @@ constexpr int p3_cstride_of(int th, int pitch)
 constexpr int P3_PITCH = p3_pitch_of(TW3);
 constexpr int P3_CSTRIDE = p3_cstride_of(TH3, P3_PITCH);
 static_assert(TW3 == 64 || TW3 == 128, "path-3 tile width");
+static_assert(TH3 <= 32 && PDD_TH <= 32, "PROG_N progress counters per CTA");
 
 // per-row masks for up to 128 columns: bit lx of word lx >> 6
 __device__ __forceinline__ void row_masks128(const DProblem &P, int TW, int i0, int gj, int Hx,
