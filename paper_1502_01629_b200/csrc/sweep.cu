@@ -1288,13 +1288,16 @@ static cudaError_t launch_one(const SweepLaunch &L, cudaStream_t s)
                             ? ((smem_base + 15) & ~(size_t)15) +
                                   sizeof(double) * (size_t)(th_ + 2 * L.g.H) * (tw_ + 2 * L.g.H)
                             : smem_base;
+    // (the opt-in for large dynamic shared memory is taken from 40 KB on: the kernels' static shared
+    // memory -- up to 4 KB for the per-patch residual table of check launches -- counts against
+    // the 48 KB default limit too)
     // path 4 is built for the work queue and for check launches only
     if constexpr (PATH == 4 && !CHECK) {
         if (!L.queued) return cudaErrorInvalidValue;
     }
     if constexpr (PATH != 4) if (L.ordered && !CHECK) {
         auto kern = k_sweep_ordered<real, PATH, CPL, WY, WX>;
-        if (smem > 48 * 1024) {
+        if (smem > 40 * 1024) {
             cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)smem);
             if (e != cudaSuccess) return e;
@@ -1313,7 +1316,7 @@ static cudaError_t launch_one(const SweepLaunch &L, cudaStream_t s)
     }
     if (L.queued && !CHECK) {
         auto kern = k_sweep_queue<real, PATH, CPL, WY, WX>;
-        if (smem > 48 * 1024) {
+        if (smem > 40 * 1024) {
             cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)smem);
             if (e != cudaSuccess) return e;
@@ -1340,7 +1343,7 @@ static cudaError_t launch_one(const SweepLaunch &L, cudaStream_t s)
         cudaGetDevice(&dev);
         int per_sm = 0, sms = 0;
         if (dev >= kMaxDev || per_sm_dev[dev] == 0) {
-            if (smem > 48 * 1024) {
+            if (smem > 40 * 1024) {
                 cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                      (int)smem);
                 if (e != cudaSuccess) return e;
@@ -1366,7 +1369,7 @@ static cudaError_t launch_one(const SweepLaunch &L, cudaStream_t s)
     }
     if constexpr (PATH != 4 || CHECK) {
         auto kern = k_sweep<real, PATH, CPL, WY, WX, CHECK>;
-        if (smem > 48 * 1024) {
+        if (smem > 40 * 1024) {
             cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)smem);
             if (e != cudaSuccess) return e;
