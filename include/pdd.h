@@ -295,6 +295,11 @@ pdd_status pdd_get_tile_rounds(pdd_ctx *ctx, int32_t *dst, int32_t count);
  * 32 x 64, 16 x 128, 16 x 64.  For A/B measurements and the forced-geometry parity tests;
  * PDD_E_INVALID for any other value.  pdd_set_tile_cols(cols): 0, 64 (32 x 64) or 128 (16 x 128). */
 pdd_status pdd_set_tile_shape(pdd_ctx *ctx, int32_t rows, int32_t cols);
+/* The automatic choice above for a fine grid of n nodes per side on [lo, hi]^2 (host arithmetic,
+ * no context, no GPU): rows x cols of the fp32 row-table kernel's tile for a patchy (1) or static
+ * (0) solve. */
+pdd_status pdd_choose_tile_shape(int32_t n, double lo, double hi, int32_t patchy, int32_t *rows,
+                                 int32_t *cols);
 pdd_status pdd_set_tile_cols(pdd_ctx *ctx, int32_t cols);
 
 /* The upwind diffusion ball analysis of P:528-697 (host arithmetic, no context, no GPU).

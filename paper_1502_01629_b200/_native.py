@@ -31,7 +31,7 @@ EXPORTS = ["pdd_version", "pdd_workspace_bytes", "pdd_create", "pdd_coarse_solve
            "pdd_apply_operator", "pdd_get_values", "pdd_set_values", "pdd_get_uhat",
            "pdd_get_coarse_values", "pdd_get_controls", "pdd_get_labels", "pdd_get_successors",
            "pdd_get_patch_rounds", "pdd_get_patch_residuals", "pdd_get_tile_rounds",
-           "pdd_set_tile_cols", "pdd_set_tile_shape", "pdd_kernel_launches", "pdd_last_error", "pdd_destroy",
+           "pdd_set_tile_cols", "pdd_set_tile_shape", "pdd_choose_tile_shape", "pdd_kernel_launches", "pdd_last_error", "pdd_destroy",
            "pdd_regime_analyse", "pdd_fuzzy_scratch_bytes", "pdd_build_fuzzy_patches",
            "pdd_fuzzy_sparse_scratch_bytes", "pdd_build_fuzzy_patches_sparse", "pdd_measure_alu_peaks"]
 
@@ -132,6 +132,8 @@ def lib():
     L.pdd_get_tile_rounds.argtypes = [ctx, vp, C.c_int32]
     L.pdd_set_tile_cols.argtypes = [ctx, C.c_int32]
     L.pdd_set_tile_shape.argtypes = [ctx, C.c_int32, C.c_int32]
+    L.pdd_choose_tile_shape.argtypes = [C.c_int32, C.c_double, C.c_double, C.c_int32,
+                                        C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
     L.pdd_fuzzy_scratch_bytes.argtypes = [C.c_int32, C.c_int32, C.POINTER(C.c_size_t)]
     L.pdd_build_fuzzy_patches.argtypes = [ctx, C.c_int32, C.c_double, C.c_double, C.c_int64, vp,
                                           C.c_size_t, C.POINTER(pdd_fuzzy_stats)]

@@ -1820,6 +1820,21 @@ pdd_status pdd_set_tile_shape(pdd_ctx *ctx, int32_t rows, int32_t cols)
     return PDD_OK;
 }
 
+pdd_status pdd_choose_tile_shape(int32_t n, double lo, double hi, int32_t patchy, int32_t *rows,
+                                 int32_t *cols)
+{
+    if (n < 3 || !(hi > lo) || !rows || !cols)
+        return fail(nullptr, PDD_E_INVALID, "pdd_choose_tile_shape: need n >= 3, hi > lo and output pointers");
+    pdd_problem p{};
+    p.n = n;
+    p.lo = lo;
+    p.hi = hi;
+    const int geo = p3_geometry_choice(&p, patchy != 0, 0, 0);
+    *rows = geo == 0 ? 32 : 16;
+    *cols = geo == 1 ? 128 : 64;
+    return PDD_OK;
+}
+
 pdd_status pdd_set_tile_cols(pdd_ctx *ctx, int32_t cols)
 {
     if (!ctx) return fail(nullptr, PDD_E_INVALID, "ctx is NULL");

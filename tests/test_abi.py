@@ -141,3 +141,26 @@ def test_boundary_side_sectors_split_the_ring_evenly():
     assert set(grid[1:-1, 0]) == {2} and set(grid[1:-1, -1]) == {0}      # left / right sides
     one = I.boundary_side_sectors(n, ring, 1)
     assert set(one[ring]) == {0} and np.all(one[~ring] == -1)
+
+
+def test_automatic_tile_shape_rule(lib):
+    """Host logic of the fp32 row-table tile choice: 16 x 64 for patchy solves
+    on grids of up to 16 k tiles (C2, C4), 32 x 64 above (C5); static solves take 16 x 128 where
+    128 dx <= 1/8 (C4, C5 at full size), else 32 x 64."""
+    import ctypes as C
+    import pdd_inputs as I
+    from paper_1502_01629_b200 import _native as N
+
+    def shape(cfg, patchy, n=None):
+        inst = I.make_config(cfg, n=n) if cfg != "C5" or n else None
+        nn, lo, hi = (inst.n, inst.lo, inst.hi) if inst is not None else (8193, -2.0, 2.0)
+        r, c = C.c_int32(0), C.c_int32(0)
+        assert lib.pdd_choose_tile_shape(nn, lo, hi, patchy, C.byref(r), C.byref(c)) == N.PDD_OK
+        return r.value, c.value
+
+    assert shape("C2", 1) == (16, 64) and shape("C2", 0) == (32, 64)
+    assert shape("C4", 1) == (16, 64) and shape("C4", 0) == (16, 128)
+    assert shape("C5", 1) == (32, 64) and shape("C5", 0) == (16, 128)
+    assert shape("C5", 1, n=513) == (16, 64) and shape("C5", 0, n=513) == (32, 64)
+    r, c = C.c_int32(0), C.c_int32(0)
+    assert lib.pdd_choose_tile_shape(2, 0.0, 1.0, 1, C.byref(r), C.byref(c)) == N.PDD_E_INVALID
