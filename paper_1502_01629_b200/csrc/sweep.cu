@@ -2181,6 +2181,26 @@ bool rowtab_build_device(const DProblem &P, int napad, int H, int precision, int
 }  // namespace pdd
 
 #if PDD_CHECKED && !PDD_ALT_UNIT
+// negative control of the checked build: one deliberately failing check (code 99) must be counted
+namespace pdd {
+__global__ void k_fault_selftest(const float *p)
+{
+    __shared__ float buf[32];
+    if (threadIdx.x == 0) {
+        chk_bounds().lo = (const char *)buf;
+        chk_bounds().hi = (const char *)(buf + 32);
+    }
+    __syncthreads();
+    PDD_CHK_TILE(buf + threadIdx.x, 1, 98);          // inside: must not count
+    if (threadIdx.x == 0) PDD_CHK_TILE(buf + 32, 1, 99);   // one past the end: must count
+    (void)p;
+}
+}  // namespace pdd
+extern "C" void pdd_dev_fault_selftest()
+{
+    pdd::k_fault_selftest<<<1, 32>>>(nullptr);
+    cudaDeviceSynchronize();
+}
 namespace pdd { namespace wide { void dev_faults(unsigned long long *out2, bool add); } }
 namespace pdd { namespace low { void dev_faults(unsigned long long *out2, bool add); } }
 // checked builds only: bounds violations counted by the sweep kernels since the last call
