@@ -30,6 +30,8 @@
  *     keeps ownership and may free them when the call returns.
  *   - The device workspace is owned by the caller (e.g. a PyTorch uint8 tensor) and must stay
  *     alive until pdd_destroy.  libpdd never calls cudaMalloc.
+ *   - Every call runs on the device that owns the workspace given to pdd_create, whatever device
+ *     the calling thread has current, and restores the caller's current device on return.
  *   - Every call enqueues its work on the stream given to pdd_create and synchronises that
  *     stream before returning, so returned statistics and fetched arrays are final.
  *   - Errors: every call returns a pdd_status; the message is in pdd_last_error(ctx)

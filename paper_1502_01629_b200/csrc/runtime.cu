@@ -42,6 +42,22 @@ const char *dev_env(const char *name)
 #endif
 }
 
+// Every entry point runs on the device that owns the context's workspace, whatever device the
+// calling thread has current (a second GPU in the same process), and restores the caller's.
+struct DevGuard {
+    int prev = -1, dev = -1;
+    explicit DevGuard(int d) : dev(d)
+    {
+        if (d < 0) return;
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != d) cudaSetDevice(d);
+    }
+    ~DevGuard()
+    {
+        if (dev >= 0 && prev >= 0 && prev != dev) cudaSetDevice(prev);
+    }
+};
+
 constexpr size_t kAlign = 256;
 constexpr int kMaxPatches = 32768;
 constexpr int64_t kMaxCoarseSweeps = 1 << 20;
@@ -175,6 +191,7 @@ struct pdd_ctx {
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     cudaEvent_t evp[2][64] = {};  // per-round sweep-kernel timing inside a batch (lazy)
     long long launches = 0;     // kernels enqueued by this context (all calls)
+    int device = -1;            // device ordinal of the workspace (DevGuard)
     bool mode_patchy = false;   // the current pdd_solve runs the patchy decomposition
 };
 
@@ -494,6 +511,15 @@ pdd_status pdd_create(const pdd_problem *fine, const pdd_problem *coarse, int32_
     }
     pdd_ctx *ctx = new pdd_ctx();
     ctx->stream = (cudaStream_t)stream;
+    {
+        // the device that owns the workspace becomes the context's device
+        cudaPointerAttributes pa{};
+        if (cudaPointerGetAttributes(&pa, workspace) == cudaSuccess && pa.type == cudaMemoryTypeDevice)
+            ctx->device = pa.device;
+        else
+            cudaGetLastError();   // not a device pointer known to the runtime: keep the current device
+    }
+    DevGuard dev_guard(ctx->device);
     ctx->precision = precision;
     ctx->fine = *fine;
     ctx->has_coarse = coarse != nullptr;
@@ -566,7 +592,10 @@ pdd_status pdd_create(const pdd_problem *fine, const pdd_problem *coarse, int32_
 void pdd_destroy(pdd_ctx *ctx)
 {
     if (!ctx) return;
-    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    {
+        DevGuard dev_guard(ctx->device);
+        if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    }
     for (int k = 0; k < 4; ++k)
         if (ctx->ev[k]) cudaEventDestroy(ctx->ev[k]);
     for (int a = 0; a < 2; ++a)
@@ -579,6 +608,7 @@ void pdd_destroy(pdd_ctx *ctx)
 pdd_status pdd_coarse_solve(pdd_ctx *ctx, double tol_c, int64_t max_sweeps, pdd_coarse_stats *st)
 {
     if (!ctx) return fail(nullptr, PDD_E_INVALID, "ctx is NULL");
+    DevGuard dev_guard(ctx->device);
     if (!ctx->has_coarse) return fail(ctx, PDD_E_STATE, "no coarse problem was given to pdd_create");
     if (!(tol_c > 0.0)) return fail(ctx, PDD_E_INVALID, "tol_c must be > 0");
     if (max_sweeps <= 0 || max_sweeps > kMaxCoarseSweeps)
@@ -651,6 +681,7 @@ pdd_status pdd_coarse_solve(pdd_ctx *ctx, double tol_c, int64_t max_sweeps, pdd_
 pdd_status pdd_synthesize(pdd_ctx *ctx)
 {
     if (!ctx) return fail(nullptr, PDD_E_INVALID, "ctx is NULL");
+    DevGuard dev_guard(ctx->device);
     if (!ctx->coarse_done) return fail(ctx, PDD_E_STATE, "pdd_synthesize needs pdd_coarse_solve first");
     cudaStream_t s = ctx->stream;
     launch_prolong(ctx->coarse.n, ctx->uc_final, ctx->fine.n, ctx->uhat, s);
@@ -672,6 +703,7 @@ pdd_status pdd_synthesize(pdd_ctx *ctx)
 pdd_status pdd_build_patches(pdd_ctx *ctx, int32_t n_patches, double M)
 {
     if (!ctx) return fail(nullptr, PDD_E_INVALID, "ctx is NULL");
+    DevGuard dev_guard(ctx->device);
     if (!ctx->synth_done) return fail(ctx, PDD_E_STATE, "pdd_build_patches needs pdd_synthesize first");
     if (n_patches < 1 || n_patches >= kMaxPatches)
         return fail(ctx, PDD_E_INVALID, "n_patches must be in 1..%d", kMaxPatches - 1);
@@ -725,6 +757,7 @@ pdd_status pdd_build_fuzzy_patches(pdd_ctx *ctx, int32_t n_patches, double eps_P
                                    pdd_fuzzy_stats *st)
 {
     if (!ctx) return fail(nullptr, PDD_E_INVALID, "ctx is NULL");
+    DevGuard dev_guard(ctx->device);
     if (!ctx->synth_done) return fail(ctx, PDD_E_STATE, "pdd_build_fuzzy_patches needs pdd_synthesize first");
     if (n_patches < 1 || n_patches >= kMaxPatches)
         return fail(ctx, PDD_E_INVALID, "n_patches must be in 1..%d", kMaxPatches - 1);
@@ -923,6 +956,7 @@ pdd_status pdd_build_fuzzy_patches_sparse(pdd_ctx *ctx, int32_t n_patches, int32
                                           size_t scratch_bytes, pdd_fuzzy_stats *st)
 {
     if (!ctx) return fail(nullptr, PDD_E_INVALID, "ctx is NULL");
+    DevGuard dev_guard(ctx->device);
     if (!ctx->synth_done) return fail(ctx, PDD_E_STATE, "pdd_build_fuzzy_patches_sparse needs pdd_synthesize first");
     if (n_patches < 1 || n_patches >= kMaxPatches)
         return fail(ctx, PDD_E_INVALID, "n_patches must be in 1..%d", kMaxPatches - 1);
@@ -1006,6 +1040,7 @@ pdd_status pdd_build_fuzzy_patches_sparse(pdd_ctx *ctx, int32_t n_patches, int32
 pdd_status pdd_build_static(pdd_ctx *ctx, int32_t px, int32_t py)
 {
     if (!ctx) return fail(nullptr, PDD_E_INVALID, "ctx is NULL");
+    DevGuard dev_guard(ctx->device);
     if (px < 1 || py < 1 || (int64_t)px * py >= kMaxPatches || px > ctx->fine.n || py > ctx->fine.n)
         return fail(ctx, PDD_E_INVALID, "bad static decomposition %d x %d", px, py);
     launch_static_labels(ctx->fine.n, px, py, ctx->F.kind, ctx->labels, ctx->stream);
@@ -1479,6 +1514,7 @@ extern "C" {
 pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
 {
     if (!ctx) return fail(nullptr, PDD_E_INVALID, "ctx is NULL");
+    DevGuard dev_guard(ctx->device);
     if (!o) return fail(ctx, PDD_E_INVALID, "opts is NULL");
     if (o->mode != 0 && o->mode != 1) return fail(ctx, PDD_E_INVALID, "mode must be 0 or 1");
     if (o->schedule < 0 || o->schedule > 3) return fail(ctx, PDD_E_INVALID, "schedule must be 0..3");
@@ -1741,6 +1777,7 @@ pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_stats *st)
 pdd_status pdd_apply_operator(pdd_ctx *ctx, double *out, int32_t kernel, double *residual)
 {
     if (!ctx) return fail(nullptr, PDD_E_INVALID, "ctx is NULL");
+    DevGuard dev_guard(ctx->device);
     if (kernel < 0 || kernel > 4) return fail(ctx, PDD_E_INVALID, "kernel must be 0..4");
     pdd_status ps = prepare(ctx, kernel, false, true);
     if (ps != PDD_OK) return ps;
@@ -1812,6 +1849,7 @@ pdd_status pdd_get_tile_rounds(pdd_ctx *ctx, int32_t *dst, int32_t count)
 pdd_status pdd_set_tile_shape(pdd_ctx *ctx, int32_t rows, int32_t cols)
 {
     if (!ctx) return fail(nullptr, PDD_E_INVALID, "ctx is NULL");
+    DevGuard dev_guard(ctx->device);
     const bool ok = (rows == 0 && cols == 0) || (rows == 32 && cols == 64) || (rows == 16 && cols == 128) ||
                     (rows == 16 && cols == 64);
     if (!ok) return fail(ctx, PDD_E_INVALID, "tile shape must be 0 x 0 (automatic), 32 x 64, 16 x 128 or 16 x 64");
@@ -1838,6 +1876,7 @@ pdd_status pdd_choose_tile_shape(int32_t n, double lo, double hi, int32_t patchy
 pdd_status pdd_set_tile_cols(pdd_ctx *ctx, int32_t cols)
 {
     if (!ctx) return fail(nullptr, PDD_E_INVALID, "ctx is NULL");
+    DevGuard dev_guard(ctx->device);
     if (cols != 0 && cols != 64 && cols != 128) return fail(ctx, PDD_E_INVALID, "tile cols must be 0, 64 or 128");
     return pdd_set_tile_shape(ctx, cols == 64 ? 32 : cols == 128 ? 16 : 0, cols);
 }
@@ -1856,6 +1895,7 @@ static pdd_status fetch(pdd_ctx *ctx, void *dst, const void *src, size_t bytes, 
 pdd_status pdd_get_values(pdd_ctx *ctx, void *dst, int32_t dst_on_device, int32_t as_fp64)
 {
     if (!ctx) return fail(nullptr, PDD_E_INVALID, "ctx is NULL");
+    DevGuard dev_guard(ctx->device);
     const size_t N = (size_t)ctx->fine.n * ctx->fine.n;
     if (as_fp64) return fetch(ctx, dst, ctx->V, sizeof(double) * N, dst_on_device);
     if (!dst) return fail(ctx, PDD_E_INVALID, "dst is NULL");
@@ -1883,6 +1923,7 @@ pdd_status pdd_set_values(pdd_ctx *ctx, const double *src, int32_t src_on_device
 pdd_status pdd_get_uhat(pdd_ctx *ctx, double *dst, int32_t on_device)
 {
     if (!ctx) return fail(nullptr, PDD_E_INVALID, "ctx is NULL");
+    DevGuard dev_guard(ctx->device);
     if (!ctx->synth_done) return fail(ctx, PDD_E_STATE, "u_hat not computed (pdd_synthesize)");
     return fetch(ctx, dst, ctx->uhat, sizeof(double) * ctx->fine.n * ctx->fine.n, on_device);
 }
@@ -1890,6 +1931,7 @@ pdd_status pdd_get_uhat(pdd_ctx *ctx, double *dst, int32_t on_device)
 pdd_status pdd_get_coarse_values(pdd_ctx *ctx, double *dst, int32_t on_device)
 {
     if (!ctx) return fail(nullptr, PDD_E_INVALID, "ctx is NULL");
+    DevGuard dev_guard(ctx->device);
     if (!ctx->coarse_done) return fail(ctx, PDD_E_STATE, "u_c not computed (pdd_coarse_solve)");
     return fetch(ctx, dst, ctx->uc_final, sizeof(double) * ctx->coarse.n * ctx->coarse.n, on_device);
 }
@@ -1897,6 +1939,7 @@ pdd_status pdd_get_coarse_values(pdd_ctx *ctx, double *dst, int32_t on_device)
 pdd_status pdd_get_controls(pdd_ctx *ctx, uint8_t *dst, int32_t on_device)
 {
     if (!ctx) return fail(nullptr, PDD_E_INVALID, "ctx is NULL");
+    DevGuard dev_guard(ctx->device);
     if (!ctx->synth_done) return fail(ctx, PDD_E_STATE, "a* not computed (pdd_synthesize)");
     return fetch(ctx, dst, ctx->astar, (size_t)ctx->fine.n * ctx->fine.n, on_device);
 }
@@ -1904,6 +1947,7 @@ pdd_status pdd_get_controls(pdd_ctx *ctx, uint8_t *dst, int32_t on_device)
 pdd_status pdd_get_labels(pdd_ctx *ctx, int16_t *dst, int32_t on_device)
 {
     if (!ctx) return fail(nullptr, PDD_E_INVALID, "ctx is NULL");
+    DevGuard dev_guard(ctx->device);
     if (!ctx->labels_mode) return fail(ctx, PDD_E_STATE, "labels not built");
     return fetch(ctx, dst, ctx->labels, sizeof(int16_t) * ctx->fine.n * ctx->fine.n, on_device);
 }
@@ -1911,6 +1955,7 @@ pdd_status pdd_get_labels(pdd_ctx *ctx, int16_t *dst, int32_t on_device)
 pdd_status pdd_get_successors(pdd_ctx *ctx, int32_t *dst, int32_t on_device)
 {
     if (!ctx) return fail(nullptr, PDD_E_INVALID, "ctx is NULL");
+    DevGuard dev_guard(ctx->device);
     if (ctx->labels_mode != 1) return fail(ctx, PDD_E_STATE, "successors not built (pdd_build_patches)");
     return fetch(ctx, dst, ctx->succ0, sizeof(int32_t) * ctx->fine.n * ctx->fine.n, on_device);
 }
