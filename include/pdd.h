@@ -10,6 +10,7 @@
  *   Pre-computation  pdd_coarse_solve    u_c on G_c, sigma = 0, until eps_c
  *                    pdd_synthesize      u_hat = interp(u_c) on G, feedback a*        P:826-827
  *                    pdd_build_patches   split of the Dirichlet set + patches
+ *                    pdd_build_fuzzy_patches[_sparse]  the paper's fuzzy patches
  *                    pdd_build_static    static equal-square decomposition (DD)
  *   Computation      pdd_solve           patch-parallel fine solve until eps
  *                    pdd_get_*           fetch V, a*, labels, u_hat, u_c
@@ -256,10 +257,14 @@ pdd_status pdd_build_fuzzy_patches_sparse(pdd_ctx *ctx, int32_t n_patches, int32
 /* Static equal squares: px columns x py rows, boundaries floor(k n / P) (R19). */
 pdd_status pdd_build_static(pdd_ctx *ctx, int32_t px, int32_t py);
 
-/* The fine solve: rounds of the tile sweep kernel over the active tile list until every tile
- * is converged, then a full-grid Jacobi verification; re-activates and continues
- * while the verification residual is >= tol.  mode 0 needs pdd_synthesize and pdd_build_patches,
- * mode 1 needs pdd_build_static. */
+/* The fine solve: tile visits (in-tile Gauss-Seidel sweeps of the scheme) scheduled by
+ * opts->schedule -- by default one persistent launch whose CTAs take dirty tiles from a work
+ * queue -- until no tile is dirty, then a full-grid Jacobi verification that also
+ * records every patch's own residual; offending tiles are re-queued and the solve continues
+ * while the verification residual is >= tol.  Returns PDD_E_NOCONVERGE (statistics still
+ * written) when max_rounds is exhausted or the residual stagnates above tol (a tolerance below
+ * the arithmetic's noise floor).  mode 0 needs pdd_synthesize and pdd_build_patches (or one of
+ * the fuzzy-patch builders), mode 1 needs pdd_build_static. */
 pdd_status pdd_solve(pdd_ctx *ctx, const pdd_solve_opts *opts, pdd_solve_stats *st);
 
 /* One application of the operator: out = T(V) on every node (Dirichlet nodes copy V), fp64
