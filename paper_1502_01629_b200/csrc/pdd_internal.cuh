@@ -129,6 +129,10 @@ struct TileState {
     int32_t *tile_lab_cnt;   // per tile: number of distinct labels (k_tile_init)
     int32_t *tile_lab_off;   // n_tiles + 1 offsets (k_scan_offsets)
     int16_t *tile_lab_ids;   // capacity n*n: a tile has at most as many labels as nodes
+    unsigned long long *tile_lab_res;   // per CSR entry: max |T(V) - V| over the tile's free nodes of
+                                        // that label in the tile's last check visit (fp64 bits);
+                                        // capacity tile_lab_cap entries (partial verifications)
+    int64_t tile_lab_cap;
     int32_t *tile_round;     // per tile: last activation round that took it (-1: never)
     int n_slots;             // patch slots: n_patches + 1 (the last one = orphans); 0 = none
     uint8_t *tile_orient;    // first in-tile sweep orientation (bit 0: -x, bit 1: -y)
@@ -252,6 +256,9 @@ struct SweepLaunch {
     const int16_t *labels;
     unsigned long long *patch_res;       // check mode: per-patch residual max (or NULL)
     int n_slots;                         // patch slots of labels / patch_res
+    const int32_t *lab_off = nullptr;    // check mode with lab_res: the tile label CSR; every tile
+    const int16_t *lab_ids = nullptr;    //   writes its per-label residuals into its CSR entries
+    unsigned long long *lab_res = nullptr;   // (then launch_patch_res_reduce gives patch_res)
     TileGeom g;
     const int32_t *list;
     int n_list;
@@ -292,6 +299,11 @@ struct SweepLaunch {
 // offending tiles)
 void launch_queue_seed(const TileState &T, const QueueArgs &Q, int n_tiles, double tol, int first,
                        int adm, cudaStream_t s);
+// partial verification of the work-queue schedule: list (T.list[0], count in T.counters) of the
+// tiles with free nodes whose 3 x 3 tile neighbourhood holds a tile visited after `mark`
+void launch_verify_list(const TileGeom &g, const TileState &T, int mark, int n_tiles, cudaStream_t s);
+// patch_res[p] = max over the CSR entries of label p of tile_lab_res (n_slots entries zeroed first)
+void launch_patch_res_reduce(const TileState &T, int n_tiles, cudaStream_t s);
 // per-patch activation trace from the per-tile one (work queue: patch_round[p] = max tile_round
 // over the tiles holding nodes of p)
 void launch_patch_rounds(const TileState &T, int n_tiles, cudaStream_t s);
@@ -330,6 +342,7 @@ int sweep_tile_rows();
 void p3_geometry(int &pitch, int &cstride, int &hmax);
 void p3_tile(int &tw, int &th);   // path-3 tile columns / rows
 void gf_geometry(int &pitch);      // compile-time shared-memory pitch of path 4 (sweep_gf.cuh)
+int pres_shared_slots();           // patch labels a check CTA accumulates in shared memory
 // the 16 x 128 path-3 tile (sweep.cu built with PDD_WIDE_UNIT=1)
 cudaError_t launch_sweep_wide(const SweepLaunch &L, cudaStream_t s);
 void p3_geometry_wide(int &pitch, int &cstride, int &hmax);

@@ -389,6 +389,8 @@ static size_t layout(pdd_ctx *c, void *ws, const pdd_problem *f, const pdd_probl
     T.tile_lab_cnt = cv.take<int32_t>(tmax);
     T.tile_lab_off = cv.take<int32_t>((size_t)tmax + 1);
     T.tile_lab_ids = cv.take<int16_t>(N);   // a tile has at most as many labels as nodes
+    T.tile_lab_cap = (int64_t)32 * tmax;    // per-entry residuals of the partial verifications
+    T.tile_lab_res = cv.take<unsigned long long>((size_t)T.tile_lab_cap);
     T.tile_round = cv.take<int32_t>(tmax);
     T.tile_orient = cv.take<uint8_t>(tmax);
     T.tile_stamp = cv.take<int32_t>(tmax);
@@ -1438,6 +1440,15 @@ static pdd_status queue_loop(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_st
     double best = INFINITY;
     int stalled = 0;
     bool first = true;
+    // partial verifications need every tile's per-label residuals in its label-list entries
+    bool partial_ok = false, verified_once = false;
+    int verify_mark = 0;
+    if (ctx->T.n_slots > 0 && ctx->T.n_slots <= pres_shared_slots() && !dev_env("PDD_FULL_VERIFY")) {
+        int32_t entries = 0;
+        CK(cudaMemcpyAsync(&entries, ctx->T.tile_lab_off + nt, sizeof entries, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        partial_ok = entries <= ctx->T.tile_lab_cap;
+    }
     for (;;) {
         // ring and cursors start empty at every launch (tickets abandoned at the last stop)
         CK(cudaMemsetAsync(ctx->qring, 0, sizeof(int32_t) * ctx->qcap, s));
@@ -1477,14 +1488,39 @@ static pdd_status queue_loop(pdd_ctx *ctx, const pdd_solve_opts *o, pdd_solve_st
                     bits_to_double(qc.max_res), qc.stop, qc.adm, ms);
         if (qc.stop == 2) break;   // visit cap reached
         if (qc.stop != 3) qc.adm = std::max(qc.adm, tiles_free);
-        // full-grid verification with each patch's own residual
+        // verification with each patch's own residual: the whole grid the first time;
+        // afterwards only the tiles whose residual can have changed (visited since the last
+        // verification, or next to such a tile) -- every other tile keeps the Jacobi residual of
+        // its last check, and the per-patch maxima are rebuilt from the per-tile entries
         CK(cudaEventRecord(ctx->ev[2], s));
-        SweepLaunch V = make_launch(ctx, ctx->T.all_list, nt, 1, 1, nullptr);
-        CK(cudaMemsetAsync(ctx->T.patch_res, 0, sizeof(unsigned long long) * ctx->T.n_slots, s));
+        const int32_t *vlist = ctx->T.all_list;
+        int vcount = nt;
+        if (partial_ok && verified_once) {
+            launch_verify_list(ctx->g, ctx->T, verify_mark, nt, s);
+            ctx->launches++;
+            CK(cudaMemcpyAsync(ctx->h_cnt, ctx->T.counters, sizeof(ActCounters), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            vlist = ctx->T.list[0];
+            vcount = ctx->h_cnt->count;
+        }
+        SweepLaunch V = make_launch(ctx, vlist, vcount, 1, 1, nullptr);
         V.patch_res = ctx->T.patch_res;
         V.n_slots = ctx->T.n_slots;
+        if (partial_ok) {
+            V.lab_off = ctx->T.tile_lab_off;
+            V.lab_ids = ctx->T.tile_lab_ids;
+            V.lab_res = ctx->T.tile_lab_res;
+        } else {
+            CK(cudaMemsetAsync(ctx->T.patch_res, 0, sizeof(unsigned long long) * ctx->T.n_slots, s));
+        }
         CK(launch_sweep(V, s));
         ctx->launches++;
+        if (partial_ok) {
+            launch_patch_res_reduce(ctx->T, nt, s);
+            ctx->launches++;
+        }
+        verified_once = true;
+        verify_mark = (int)std::min<unsigned long long>(qc.visits, 0x7fffffffull);
         CK(cudaEventRecord(ctx->ev[3], s));
         S.rounds++;
         S.verify_passes++;

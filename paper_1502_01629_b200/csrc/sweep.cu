@@ -176,6 +176,9 @@ struct KP {
     int32_t *tile_sweeps;
     const int16_t *labels;            // check mode: patch labels for the per-patch residuals
     unsigned long long *patch_res;    //   per-patch max |T(V) - V| (fp64 bits) or NULL
+    const int32_t *lab_off;           //   with lab_res: per-tile, per-label residuals into the
+    const int16_t *lab_ids;           //   tile's CSR entries instead of atomics on patch_res
+    unsigned long long *lab_res;
     int n_slots;
 };
 
@@ -917,7 +920,12 @@ __device__ __forceinline__ void sweep_tile(const KP<real> &A, int t, unsigned ch
     if (threadIdx.x == 0) A.tile_res[t] = rmaxv;
     if (res_out) *res_out = rmaxv;
     if constexpr (CHECK) {
-        if (A.patch_res) {
+        if (A.patch_res && A.lab_res) {
+            // per-label residuals of THIS tile into its CSR entries (labels < PRES_SH: the caller
+            // checks n_slots): a later partial verification replaces only the visited tiles' entries
+            for (int k = A.lab_off[t] + threadIdx.x; k < A.lab_off[t + 1]; k += blockDim.x)
+                A.lab_res[k] = pres_table()[A.lab_ids[k]];
+        } else if (A.patch_res) {
             const int m = min(A.n_slots, PRES_SH);
             for (int e = threadIdx.x; e < m; e += blockDim.x) {
                 const unsigned long long v = pres_table()[e];
@@ -1279,6 +1287,9 @@ static cudaError_t launch_one(const SweepLaunch &L, cudaStream_t s)
     A.nu_counter = L.nu_counter;
     A.labels = L.labels;
     A.patch_res = CHECK ? L.patch_res : nullptr;
+    A.lab_off = L.lab_off;
+    A.lab_ids = L.lab_ids;
+    A.lab_res = CHECK ? L.lab_res : nullptr;
     A.n_slots = L.n_slots;
     const size_t smem_base = sweep_smem_base<real, PATH>(L.g.H, L.g.pitch, L.g.cstride);
     const int tw_ = PATH == 2 ? TWOf<WY, WX>::value : PATH == 3 ? TW3 : TW_GENERAL;
@@ -1429,6 +1440,7 @@ void p3_geometry(int &pitch, int &cstride, int &hmax)
 
 #if !PDD_ALT_UNIT
 void gf_geometry(int &pitch) { pitch = GF_PITCH; }
+int pres_shared_slots() { return PRES_SH; }
 #endif
 
 void p3_tile(int &tw, int &th)
@@ -2023,6 +2035,51 @@ __global__ void k_patch_rounds(const int32_t *tile_round, const int32_t *lab_off
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n_tiles || tile_round[t] < 0) return;
     for (int k = lab_off[t]; k < lab_off[t + 1]; ++k) atomicMax(&patch_round[lab_ids[k]], tile_round[t]);
+}
+
+__global__ void k_verify_list(TileGeom g, TileState T, int mark, int n_tiles)
+{
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    ActCounters *C = reinterpret_cast<ActCounters *>(T.counters);
+    bool take = false;
+    if (t < n_tiles && T.tile_free[t] > 0) {
+        const int tx = t % g.tiles_x, ty = t / g.tiles_x;
+        for (int dy = -1; dy <= 1 && !take; ++dy)
+            for (int dx = -1; dx <= 1; ++dx) {
+                const int ax = tx + dx, ay = ty + dy;
+                if (ax < 0 || ay < 0 || ax >= g.tiles_x || ay >= g.tiles_y) continue;
+                if (T.tile_round[ay * g.tiles_x + ax] > mark) { take = true; break; }
+            }
+    }
+    const unsigned m = __ballot_sync(FULL, take);
+    if (!m) return;
+    const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+    int basei = 0;
+    if (lane == leader) basei = atomicAdd(&C->count, __popc(m));
+    basei = __shfl_sync(FULL, basei, leader);
+    if (take) T.list[0][basei + __popc(m & ((1u << lane) - 1u))] = t;
+}
+
+void launch_verify_list(const TileGeom &g, const TileState &T, int mark, int n_tiles, cudaStream_t s)
+{
+    cudaMemsetAsync(T.counters, 0, sizeof(ActCounters), s);
+    k_verify_list<<<(n_tiles + 255) / 256, 256, 0, s>>>(g, T, mark, n_tiles);
+}
+
+__global__ void k_patch_res_reduce(TileState T, int n_tiles)
+{
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n_tiles) return;
+    for (int k = T.tile_lab_off[t]; k < T.tile_lab_off[t + 1]; ++k) {
+        const unsigned long long v = T.tile_lab_res[k];
+        if (v) atomicMax(T.patch_res + T.tile_lab_ids[k], v);
+    }
+}
+
+void launch_patch_res_reduce(const TileState &T, int n_tiles, cudaStream_t s)
+{
+    cudaMemsetAsync(T.patch_res, 0, sizeof(unsigned long long) * T.n_slots, s);
+    k_patch_res_reduce<<<(n_tiles + 255) / 256, 256, 0, s>>>(T, n_tiles);
 }
 
 void launch_patch_rounds(const TileState &T, int n_tiles, cudaStream_t s)
