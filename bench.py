@@ -4,8 +4,8 @@
 A step = one pass of the whole hot path on config C5
 (8193^2 Zermelo navigation, 64 controls, 4 Markov branches, fp32 arithmetic): coarse solve on
 513^2 -> prolongation -> synthesis -> patch labels (256 patches) -> patchy fine solve until the
-full-grid Jacobi residual is < 1e-7 (verified; at 1e-7 the fp32 V is within 6e-6 max|V| of the
-certified fp64 fixed point, R12).  Inputs are resident in HBM when the timed
+full-grid Jacobi residual is < 1e-7 (verified; at 1e-7 the fp32 V is within 1e-6 max|V| of the
+certified fp64 fixed point).  Inputs are resident in HBM when the timed
 region starts (the problem arrays are uploaded once by pdd_create); V (fp64, 537 MB) and the
 other per-node arrays are larger than L2, so no flush is needed between steps.
 
@@ -15,13 +15,19 @@ value      = free-node updates performed by the sweep kernel in the K timed step
 e2e        = same metric through the C ABI with HOST buffers: every step creates the context
              from pinned host arrays (H2D inside the timed region), runs the pipeline and copies
              V back to pinned host memory (D2H).
-roofline   = the sweep kernel (k_sweep): algorithmic fp32 flop per node-update
-             F = N_A * (15 * 2p + 10) (4480 at C5; the bilinear reconstructions
-             alone, N_A 2p x 4 FMA = 2048, are reported as frac_bilinear_only) times the
-             updates of the timed region / the summed
-             duration of the sweep launches (CUDA events on the launching stream); peak = FP32
-             FMA rate derived from the guide's unit counts: 148 SMs x 128 lanes x 2 flop x
-             1965 MHz = 74.4 TFLOP/s ("bound": "alu").
+roofline   = the sweep kernel (k_sweep_queue, the persistent work-queue launch): algorithmic fp32
+             flop per node-update F = N_A * (15 * 2p + 10) (4480 at C5; the
+             bilinear reconstructions alone, N_A 2p x 4 FMA = 2048, are reported as
+             frac_bilinear_only) times the updates of the timed region / the summed duration of
+             the sweep launches (CUDA events on the launching stream); peak = the FP32 FFMA rate
+             MEASURED on the box by libpdd's micro-benchmark (pdd_measure_alu_peaks; the derived
+             148 SMs x 128 lanes x 2 flop x 1965 MHz = 74.4 TFLOP/s is reported beside it);
+             "bound": "alu"; traffic = DRAM bytes per node-update of the committed ncu capture
+             (profiles/sweep_traffic.json) x the node-updates per launch.
+accuracy_run = the same pipeline in fp64 arithmetic (BASELINE config C5: "fp32 with an fp64
+             accuracy run") and max |V32 - V64| / max|V|, computed on the device.
+oracle_time_to_converge = MEASURED plain-Jacobi oracle solves (C1, C2 by default); C5's figure in
+             time_to_converge is extrapolated and named so.
 cpu_baseline = the fp64 oracle (oracle/, plain C + OpenMP on all host cores) applying the same
              operator T to a bounded sample of the same grid (a band of rows of C5), in
              node-updates/s.

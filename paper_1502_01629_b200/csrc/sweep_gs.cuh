@@ -24,7 +24,10 @@
 // come from one LDS.128, columns 4.. from a second LDS.64 / LDS.128.
 
 #ifndef PDD_SPIN_NS
-#define PDD_SPIN_NS 0     // 0: plain spin on the shared-memory progress counter
+#define PDD_SPIN_NS 32    // pause (ns) between polls of the previous row's progress counter; 0 = plain
+                          // spin.  A waiting warp's polls compete for issue slots with the working
+                          // warps of the SM: measured under the work queue (profiles/r3j_spin_ab.txt)
+                          // 32 or 100 ns give +2 % kernel throughput on C5 / C4 (patchy and static)
 #endif
 #if PDD_SPIN_NS > 0
 #define PDD_SPIN_PAUSE() __nanosleep(PDD_SPIN_NS)
