@@ -43,7 +43,13 @@
 #endif
 __device__ __forceinline__ void prog_release(volatile int *p, int v)
 {
-#if PDD_ACQREL
+#if PDD_ACQREL == 2
+    // relaxed: volatile store behind a compiler barrier, no hardware fence (development A/B; the
+    // node commits of this warp precede it in program order on the SM's in-order LSU; a late
+    // commit would only make the next row read an older iterate, which chaotic relaxation allows)
+    const unsigned a = (unsigned)__cvta_generic_to_shared((const void *)p);
+    asm volatile("st.volatile.shared.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+#elif PDD_ACQREL
     const unsigned a = (unsigned)__cvta_generic_to_shared((const void *)p);
     asm volatile("st.release.cta.shared.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 #else
@@ -55,7 +61,11 @@ __device__ __forceinline__ void prog_release(volatile int *p, int v)
 __device__ __forceinline__ int prog_acquire_addr(unsigned a)
 {
     int v;
+#if PDD_ACQREL == 2
+    asm volatile("ld.volatile.shared.s32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+#else
     asm volatile("ld.acquire.cta.shared.s32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+#endif
     return v;
 }
 
