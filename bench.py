@@ -457,6 +457,8 @@ def main():
             per_launch_updates = nu / max(1, sweep_launches)
             roof["traffic"] = pj["dram_bytes_per_node_update"] * per_launch_updates
             roof["algorithmic_bytes_per_launch"] = pj.get("algorithmic_bytes_per_node_update", 18.4) * per_launch_updates
+            if "ncu_pipes" in pj:
+                roof["ncu"] = pj["ncu_pipes"]
             roof["traffic_basis"] = ("dram bytes per node-update from ncu --set full (%s) x the "
                                      "average node-updates per sweep launch of this run; "
                                      "algorithmic bytes per node-update ~18.4 at one sweep per visit "
@@ -534,6 +536,10 @@ def main():
             "gpu_launches": launches,
             "clocks": clk,
         }
+        # SURVEY.md 8(d) metric 2, work-normalised speed: free nodes x the oracle's Jacobi sweep count
+        # (C5: ~0.71 n sweeps, extrapolated from the measured 513^2 / 1025^2 oracle runs) / GPU time
+        out["time_to_converge"]["effective_node_updates_per_s_vs_jacobi"] = (
+            inst.free_count() * 0.71 * inst.n / (t_max / args.steps))
         if cpu:
             # EXTRAPOLATED (not measured): plain-Jacobi oracle sweeps ~ 0.71 n (
             # the measured oracle solves of the smaller configs are in oracle_time_to_converge)
