@@ -78,9 +78,21 @@ __global__ void k_init_values(DProblem P, double *V)
 #ifndef PDD_COARSE_RTSMEM
 #define PDD_COARSE_RTSMEM 1   // ... and the tile's rows of the row-invariant table
 #endif
+#ifndef PDD_CANON_UNROLL
+#define PDD_CANON_UNROLL 1   // controls per loop trip in the staged coarse / synthesis kernels (A/B: profiles/r4a_*)
+#endif
+#ifndef PDD_CANON_MINB
+#define PDD_CANON_MINB 4     // __launch_bounds__ min blocks per SM of those kernels (A/B)
+#endif
+#define PDD_PRAGMA_(x) _Pragma(#x)
+#define PDD_UNROLL_(n) PDD_PRAGMA_(unroll n)
 #ifndef PDD_EXACT_MIN
 #define PDD_EXACT_MIN 0   // measured slower on sm_100a (C5 coarse 31 vs 24 ms): kept as an option
 #endif
+// tile geometry of the staged coarse sweep and synthesis: CT x CT nodes per CTA, halo of CH cells
+constexpr int CT = 16;
+constexpr int CH = 4;
+constexpr int CSW = CT + 2 * CH;   // staged row width
 constexpr int EXK = 4;
 struct ExactMin {
     float mt = INFINITY;                     // running estimate of the minimum
@@ -172,7 +184,14 @@ __global__ void k_coarse_rowtab(DProblem P, CoarseRowEntry *tab)
     const double l = coef_at(P.cost, 0, j, n);
     e.hl = DMUL(P.h, P.cost_ctrl ? DADD(l, P.cost_ctrl[a]) : l);
     e.cy = cy;
-    e.pad = 0;
+    // interior fast path (canon_ctrl_fast): x cell relative to the node, corner that is the node
+    const double fb = floor(e.bxq);
+    e.fbd = fb;
+    const int fbi = fb < -1000.0 ? -1000 : (fb > 1000.0 ? 1000 : (int)fb);
+    const int sx = fbi == 0 ? 0 : (fbi == -1 ? 1 : -1);         // corner column that holds x = i
+    const int sy = cy == j ? 0 : (cy + 1 == j ? 1 : -1);        // corner row that holds y = j
+    const int sc = (sx >= 0 && sy >= 0) ? 2 * sy + sx : -1;
+    e.pk = (((cy - j) * CSW + fbi + 32768) & 0xffff) | (sc >= 0 ? (0x10000 << sc) : 0);
     tab[id] = e;
 }
 
@@ -216,14 +235,13 @@ __device__ double canon_node_update_rt(const DProblem &P, const double *V, int i
 // The same update reading V from a shared-memory copy of the tile + halo (CH cells): the 4 x N_A
 // corner gathers per node hit shared memory instead of L1/L2 (the coarse sweep stalled on them:
 // long scoreboard 3.4 per issue).  Same values, same operations: bit-identical.
-constexpr int CH = 4;
-constexpr int CSW = 16 + 2 * CH;   // staged row width (CT + 2 CH)
 __device__ double canon_node_update_rt_s(const DProblem &P, const double *__restrict__ sV, int i,
                                          int j, int ib, int jb, const CoarseRowEntry *__restrict__ row)
 {
     const int n = P.n;
     const double top = (double)(n - 1);
     double best = INFINITY;
+    PDD_UNROLL_(PDD_CANON_UNROLL)
     for (int a = 0; a < P.na; ++a) {
         const CoarseRowEntry e = row[a];
         double gx = DADD((double)i, e.bxq);
@@ -248,6 +266,103 @@ __device__ double canon_node_update_rt_s(const DProblem &P, const double *__rest
         if (v < best) best = v;
     }
     return best;
+}
+
+// ---- interior fast path of the staged coarse sweep and synthesis (bit-identical) ----------------
+// In a tile none of whose feet is clamped in x (columns in [CH, n-1-CH]; the y clamps are already
+// in the table) the per-control work of canon_node_update_rt_s shrinks without changing a bit:
+//  * cell: g = rn(i + q f1) lies in [i + fb, i + fb + 1] for fb = floor(q f1) (both ends are
+//    representable and rounding is monotone), so floor(g) = i + fb unless g == i + fb + 1; then
+//    t = g - (i + fb) == 1 and that control is evaluated by the generic code (canon_ctrl_generic).
+//    i + fb is formed by an exact fp64 addition: no float <-> int conversion, no clamps.
+//  * the offset of corner 00 in the staged tile and the corner that is the node itself depend on
+//    (row, control) only and come from the table (CoarseRowEntry::pk).
+//  * the sum over the non-self corners keeps the corner order 00, 10, 01, 11; its first term is not
+//    added to 0.0 (0.0 + x == x for every x but -0.0, and the products w V are >= +0.0), lam0 is the
+//    self corner's weight (0.0 + w == w).
+//  * the minimum of the IEEE quotients num_a / den_a (den_a = 1 - beta lam0 > 0 for beta < 1) is the
+//    quotient of the exact minimiser, because rounding is monotone; the minimiser is found without
+//    dividing: num_a / den_a < num_b / den_b  <=>  num_a den_b < num_b den_a, decided by the rounded
+//    products when they differ (monotone rounding again) and by the exact FMA residuals when they are
+//    equal.  One IEEE division of the minimiser at the end: the bits of min_a rn(num_a / den_a).
+#ifndef PDD_CANON_FAST
+#define PDD_CANON_FAST 1
+#endif
+
+// one control in the generic form: numerator and denominator of its quotient (same operations as
+// canon_node_update_rt_s)
+__device__ __noinline__ double2 canon_ctrl_generic(int n, double beta, const double *sV, int i, int j,
+                                                   int ib, int jb, double bxq, double ty, double uy,
+                                                   double hl, int cy)
+{
+    const double top = (double)(n - 1);
+    double gx = DADD((double)i, bxq);
+    if (gx < 0.0) gx = 0.0;
+    if (gx > top) gx = top;
+    int cx = (int)floor(gx);
+    if (cx > n - 2) cx = n - 2;
+    const double tx = DSUB(gx, (double)cx);
+    const double ux = DSUB(1.0, tx);
+    const double wg[4] = {DMUL(ux, uy), DMUL(tx, uy), DMUL(ux, ty), DMUL(tx, ty)};
+    const int s0 = (cy - jb) * CSW + (cx - ib);
+    const int sr[4] = {s0, s0 + 1, s0 + CSW, s0 + CSW + 1};
+    const bool self[4] = {cx == i && cy == j, cx + 1 == i && cy == j, cx == i && cy + 1 == j,
+                          cx + 1 == i && cy + 1 == j};
+    double lam0 = 0.0, rp = 0.0;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        if (self[t]) lam0 = DADD(lam0, wg[t]);
+        else rp = DADD(rp, DMUL(wg[t], sV[sr[t]]));
+    }
+    return make_double2(DADD(hl, DMUL(beta, rp)), DSUB(1.0, DMUL(beta, lam0)));
+}
+
+__device__ __forceinline__ double canon_node_update_fast(const DProblem &P, const double *__restrict__ sV,
+                                                         int i, int j, int ib, int jb,
+                                                         const CoarseRowEntry *__restrict__ row)
+{
+    const double id = (double)i;
+    const double beta = P.beta;
+    const int sself = (j - jb) * CSW + (i - ib) - 32768;
+    double nb = INFINITY, db = 1.0;          // the best quotient so far as numerator / denominator
+    PDD_UNROLL_(PDD_CANON_UNROLL)
+    for (int a = 0; a < P.na; ++a) {
+        const double bxq = row[a].bxq, fbd = row[a].fbd;
+        const double gx = DADD(id, bxq);
+        const double tx = DSUB(gx, DADD(id, fbd));
+        double num, den;
+        if (__double2hiint(tx) >= 0x3ff00000) {          // t == 1: the rounded foot is the next integer
+            const double2 nd = canon_ctrl_generic(P.n, beta, sV, i, j, ib, jb, bxq, row[a].ty, row[a].uy,
+                                                  row[a].hl, row[a].cy);
+            num = nd.x;
+            den = nd.y;
+        } else {
+            const double ty = row[a].ty, uy = row[a].uy;
+            const int pk = row[a].pk;
+            const int s0 = sself + (pk & 0xffff);
+            const double ux = DSUB(1.0, tx);
+            const double w0 = DMUL(ux, uy), w1 = DMUL(tx, uy), w2 = DMUL(ux, ty), w3 = DMUL(tx, ty);
+            // the corner that is the node itself (one-hot in bits 16..19 of pk, none: 0) contributes
+            // +0.0 in its place of the corner-order sum: x + 0.0 == x
+            const double p0 = (pk & 0x10000) ? 0.0 : DMUL(w0, sV[s0]);
+            const double p1 = (pk & 0x20000) ? 0.0 : DMUL(w1, sV[s0 + 1]);
+            const double p2 = (pk & 0x40000) ? 0.0 : DMUL(w2, sV[s0 + CSW]);
+            const double p3 = (pk & 0x80000) ? 0.0 : DMUL(w3, sV[s0 + CSW + 1]);
+            const bool has = pk & 0xf0000, bx = pk & 0xa0000, by = pk & 0xc0000;
+            const double rp = DADD(DADD(DADD(p0, p1), p2), p3);
+            const double lam0 = DMUL(bx ? tx : ux, by ? ty : uy);     // the self corner's weight
+            num = DADD(row[a].hl, DMUL(beta, rp));
+            den = has ? DSUB(1.0, DMUL(beta, lam0)) : 1.0;            // 1 - beta 0 == 1
+        }
+        const double c1 = DMUL(num, db), c2 = DMUL(nb, den);
+        bool take = c1 < c2;
+        if (c1 == c2) take = __fma_rn(num, db, -c1) < __fma_rn(nb, den, -c2);
+        if (take) {
+            nb = num;
+            db = den;
+        }
+    }
+    return DDIV(nb, db);
 }
 
 __global__ void k_coarse_sweep(DProblem P, const double *__restrict__ Vin, double *__restrict__ Vout,
@@ -282,8 +397,7 @@ __global__ void k_coarse_sweep(DProblem P, const double *__restrict__ Vin, doubl
 // new value is the value the last sweep wrote, i.e. Vin.  Ahead of the front (V0, stationary) and
 // behind it (converged) most tiles are skipped.  fprev / fout: per-tile "changed" flags of the
 // previous / this sweep (fprev unused at sweep 0).
-constexpr int CT = 16;
-__global__ void __launch_bounds__(CT * CT) k_coarse_sweep_tiles(
+__global__ void __launch_bounds__(CT * CT, PDD_CANON_MINB) k_coarse_sweep_tiles(
     DProblem P, const double *__restrict__ Vin, double *__restrict__ Vout, double tol,
     unsigned long long *res_hist, int sweep, int *sweeps_done, const uint8_t *fprev,
     uint8_t *fout, int tiles_x, const CoarseRowEntry *rowtab, int stage_ok)
@@ -312,6 +426,9 @@ __global__ void __launch_bounds__(CT * CT) k_coarse_sweep_tiles(
     __shared__ double sV[CSW * CSW];
     extern __shared__ CoarseRowEntry sRT[];      // the tile's CT rows of the row table (if sized)
     const bool staged = rowtab && PDD_COARSE_SMEM && s_act && stage_ok;
+    // interior tile (no foot clamped in x), table rows staged, den > 0: the fast path above
+    const bool fast = PDD_CANON_FAST && staged && stage_ok > 1 && P.beta < 1.0 && tx * CT >= CH &&
+                      tx * CT + CT - 1 + CH <= n - 1;
     if (staged) {
         for (int e = threadIdx.x; e < CSW * CSW; e += CT * CT) {
             const int gi = ib + e % CSW, gj = jb + e / CSW;
@@ -332,7 +449,8 @@ __global__ void __launch_bounds__(CT * CT) k_coarse_sweep_tiles(
         if (!s_act || P.kind[k] != 0) {
             Vout[k] = vin;
         } else {
-            const double v = staged ? canon_node_update_rt_s(P, sV, i, j, ib, jb,
+            const double v = fast ? canon_node_update_fast(P, sV, i, j, ib, jb, sRT + (j - ty * CT) * P.na)
+                           : staged ? canon_node_update_rt_s(P, sV, i, j, ib, jb,
                                                              stage_ok > 1 ? sRT + (j - ty * CT) * P.na
                                                                           : rowtab + (int64_t)j * P.na)
                            : rowtab ? canon_node_update_rt(P, Vin, i, j, rowtab + (int64_t)j * P.na)
@@ -658,45 +776,68 @@ __global__ void k_synthesize_rt(DProblem P, const double *__restrict__ uhat,
 
 // k_synthesize_rt on 16 x 16 node tiles with u_hat's tile + halo (CH cells) staged in shared
 // memory: the 4 N_A gathers per node hit shared memory.  Same operations: bit-identical.
-__global__ void __launch_bounds__(256) k_synthesize_rt_s(DProblem P, const double *__restrict__ uhat,
+#ifndef PDD_SYNTH_UNROLL
+#define PDD_SYNTH_UNROLL 1 // controls per loop trip of the strip kernel (A/B)
+#endif
+#ifndef PDD_SYNTH_STRIP
+#define PDD_SYNTH_STRIP 8  // tiles per CTA (one strip of a tile row)
+#endif
+// A CTA walks `strip` consecutive tiles of one tile row; when `rt_staged` the 16 rows of the table
+// it needs are copied to shared memory once per CTA (the per-control table reads from global memory
+// were the kernel's main stall: long scoreboard 6.6 per issue, profiles/r4b_*).
+template <bool rt_staged>
+__global__ void __launch_bounds__(256, PDD_CANON_MINB) k_synthesize_rt_s(DProblem P, const double *__restrict__ uhat,
                                                          const CoarseRowEntry *__restrict__ tab,
-                                                         uint8_t *__restrict__ astar, int tiles_x)
+                                                         uint8_t *__restrict__ astar, int tiles_x,
+                                                         int strip)
 {
     __shared__ double sU[CSW * CSW];
+    extern __shared__ CoarseRowEntry sRTs[];
     const int n = P.n;
-    const int tx = blockIdx.x % tiles_x, ty = blockIdx.x / tiles_x;
-    const int ib = tx * 16 - CH, jb = ty * 16 - CH;
-    for (int e = threadIdx.x; e < CSW * CSW; e += 256) {
-        const int gi = ib + e % CSW, gj = jb + e / CSW;
-        sU[e] = (gi >= 0 && gj >= 0 && gi < n && gj < n) ? uhat[(int64_t)gj * n + gi] : 0.0;
+    const int strips_x = (tiles_x + strip - 1) / strip;
+    const int ty = blockIdx.x / strips_x, tx0 = (blockIdx.x % strips_x) * strip;
+    const int jb = ty * 16 - CH;
+    const int j = ty * 16 + (int)(threadIdx.x >> 4);
+    if (rt_staged) {
+        const int rows = min(16, n - ty * 16);
+        for (int e = threadIdx.x; e < rows * P.na; e += 256) sRTs[e] = tab[(int64_t)ty * 16 * P.na + e];
     }
-    __syncthreads();
-    const int i = tx * 16 + (int)(threadIdx.x & 15), j = ty * 16 + (int)(threadIdx.x >> 4);
-    if (i >= n || j >= n) return;
-    const int64_t k = (int64_t)j * n + i;
-    if (P.kind[k] != 0) { astar[k] = 255; return; }
+    const CoarseRowEntry *row = rt_staged ? sRTs + (j - ty * 16) * P.na : tab + (int64_t)min(j, n - 1) * P.na;
     const double top = (double)(n - 1);
-    const CoarseRowEntry *row = tab + (int64_t)j * P.na;
-    double best = INFINITY;
-    int arg = -1;
-    for (int a = 0; a < P.na; ++a) {
-        const CoarseRowEntry e = row[a];
-        double gx = DADD((double)i, e.bxq);
-        if (gx < 0.0) gx = 0.0;
-        if (gx > top) gx = top;
-        int cx = (int)floor(gx);
-        if (cx > n - 2) cx = n - 2;
-        const double tx2 = DSUB(gx, (double)cx);
-        const double ux = DSUB(1.0, tx2);
-        const int s0 = (e.cy - jb) * CSW + (cx - ib);
-        double sm = DMUL(DMUL(ux, e.uy), sU[s0]);
-        sm = DADD(sm, DMUL(DMUL(tx2, e.uy), sU[s0 + 1]));
-        sm = DADD(sm, DMUL(DMUL(ux, e.ty), sU[s0 + CSW]));
-        sm = DADD(sm, DMUL(DMUL(tx2, e.ty), sU[s0 + CSW + 1]));
-        const double v = DADD(e.hl, DMUL(P.beta, sm));
-        if (v < best) { best = v; arg = a; }
+    for (int tx = tx0; tx < min(tx0 + strip, tiles_x); ++tx) {
+        const int ib = tx * 16 - CH;
+        __syncthreads();                       // the previous tile's readers are done (and sRTs is filled)
+        for (int e = threadIdx.x; e < CSW * CSW; e += 256) {
+            const int gi = ib + e % CSW, gj = jb + e / CSW;
+            sU[e] = (gi >= 0 && gj >= 0 && gi < n && gj < n) ? uhat[(int64_t)gj * n + gi] : 0.0;
+        }
+        __syncthreads();
+        const int i = tx * 16 + (int)(threadIdx.x & 15);
+        if (i >= n || j >= n) continue;
+        const int64_t k = (int64_t)j * n + i;
+        if (P.kind[k] != 0) { astar[k] = 255; continue; }
+        double best = INFINITY;
+        int arg = -1;
+        PDD_UNROLL_(PDD_SYNTH_UNROLL)
+        for (int a = 0; a < P.na; ++a) {
+            const CoarseRowEntry e = row[a];
+            double gx = DADD((double)i, e.bxq);
+            if (gx < 0.0) gx = 0.0;
+            if (gx > top) gx = top;
+            int cx = (int)floor(gx);
+            if (cx > n - 2) cx = n - 2;
+            const double tx2 = DSUB(gx, (double)cx);
+            const double ux = DSUB(1.0, tx2);
+            const int s0 = (e.cy - jb) * CSW + (cx - ib);
+            double sm = DMUL(DMUL(ux, e.uy), sU[s0]);
+            sm = DADD(sm, DMUL(DMUL(tx2, e.uy), sU[s0 + 1]));
+            sm = DADD(sm, DMUL(DMUL(ux, e.ty), sU[s0 + CSW]));
+            sm = DADD(sm, DMUL(DMUL(tx2, e.ty), sU[s0 + CSW + 1]));
+            const double v = DADD(e.hl, DMUL(P.beta, sm));
+            if (v < best) { best = v; arg = a; }
+        }
+        astar[k] = (uint8_t)arg;
     }
-    astar[k] = (uint8_t)arg;
 }
 
 __global__ void k_successor(DProblem P, double M, const uint8_t *__restrict__ astar,
@@ -804,10 +945,13 @@ void launch_coarse_sweep_tiles(const DProblem &P, const double *Vin, double *Vou
         dyn = sizeof(CoarseRowEntry) * CT * (size_t)P.na;
         if (dyn > 64 * 1024) dyn = 0;
         else {
-            static bool attr = false;
-            if (!attr) {
+            // the attribute is per device: set it once on each device the library runs on
+            static bool attr[64] = {};
+            int dev = 0;
+            cudaGetDevice(&dev);
+            if (dev < 0 || dev >= 64 || !attr[dev]) {
                 cudaFuncSetAttribute(k_coarse_sweep_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-                attr = true;
+                if (dev >= 0 && dev < 64) attr[dev] = true;
             }
             stage_ok = 2;
         }
@@ -891,7 +1035,24 @@ void launch_synthesize_rt(const DProblem &P, const double *uhat, const CoarseRow
 {
     if (stage_ok && PDD_COARSE_SMEM) {
         const int tx = (P.n + 15) / 16;
-        k_synthesize_rt_s<<<tx * tx, 256, 0, s>>>(P, uhat, tab, astar, tx);
+        // strips of PDD_SYNTH_STRIP tiles; the CTA's 16 table rows staged in shared memory when they fit
+        // (shorter strips on small grids: keep >= 8 CTAs per SM in the grid)
+        int strip = PDD_SYNTH_STRIP;
+        while (strip > 1 && ((tx + strip - 1) / strip) * tx < 148 * 8) strip /= 2;
+        const int strips_x = (tx + strip - 1) / strip;
+        size_t dyn = sizeof(CoarseRowEntry) * 16 * (size_t)P.na;
+        if (dyn > 64 * 1024) dyn = 0;
+        else {
+            static bool attr[64] = {};
+            int dev = 0;
+            cudaGetDevice(&dev);
+            if (dev < 0 || dev >= 64 || !attr[dev]) {
+                cudaFuncSetAttribute(k_synthesize_rt_s<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+                if (dev >= 0 && dev < 64) attr[dev] = true;
+            }
+        }
+        if (dyn) k_synthesize_rt_s<true><<<strips_x * tx, 256, dyn, s>>>(P, uhat, tab, astar, tx, strip);
+        else k_synthesize_rt_s<false><<<strips_x * tx, 256, 0, s>>>(P, uhat, tab, astar, tx, strip);
         return;
     }
     const int64_t N = (int64_t)P.n * P.n;

@@ -72,7 +72,11 @@ struct CoarseRowEntry {
     double bxq;      // q f1
     double ty, uy;   // clamped y fraction and 1 - ty
     double hl;       // h l(x, a)
-    int cy, pad;     // y cell
+    double fbd;      // floor(q f1) (an integer): an unclamped foot's x cell is i + fbd or i + fbd + 1
+    int cy;          // y cell
+    int pk;          // interior fast path: low 16 bits = (cy - j) * CSW + floor(q f1) + 32768 (offset of
+                     // the stencil's corner 00 from the node in the staged tile); bits 16..19: one-hot,
+                     // the corner (00, 10, 01, 11) that is the node itself when the x cell is i + fbd
 };
 void launch_coarse_rowtab(const DProblem &P, CoarseRowEntry *tab, cudaStream_t s);
 // synthesis with the same row-invariant table built on the fine grid (bit-identical)
