@@ -170,3 +170,30 @@ def test_calls_out_of_order_and_bad_arguments():
         s.get_labels() if False else s.build_patches(4)   # no synthesis yet
     assert e.value.status == N.PDD_E_STATE
     s.close()
+
+
+def test_coarse_fast_path_rounded_foot_on_next_integer():
+    """The interior fast path of the coarse sweep (canonical.cu: canon_node_update_fast) takes the x
+    cell of a foot as i + floor(q f1) and sends the one exception -- rn(i + q f1) == i + floor(q f1)
+    + 1 -- to the generic code.  No config ever hits it, so this instance forces it: control 0 is
+    (1 - 2^-53, 0) with q = c = 1, d = 0, so for every i >= 1 the sum i + q f1 rounds to i + 1 while
+    floor(q f1) = 0.  u_c, the sweep count, u_hat and a* must still match the oracle bit for bit."""
+    inst = I.make_config("C4", n=2049)                    # coarse grid 129^2: 6 x 8 interior tiles
+    one = np.nextafter(1.0, 0.0)
+    for p in (inst, inst.coarse):
+        assert p.h / p.dx == 1.0 and p.speed.kind == 0 and p.speed.value == 1.0
+        p.controls = p.controls.copy()
+        p.controls[0] = (one, 0.0)
+    i = np.arange(inst.coarse.n, dtype=np.float64)
+    assert np.count_nonzero(i + one == i + 1.0) >= inst.coarse.n - 1      # the case is hit
+    ref = O.coarse_solve(inst)
+    from paper_1502_01629_b200 import Solver
+    s = Solver(inst, precision=32)
+    st = s.coarse_solve(inst.tol_coarse)
+    assert st["sweeps"] == ref["sweeps"]
+    uc = s.get_coarse_values()
+    assert np.array_equal(uc.view(np.uint64), ref["V"].view(np.uint64))
+    s.synthesize()
+    uref = O.prolong(inst.coarse.n, ref["V"], inst.n)
+    assert np.array_equal(s.get_uhat().view(np.uint64), uref.view(np.uint64))
+    assert np.array_equal(s.get_controls(), O.synthesize(inst, uref))
