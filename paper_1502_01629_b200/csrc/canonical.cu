@@ -79,7 +79,7 @@ __global__ void k_init_values(DProblem P, double *V)
 #define PDD_COARSE_RTSMEM 1   // ... and the tile's rows of the row-invariant table
 #endif
 #ifndef PDD_CANON_UNROLL
-#define PDD_CANON_UNROLL 1   // controls per loop trip in the staged coarse / synthesis kernels (A/B: profiles/r4a_*)
+#define PDD_CANON_UNROLL 2   // controls per loop trip in the staged coarse / synthesis kernels (A/B: profiles/r4_canon_ab.txt)
 #endif
 #ifndef PDD_CANON_MINB
 #define PDD_CANON_MINB 4     // __launch_bounds__ min blocks per SM of those kernels (A/B)
@@ -777,7 +777,7 @@ __global__ void k_synthesize_rt(DProblem P, const double *__restrict__ uhat,
 // k_synthesize_rt on 16 x 16 node tiles with u_hat's tile + halo (CH cells) staged in shared
 // memory: the 4 N_A gathers per node hit shared memory.  Same operations: bit-identical.
 #ifndef PDD_SYNTH_UNROLL
-#define PDD_SYNTH_UNROLL 1 // controls per loop trip of the strip kernel (A/B)
+#define PDD_SYNTH_UNROLL 4 // controls per loop trip of the strip kernel (A/B)
 #endif
 #ifndef PDD_SYNTH_STRIP
 #define PDD_SYNTH_STRIP 8  // tiles per CTA (one strip of a tile row)
