@@ -818,6 +818,28 @@ __global__ void __launch_bounds__(256, PDD_CANON_MINB) k_synthesize_rt_s(DProble
         if (P.kind[k] != 0) { astar[k] = 255; continue; }
         double best = INFINITY;
         int arg = -1;
+        if (tx * 16 >= CH && tx * 16 + 15 + CH <= n - 1) {
+            // interior tile: with reach <= CH - 1 no foot of its nodes is clamped in x (0 <= i + q f1 <=
+            // n - 1 and floor <= n - 2), so the three clamps below are dropped -- same bits, 2 FP64
+            // compares fewer per control on a kernel bound by the FP64 pipe (profiles/r4n_synth_*)
+            PDD_UNROLL_(PDD_SYNTH_UNROLL)
+            for (int a = 0; a < P.na; ++a) {
+                const CoarseRowEntry e = row[a];
+                const double gx = DADD((double)i, e.bxq);
+                const int cx = (int)floor(gx);
+                const double tx2 = DSUB(gx, (double)cx);
+                const double ux = DSUB(1.0, tx2);
+                const int s0 = (e.cy - jb) * CSW + (cx - ib);
+                double sm = DMUL(DMUL(ux, e.uy), sU[s0]);
+                sm = DADD(sm, DMUL(DMUL(tx2, e.uy), sU[s0 + 1]));
+                sm = DADD(sm, DMUL(DMUL(ux, e.ty), sU[s0 + CSW]));
+                sm = DADD(sm, DMUL(DMUL(tx2, e.ty), sU[s0 + CSW + 1]));
+                const double v = DADD(e.hl, DMUL(P.beta, sm));
+                if (v < best) { best = v; arg = a; }
+            }
+            astar[k] = (uint8_t)arg;
+            continue;
+        }
         PDD_UNROLL_(PDD_SYNTH_UNROLL)
         for (int a = 0; a < P.na; ++a) {
             const CoarseRowEntry e = row[a];
