@@ -14,8 +14,12 @@
 //                   P:473-491 with discount R3) + sup-norm residual; stops itself once the
 //                   previous sweep's residual is < tol (so the result does not depend on how
 //                   many sweeps the host enqueues)
+//                   (k_coarse_sweep_tiles: the same sweep on the 16 x 16 tiles whose neighbourhood
+//                   changed, tile + halo and the row-invariant table staged in shared memory; interior
+//                   tiles take canon_node_update_fast -- all bit-identical rewrites, see there)
 //   k_prolong       u_hat = bilinear(u_c) (R15)
 //   k_synthesize    a* = argmin_k [h l + beta u_hat(x + h f)] (R16)
+//                   (k_synthesize_rt_s: strips of 16 x 16 tiles with u_hat and the table staged)
 //   k_successor     nearest node to x + M f*/|f*| (R18)
 //   k_jump          pointer jumping s <- s[s]
 //   k_labels        label = sector[root] for target roots, orphan otherwise (R17)
